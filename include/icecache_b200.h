@@ -1,0 +1,179 @@
+/* icecache_b200.h -- C ABI of the B200-native IceCache decode hot path.
+ *
+ * The reference (arXiv 2604.10539, /root/reference/pkg/src/icecache) exposes
+ * this path as a Python/NumPy API; there is no FFI in the reference.  Each
+ * entry point below replaces the reference call named beside it, batched over
+ * T independent DCI trees (one per (sequence, layer, kv head)):
+ *
+ *   icb_build            dci_indexing                 dci.py:479-568
+ *   icb_query            DciTree.query + find_page_index + gqa_union
+ *                                                     dci.py:318-364, pagestore.py:111-113,
+ *                                                     attention.py:96-103, engine.py:436-447
+ *   icb_insert           DciTree.insert / _grow_top   dci.py:385-449
+ *   icb_alloc_resident_pages  TierStore.allocate_page (sink / window)
+ *                                                     pagestore.py:138-149, engine.py:263-276
+ *   icb_rotate_window    Engine._rotate_layer         engine.py:516-534
+ *   icb_append_window    window append                engine.py:426-429
+ *   icb_sparse_attention sparse_attention + TierStore.backload/evict_unselected
+ *                                                     attention.py:77-93, pagestore.py:169-215,
+ *                                                     engine.py:449-475
+ *   icb_dense_attention  full_attention (skip layers) attention.py:55-74, engine.py:418-422
+ *   icb_export_tree / icb_tree_info  host mirror for structure checks (DciTree fields,
+ *                                                     check_invariants dci.py:453-476)
+ *
+ * All array arguments marked "dev" are device pointers (plain CUDA memory);
+ * "host" arguments are host memory.  `stream` is a cudaStream_t (NULL = legacy
+ * default stream).  Every call returns ICB_OK or an error code; the message is
+ * available from icb_last_error().  Errors map to the reference exceptions
+ * (errors.py:8-40): ICB_E_INPUT -> InputError, ICB_E_CONFIG -> ConfigError,
+ * ICB_E_CONSISTENCY -> ConsistencyError, ICB_E_DEGENERATE -> DegenerateQueryError.
+ */
+#ifndef ICECACHE_B200_H
+#define ICECACHE_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ICB_OK 0
+#define ICB_E_INPUT 1
+#define ICB_E_CONFIG 2
+#define ICB_E_CONSISTENCY 3
+#define ICB_E_CUDA 4
+#define ICB_E_CAPACITY 5
+#define ICB_E_POLICY 6
+#define ICB_E_DEGENERATE 7
+
+#define ICB_KV_F32 0
+#define ICB_KV_BF16 1
+
+#define ICB_ROLE_SINK 1
+#define ICB_ROLE_WINDOW 2
+#define ICB_ROLE_INDEXED 3
+
+#define ICB_SENTINEL_LEVEL (-1)
+
+typedef struct icb_forest icb_forest;
+
+typedef struct {
+  int32_t n_trees;     /* T */
+  int32_t dim;         /* key dim d (<= 128) */
+  int32_t dim_v;       /* value dim d' (<= 128) */
+  int32_t page_size;   /* s (2..32) */
+  int32_t kv_dtype;    /* ICB_KV_F32 | ICB_KV_BF16: storage of page K/V */
+  int32_t tok_cap;     /* token ids must be < tok_cap (rows are indexed by token id) */
+  int32_t node_cap;    /* nodes per tree */
+  int32_t page_cap;    /* page ids per tree */
+  int32_t member_cap;  /* member-pool entries per tree */
+  int32_t own_cap;     /* owned-node list entries per tree */
+  int32_t dirs_cap;    /* cached P-DCI direction sets per tree */
+  double promotion_ratio; /* r */
+} icb_forest_config;
+
+const char *icb_last_error(void);
+int icb_version(void);
+
+int icb_forest_create(const icb_forest_config *cfg, icb_forest **out);
+int icb_forest_destroy(icb_forest *f);
+
+/* Seed each tree's level stream: SeedSequence(entropy words).spawn_key=(0,)
+ * (dci.py:180-183).  host: trees[n], words[n][stride], n_words[n]. */
+int icb_seed_trees(icb_forest *f, const int32_t *trees, int32_t n, const uint32_t *words,
+                   int32_t stride, const int32_t *n_words);
+
+/* Allocate `count` resident pinned pages of `role` per tree and fill them in
+ * token order with `n_tokens` entries (tokens dev [n][n_tokens], keys dev
+ * [n][n_tokens][dim], values dev [n][n_tokens][dim_v]).  Sink pages are
+ * recorded as the tree's sink list, window pages appended to its window ring. */
+int icb_alloc_resident_pages(icb_forest *f, const int32_t *trees, int32_t n, int32_t role,
+                             int32_t count, int32_t n_tokens, const int32_t *tokens,
+                             const float *keys, const float *values, void *stream);
+
+/* Batch build of n trees over n_points (token, key) pairs each.  trees dev[n];
+ * tokens dev [n][n_points]; keys dev [n][n_points][dim] fp32; values dev or
+ * NULL; scales dev [n] fp64 or NULL (derive KeyScale.from_keys). */
+int icb_build(icb_forest *f, const int32_t *trees, int32_t n, int32_t n_points,
+              const int32_t *tokens, const float *keys, const float *values,
+              const double *scales, void *stream);
+
+/* Multi-level search for G query heads per tree plus the GQA page union.
+ * queries dev [n][G][dim] raw queries (lifted in-kernel, geometry.py:89-98),
+ * or, with lifted_input=1, [n][G][dim+1] already-lifted vectors.
+ * out_ids dev [n][G][k_out] ranked by (d2, id); out_counts dev [n][G];
+ * out_pages dev [n][pages_cap] ascending unique page ids (may be NULL);
+ * out_npages dev [n].  distance/queries counters accumulate in the trees. */
+int icb_query(icb_forest *f, const int32_t *trees, int32_t n, int32_t G, const float *queries,
+              int32_t lifted_input, int32_t k, int64_t beam, int64_t visit_cap,
+              int32_t target_level, int32_t *out_ids, int32_t k_out, int32_t *out_counts,
+              int32_t *out_pages, int32_t pages_cap, int32_t *out_npages, void *stream);
+
+/* Sequential inserts of m points per tree (trees in parallel).  levels dev
+ * [n][m] or NULL (draw from the tree's stream); out_levels dev or NULL. */
+int icb_insert(icb_forest *f, const int32_t *trees, int32_t n, int32_t m, const int32_t *tokens,
+               const float *keys, const float *values, const int32_t *levels,
+               int32_t *out_levels, void *stream);
+
+/* Engine._rotate_layer: offload the oldest window page, insert its entries,
+ * release it, allocate a fresh window page.  stats dev [n][2] += (bytes, 1). */
+int icb_rotate_window(icb_forest *f, const int32_t *trees, int32_t n, int32_t scalar_bytes,
+                      int64_t *stats, void *stream);
+
+/* Append one token to the first non-full window page of each tree.
+ * keys dev [n][dim], values dev [n][dim_v]. */
+int icb_append_window(icb_forest *f, const int32_t *trees, int32_t n, int32_t token,
+                      const float *keys, const float *values, void *stream);
+
+/* Sparse attention of G query heads per tree over sink, window and the
+ * selected pages (pages dev [n][pages_cap], npages dev [n]); out dev
+ * [n][G][dim_v] fp32.  stats dev [n][5] (accumulated): pages_selected,
+ * tokens_loaded, pages_loaded, bytes_moved, transactions.  Residency
+ * (hot = selected U pinned) is updated per tree.  splits: split-K factor
+ * (0 = auto). */
+int icb_sparse_attention(icb_forest *f, const int32_t *trees, int32_t n, int32_t G,
+                         const float *queries, const int32_t *pages, int32_t pages_cap,
+                         const int32_t *npages, float *out, int64_t *stats,
+                         int32_t scalar_bytes, int32_t splits, void *stream);
+
+/* Dense decode attention (skip layers / fallback): n heads-groups, G query
+ * heads each, over n_tokens contiguous K/V rows.  k, v dev [n][ld][dim]
+ * (kv_dtype), q dev [n][G][dim], out dev [n][G][dim_v]. */
+int icb_dense_attention(int32_t n, int32_t G, int32_t dim, int32_t dim_v, int32_t kv_dtype,
+                        const float *q, const void *k, const void *v, int64_t ld,
+                        int32_t n_tokens, float *out, int32_t splits, void *stream);
+
+/* Per-tree summary (host out[16]): levels, top_node, n_nodes, next_page,
+ * n_points, err, n_window, n_sink, query_count, distance_evals, scale_clamps,
+ * member_top, own_top, n_dirs, 0, 0.  Synchronizes the device. */
+int icb_tree_info(icb_forest *f, int32_t tree, int64_t *out);
+
+/* Copy one tree's arrays to host buffers (any may be NULL).  Sizes: node
+ * arrays node_cap, members member_cap, page arrays page_cap (page_tok
+ * page_cap*s), token arrays tok_cap, own_list own_cap.  win/sink: 8 each. */
+int icb_export_tree(icb_forest *f, int32_t tree, int32_t *node_level, int32_t *node_parent,
+                    int32_t *node_owner, int32_t *node_off, int32_t *node_size,
+                    int32_t *node_lastpage, int32_t *members, int32_t *page_fill,
+                    int8_t *page_role, int32_t *page_tok, int32_t *tok2page, int8_t *level,
+                    int32_t *own_base, int32_t *own_list, float *lift, float *tail,
+                    int32_t *win, int32_t *sink);
+
+/* Read page K/V back (host float, converted from the storage dtype):
+ * keys [count][s][dim], values [count][s][dim_v] for page ids pages[count]. */
+int icb_read_pages(icb_forest *f, int32_t tree, const int32_t *pages, int32_t count, float *keys,
+                   float *values);
+
+/* Sticky device error bits of every tree (host out[n_trees]); clear=1 resets
+ * them.  Synchronizes the device. */
+int icb_errors(icb_forest *f, int32_t *out, int32_t clear);
+/* Clear a tree's sticky device error bits (after the host reported them). */
+int icb_clear_errors(icb_forest *f, int32_t tree);
+/* KeyScale.c of a built tree (host out). */
+int icb_read_meta_c(icb_forest *f, int32_t tree, double *c);
+/* Host-side restatement check: n PCG64 doubles of SeedSequence(words, spawn). */
+int icb_host_pcg_doubles(const uint32_t *words, int32_t n_words, const uint32_t *spawn,
+                         int32_t n_spawn, int32_t n, double *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

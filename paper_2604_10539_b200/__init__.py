@@ -1,0 +1,13 @@
+"""B200-native IceCache decode hot path (arXiv 2604.10539).
+
+Drop-in for the reference package's cache/index API on the decode path:
+DCI-tree build and insert, query-aware top-k page selection, page union and
+sparse paged attention run as sm_100a kernels behind a C ABI
+(include/icecache_b200.h); this package is the Python host side.
+"""
+
+from .errors import (ConfigError, ConsistencyError, DegenerateQueryError, IceCacheError, InputError,
+                     InvariantViolation, PolicyError, ScaleViolationError)
+from .forest import DeviceForest, ForestCaps, dense_attention, entropy_words
+
+__version__ = "0.1.0"

@@ -1,0 +1,305 @@
+// Decode attention over pages: sparse_attention (attention.py:77-93) over
+// sink U window U selected pages in the reference's entry order
+// (engine.py:449-475), and dense full_attention for skip layers
+// (attention.py:55-74, engine.py:418-422).
+//
+// Memory-bound: every K/V row is read once with 8/16-byte vector loads (one
+// warp per page, lane l owns dims 4l..4l+3), the G query heads of a GQA group
+// share each row (G logits per row), softmax is online in fp32, split-K
+// partials (m, l, acc) are combined by the last CTA of each tree.
+#include "icb.cuh"
+#include "internal.h"
+
+namespace icb {
+
+constexpr int kAttnThreads = 256;
+
+template <typename KT>
+__device__ __forceinline__ float4 load4(const KT* p);
+template <>
+__device__ __forceinline__ float4 load4<float>(const float* p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
+}
+template <>
+__device__ __forceinline__ float4 load4<__nv_bfloat16>(const __nv_bfloat16* p) {
+  uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+  float2 a = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.x));
+  float2 b = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
+struct AttnArgs {
+  int n, G, dim, dim_v, splits;
+  const int32_t* trees;        // paged mode
+  const float* q;              // [n][G][dim]
+  const int32_t* pages;        // [n][pages_cap]
+  int pages_cap;
+  const int32_t* npages;
+  // dense mode
+  const void* k;
+  const void* v;
+  long long ld;
+  int n_tokens;
+  float* out;                  // [n][G][dim_v]
+  float* part;                 // [n][splits][G][2 + dim_v]
+  unsigned* counter;           // [n]
+  int64_t* stats;              // [n][5]
+  int scalar_bytes;
+  float scale_log2;            // log2(e) / sqrt(dim)
+};
+
+struct HeadAcc {
+  float m, l;
+  float4 acc;
+};
+
+template <typename KT, int G>
+__device__ __forceinline__ void attend_row(HeadAcc (&h)[G], const float4 (&qv)[G], const KT* krow, const KT* vrow,
+                                           int lane, int dim, int dim_v, float scale_log2) {
+  float4 k = lane * 4 < dim ? load4<KT>(krow + lane * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 v = lane * 4 < dim_v ? load4<KT>(vrow + lane * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  float s[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) s[g] = qv[g].x * k.x + qv[g].y * k.y + qv[g].z * k.z + qv[g].w * k.w;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int g = 0; g < G; ++g) s[g] += __shfl_xor_sync(0xffffffffu, s[g], o);
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    float x = s[g] * scale_log2;
+    float mn = fmaxf(h[g].m, x);
+    float a = exp2f(h[g].m - mn), p = exp2f(x - mn);
+    h[g].l = h[g].l * a + p;
+    h[g].acc.x = h[g].acc.x * a + p * v.x;
+    h[g].acc.y = h[g].acc.y * a + p * v.y;
+    h[g].acc.z = h[g].acc.z * a + p * v.z;
+    h[g].acc.w = h[g].acc.w * a + p * v.w;
+    h[g].m = mn;
+  }
+}
+
+// Block = (tree b, split sp).  PAGED: rows come from the tree's sink, window
+// and selected pages; DENSE: rows [0, n_tokens) of k/v[b].
+template <typename KT, int G, bool PAGED>
+__global__ void __launch_bounds__(kAttnThreads) attn_kernel(ForestView F, AttnArgs A) {
+  const int b = blockIdx.x, sp = blockIdx.y, S = A.splits;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = kAttnThreads / 32;
+  __shared__ int s_pages[1024];
+  __shared__ int s_np;
+  __shared__ float s_red[kAttnThreads / 32][G][2];
+  __shared__ float4 s_acc[kAttnThreads / 32][G][32];
+  __shared__ bool s_last;
+  const int t = PAGED ? A.trees[b] : 0;
+  float4 qv[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const float* q = A.q + ((size_t)b * G + g) * A.dim;
+    const int j = lane * 4;
+    qv[g] = make_float4(j < A.dim ? q[j] : 0.f, j + 1 < A.dim ? q[j + 1] : 0.f, j + 2 < A.dim ? q[j + 2] : 0.f,
+                        j + 3 < A.dim ? q[j + 3] : 0.f);
+  }
+  HeadAcc h[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) { h[g].m = -INFINITY; h[g].l = 0.f; h[g].acc = make_float4(0.f, 0.f, 0.f, 0.f); }
+
+  if (PAGED) {
+    // page list: sink, window, selected (entry order of engine.py:457-461)
+    const TreeMeta* m = F.meta + t;
+    const int nsel = A.npages[b];
+    const int nfix = m->n_sink + m->n_window;
+    const int total = nfix + nsel;
+    const int p0 = (int)((long long)total * sp / S), p1 = (int)((long long)total * (sp + 1) / S);
+    if (threadIdx.x == 0) s_np = min(p1 - p0, 1024);
+    for (int i = threadIdx.x; i < p1 - p0 && i < 1024; i += kAttnThreads) {
+      int gi = p0 + i;
+      int p;
+      if (gi < m->n_sink) p = m->sink[gi];
+      else if (gi < nfix) p = m->win[gi - m->n_sink];
+      else p = A.pages[(size_t)b * A.pages_cap + gi - nfix];
+      s_pages[i] = p;
+    }
+    __syncthreads();
+    const KT* K = (const KT*)F.page_k;
+    const KT* V = (const KT*)F.page_v;
+    for (int i = warp; i < s_np; i += NW) {
+      const int p = s_pages[i];
+      const int fill = F.page_fill[F.pg(t, p)];
+      const size_t base = F.pg(t, p) * F.s;
+      for (int r = 0; r < fill; ++r)
+        attend_row<KT, G>(h, qv, K + (base + r) * F.dkp, V + (base + r) * F.dvp, lane, A.dim, A.dim_v,
+                          A.scale_log2);
+    }
+    // residency accounting (pagestore.py:169-215) by split 0
+    if (sp == 0 && A.stats) {
+      __shared__ int s_fill_sel, s_loaded, s_fill_loaded;
+      if (threadIdx.x == 0) { s_fill_sel = 0; s_loaded = 0; s_fill_loaded = 0; }
+      __syncthreads();
+      uint32_t* bits = F.prev_sel + (size_t)t * F.pwords();
+      int fs = 0, ld = 0, fl = 0;
+      for (int i = threadIdx.x; i < nsel; i += kAttnThreads) {
+        int p = A.pages[(size_t)b * A.pages_cap + i];
+        int f = F.page_fill[F.pg(t, p)];
+        fs += f;
+        if (!((bits[p >> 5] >> (p & 31)) & 1u)) { ld += 1; fl += f; }
+      }
+      atomicAdd(&s_fill_sel, fs);
+      atomicAdd(&s_loaded, ld);
+      atomicAdd(&s_fill_loaded, fl);
+      __syncthreads();
+      for (int w = threadIdx.x; w < F.pwords(); w += kAttnThreads) bits[w] = 0u;
+      __syncthreads();
+      for (int i = threadIdx.x; i < nsel; i += kAttnThreads) {
+        int p = A.pages[(size_t)b * A.pages_cap + i];
+        atomicOr(bits + (p >> 5), 1u << (p & 31));
+      }
+      if (threadIdx.x == 0) {
+        int64_t* st = A.stats + (size_t)b * 5;
+        st[0] += nsel;
+        st[1] += s_fill_sel;
+        st[2] += s_loaded;
+        st[3] += (int64_t)s_fill_loaded * (A.dim + A.dim_v) * A.scalar_bytes;
+        st[4] += s_loaded > 0 ? 1 : 0;
+      }
+    }
+  } else {
+    const KT* K = (const KT*)A.k + (size_t)b * A.ld * A.dim;
+    const KT* V = (const KT*)A.v + (size_t)b * A.ld * A.dim_v;
+    const int r0 = (int)((long long)A.n_tokens * sp / S), r1 = (int)((long long)A.n_tokens * (sp + 1) / S);
+    const int CH = 4;
+    for (int r = r0 + warp * CH; r < r1; r += NW * CH) {
+#pragma unroll
+      for (int u = 0; u < CH; ++u)
+        if (r + u < r1)
+          attend_row<KT, G>(h, qv, K + (size_t)(r + u) * A.dim, V + (size_t)(r + u) * A.dim_v, lane, A.dim,
+                            A.dim_v, A.scale_log2);
+    }
+  }
+  // combine warps
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    if (lane == 0) { s_red[warp][g][0] = h[g].m; s_red[warp][g][1] = h[g].l; }
+    s_acc[warp][g][lane] = h[g].acc;
+  }
+  __syncthreads();
+  float* part = A.part + ((size_t)b * S + sp) * G * (2 + A.dim_v);
+  for (int x = threadIdx.x; x < G * 32; x += kAttnThreads) {
+    int g = x / 32, ln = x % 32;
+    float mx = -INFINITY;
+    for (int w = 0; w < NW; ++w) mx = fmaxf(mx, s_red[w][g][0]);
+    float l = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int w = 0; w < NW; ++w) {
+      float sc = s_red[w][g][0] == -INFINITY ? 0.f : exp2f(s_red[w][g][0] - mx);
+      l += s_red[w][g][1] * sc;
+      float4 a = s_acc[w][g][ln];
+      acc.x += a.x * sc; acc.y += a.y * sc; acc.z += a.z * sc; acc.w += a.w * sc;
+    }
+    float* pg = part + (size_t)g * (2 + A.dim_v);
+    if (ln == 0) { pg[0] = mx; pg[1] = l; }
+    if (ln * 4 < A.dim_v) { pg[2 + ln * 4] = acc.x; pg[3 + ln * 4] = acc.y; pg[4 + ln * 4] = acc.z; pg[5 + ln * 4] = acc.w; }
+  }
+  // last CTA of this tree combines the splits
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned prev = atomicAdd(A.counter + b, 1u);
+    s_last = (prev == (unsigned)(S - 1));
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const float* pb = A.part + (size_t)b * S * G * (2 + A.dim_v);
+  for (int x = threadIdx.x; x < G * A.dim_v; x += kAttnThreads) {
+    int g = x / A.dim_v, j = x % A.dim_v;
+    float mx = -INFINITY;
+    for (int s = 0; s < S; ++s) mx = fmaxf(mx, __ldcg(pb + ((size_t)s * G + g) * (2 + A.dim_v)));
+    float l = 0.f, acc = 0.f;
+    for (int s = 0; s < S; ++s) {
+      const float* pg = pb + ((size_t)s * G + g) * (2 + A.dim_v);
+      float ms = __ldcg(pg);
+      float sc = ms == -INFINITY ? 0.f : exp2f(ms - mx);
+      l += __ldcg(pg + 1) * sc;
+      acc += __ldcg(pg + 2 + j) * sc;
+    }
+    A.out[((size_t)b * G + g) * A.dim_v + j] = acc / l;
+  }
+  if (threadIdx.x == 0) A.counter[b] = 0;   // ready for the next launch
+}
+
+template <typename KT, bool PAGED>
+void launch_attn(int G, dim3 grid, cudaStream_t st, const ForestView& F, const AttnArgs& A) {
+  switch (G) {
+    case 1: attn_kernel<KT, 1, PAGED><<<grid, kAttnThreads, 0, st>>>(F, A); break;
+    case 2: attn_kernel<KT, 2, PAGED><<<grid, kAttnThreads, 0, st>>>(F, A); break;
+    case 4: attn_kernel<KT, 4, PAGED><<<grid, kAttnThreads, 0, st>>>(F, A); break;
+    case 8: attn_kernel<KT, 8, PAGED><<<grid, kAttnThreads, 0, st>>>(F, A); break;
+    default: break;
+  }
+}
+
+}  // namespace icb
+
+using namespace icb;
+
+static int ensure_attn_scratch(icb_forest* f, size_t part_floats, int n, float** part, unsigned** counter) {
+  static thread_local void* dense_buf = nullptr;
+  static thread_local size_t dense_bytes = 0;
+  void** buf = f ? &f->ascratch : &dense_buf;
+  size_t* bytes = f ? &f->ascratch_bytes : &dense_bytes;
+  size_t need = part_floats * 4 + 256 + (size_t)n * 4;
+  if (need > *bytes) {
+    if (*buf) ICB_CUDA(cudaFree(*buf));
+    *buf = nullptr;
+    *bytes = 0;
+    ICB_CUDA(cudaMalloc(buf, need));
+    ICB_CUDA(cudaMemset(*buf, 0, need));
+    *bytes = need;
+  }
+  *counter = (unsigned*)*buf;
+  *part = (float*)((char*)*buf + (((size_t)n * 4 + 255) & ~(size_t)255));
+  return ICB_OK;
+}
+
+static bool valid_g(int G) { return G == 1 || G == 2 || G == 4 || G == 8; }
+
+int icb_attention_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, const float* queries,
+                       const int32_t* pages, int32_t pages_cap, const int32_t* npages, float* out,
+                       int64_t* stats, int32_t scalar_bytes, int32_t splits, cudaStream_t st) {
+  if (n <= 0) return ICB_OK;
+  if (!valid_g(G)) { icb_set_error(ICB_E_CONFIG, "attention supports G in {1,2,4,8}"); return ICB_E_CONFIG; }
+  const auto& c = f->cfg;
+  if (splits <= 0) splits = std::max(1, std::min(8, (2 * 148 + n - 1) / n));
+  AttnArgs A{};
+  A.n = n; A.G = G; A.dim = c.dim; A.dim_v = c.dim_v; A.splits = splits; A.trees = trees; A.q = queries;
+  A.pages = pages; A.pages_cap = pages_cap; A.npages = npages; A.out = out; A.stats = stats;
+  A.scalar_bytes = scalar_bytes;
+  A.scale_log2 = (float)(1.4426950408889634 / sqrt((double)c.dim));
+  int rc = ensure_attn_scratch(f, (size_t)n * splits * G * (2 + c.dim_v), n, &A.part, &A.counter);
+  if (rc) return rc;
+  dim3 grid(n, splits);
+  if (c.kv_dtype == ICB_KV_BF16) launch_attn<__nv_bfloat16, true>(G, grid, st, f->view, A);
+  else launch_attn<float, true>(G, grid, st, f->view, A);
+  ICB_CUDA(cudaGetLastError());
+  return ICB_OK;
+}
+
+int icb_dense_attention_impl(int32_t n, int32_t G, int32_t dim, int32_t dim_v, int32_t kv_dtype, const float* q,
+                             const void* k, const void* v, int64_t ld, int32_t n_tokens, float* out,
+                             int32_t splits, cudaStream_t st) {
+  if (n <= 0) return ICB_OK;
+  if (!valid_g(G)) { icb_set_error(ICB_E_CONFIG, "attention supports G in {1,2,4,8}"); return ICB_E_CONFIG; }
+  if (splits <= 0) splits = std::max(1, std::min((n_tokens + 255) / 256, (4 * 148 + n - 1) / n));
+  AttnArgs A{};
+  A.n = n; A.G = G; A.dim = dim; A.dim_v = dim_v; A.splits = splits; A.q = q; A.k = k; A.v = v; A.ld = ld;
+  A.n_tokens = n_tokens; A.out = out;
+  A.scale_log2 = (float)(1.4426950408889634 / sqrt((double)dim));
+  int rc = ensure_attn_scratch(nullptr, (size_t)n * splits * G * (2 + dim_v), n, &A.part, &A.counter);
+  if (rc) return rc;
+  ForestView F{};
+  dim3 grid(n, splits);
+  if (kv_dtype == ICB_KV_BF16) launch_attn<__nv_bfloat16, false>(G, grid, st, F, A);
+  else launch_attn<float, false>(G, grid, st, F, A);
+  ICB_CUDA(cudaGetLastError());
+  return ICB_OK;
+}

@@ -1,0 +1,357 @@
+// Forest arena (HBM) and the C ABI entry points (include/icecache_b200.h).
+#include "icb.cuh"
+#include "internal.h"
+#include <cstring>
+#include <mutex>
+
+static thread_local std::string g_last_error;
+static thread_local int g_last_code = 0;
+
+void icb_set_error(int code, const std::string& msg) {
+  g_last_code = code;
+  g_last_error = msg;
+}
+
+namespace icb {
+
+__global__ void zero_nodes_kernel(ForestView F, const int32_t* trees, int n) {
+  int b = blockIdx.y;
+  int t = trees[b];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < F.node_cap; i += gridDim.x * blockDim.x)
+    F.node_size[F.nd(t, i)] = 0;
+}
+
+__global__ void seed_kernel(ForestView F, int t, Pcg64 g, int n_words, uint32_t w0, uint32_t w1, uint32_t w2,
+                            uint32_t w3, uint32_t w4, uint32_t w5, uint32_t w6, uint32_t w7) {
+  TreeMeta* m = F.meta + t;
+  m->rng = g;
+  m->n_entropy = n_words;
+  uint32_t w[8] = {w0, w1, w2, w3, w4, w5, w6, w7};
+  for (int i = 0; i < 8; ++i) m->entropy[i] = w[i];
+}
+
+}  // namespace icb
+
+using namespace icb;
+
+void zero_node_sizes(icb_forest* f, const int32_t* trees, int n, cudaStream_t st) {
+  dim3 grid((f->cfg.node_cap + 255) / 256, n);
+  zero_nodes_kernel<<<grid, 256, 0, st>>>(f->view, trees, n);
+}
+
+static cudaStream_t S_(void* s) { return (cudaStream_t)s; }
+
+#define ICB_TRY(expr)            \
+  do {                           \
+    int _rc = (expr);            \
+    if (_rc != ICB_OK) return _rc; \
+  } while (0)
+
+template <typename T>
+static int falloc(icb_forest* f, T** p, size_t n, int fill_byte) {
+  void* q = nullptr;
+  size_t bytes = std::max<size_t>(n * sizeof(T), 16);
+  cudaError_t e = cudaMalloc(&q, bytes);
+  if (e != cudaSuccess) {
+    icb_set_error(ICB_E_CUDA, std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+    return ICB_E_CUDA;
+  }
+  e = cudaMemset(q, fill_byte, bytes);
+  if (e != cudaSuccess) {
+    icb_set_error(ICB_E_CUDA, cudaGetErrorString(e));
+    return ICB_E_CUDA;
+  }
+  f->allocs.push_back(q);
+  *p = (T*)q;
+  return ICB_OK;
+}
+
+extern "C" {
+
+const char* icb_last_error(void) { return g_last_error.c_str(); }
+int icb_version(void) { return 1; }
+
+int icb_forest_create(const icb_forest_config* cfg, icb_forest** out) {
+  if (!cfg || !out) { icb_set_error(ICB_E_INPUT, "null argument"); return ICB_E_INPUT; }
+  const auto& c = *cfg;
+  if (c.n_trees < 1 || c.dim < 1 || c.dim > ICB_DPAD || c.dim_v < 1 || c.dim_v > ICB_DPAD) {
+    icb_set_error(ICB_E_CONFIG, "dims must be in [1, 128] and n_trees >= 1");
+    return ICB_E_CONFIG;
+  }
+  if (c.page_size < 2 || c.page_size > 64) { icb_set_error(ICB_E_CONFIG, "page_size must be in [2, 64]"); return ICB_E_CONFIG; }
+  if (!(c.promotion_ratio > 0.0 && c.promotion_ratio < 1.0)) {
+    icb_set_error(ICB_E_CONFIG, "promotion ratio must lie in (0, 1)");
+    return ICB_E_CONFIG;
+  }
+  if (c.tok_cap < 1 || c.node_cap < 1 || c.page_cap < 1 || c.member_cap < 1 || c.own_cap < 1) {
+    icb_set_error(ICB_E_CONFIG, "capacities must be positive");
+    return ICB_E_CONFIG;
+  }
+  icb_forest* f = new icb_forest();
+  f->cfg = c;
+  ForestView& F = f->view;
+  F.T = c.n_trees; F.dim = c.dim; F.dim_v = c.dim_v; F.s = c.page_size; F.kv_bf16 = c.kv_dtype == ICB_KV_BF16;
+  F.dkp = (c.dim + 3) & ~3; F.dvp = (c.dim_v + 3) & ~3;
+  F.tok_cap = c.tok_cap; F.node_cap = c.node_cap; F.page_cap = c.page_cap; F.member_cap = c.member_cap;
+  F.own_cap = c.own_cap; F.dirs_cap = std::max(1, c.dirs_cap); F.r = c.promotion_ratio;
+  const size_t T = c.n_trees;
+  const size_t kvb = F.kv_bf16 ? 2 : 4;
+  int rc = ICB_OK;
+#define AL(ptr, n, fb) if (rc == ICB_OK) rc = falloc(f, &ptr, n, fb)
+  AL(F.meta, T, 0);
+  AL(F.lift, T * c.tok_cap * ICB_DPAD, 0);
+  AL(F.tail, T * c.tok_cap, 0);
+  AL(F.level, T * c.tok_cap, 0);
+  AL(F.own_base, T * c.tok_cap, 0);
+  AL(F.tok2page, T * c.tok_cap, 0xff);
+  AL(F.own_list, T * c.own_cap, 0);
+  AL(F.node_level, T * c.node_cap, 0);
+  AL(F.node_parent, T * c.node_cap, 0);
+  AL(F.node_owner, T * c.node_cap, 0);
+  AL(F.node_off, T * c.node_cap, 0);
+  AL(F.node_size, T * c.node_cap, 0);
+  AL(F.node_capm, T * c.node_cap, 0);
+  AL(F.node_lastpage, T * c.node_cap, 0xff);
+  AL(F.node_dirs, T * c.node_cap, 0xff);
+  AL(F.members, T * c.member_cap, 0);
+  AL(F.page_fill, T * c.page_cap, 0);
+  AL(F.page_role, T * c.page_cap, 0);
+  AL(F.page_tok, T * c.page_cap * c.page_size, 0xff);
+  AL(F.dirs, T * F.dirs_cap * ICB_NPROJ * (c.dim + 1), 0);
+  AL(F.prev_sel, T * (c.page_cap / 32 + 1), 0);
+#undef AL
+  if (rc == ICB_OK) {
+    char* pk = nullptr;
+    char* pv = nullptr;
+    rc = falloc(f, &pk, T * c.page_cap * c.page_size * F.dkp * kvb, 0);
+    if (rc == ICB_OK) rc = falloc(f, &pv, T * c.page_cap * c.page_size * F.dvp * kvb, 0);
+    F.page_k = pk;
+    F.page_v = pv;
+  }
+  if (rc != ICB_OK) {
+    icb_forest_destroy(f);
+    return rc;
+  }
+  *out = f;
+  return ICB_OK;
+}
+
+int icb_forest_destroy(icb_forest* f) {
+  if (!f) return ICB_OK;
+  cudaDeviceSynchronize();
+  for (void* p : f->allocs) cudaFree(p);
+  if (f->qscratch) cudaFree(f->qscratch);
+  if (f->iscratch) cudaFree(f->iscratch);
+  if (f->ascratch) cudaFree(f->ascratch);
+  delete f;
+  return ICB_OK;
+}
+
+int icb_seed_trees(icb_forest* f, const int32_t* trees, int32_t n, const uint32_t* words, int32_t stride,
+                   const int32_t* n_words) {
+  for (int i = 0; i < n; ++i) {
+    int t = trees[i];
+    if (t < 0 || t >= f->cfg.n_trees) { icb_set_error(ICB_E_INPUT, "tree index out of range"); return ICB_E_INPUT; }
+    int nw = n_words[i];
+    if (nw < 1 || nw > 8) { icb_set_error(ICB_E_INPUT, "1..8 entropy words supported"); return ICB_E_INPUT; }
+    uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int j = 0; j < nw; ++j) w[j] = words[(size_t)i * stride + j];
+    uint32_t spawn0 = 0;
+    uint64_t st[4];
+    icb_seedseq_u64x4(w, nw, &spawn0, 1, st);
+    Pcg64 g = icb_pcg_seed(st);
+    seed_kernel<<<1, 1>>>(f->view, t, g, nw, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7]);
+  }
+  ICB_CUDA(cudaGetLastError());
+  ICB_CUDA(cudaDeviceSynchronize());
+  return ICB_OK;
+}
+
+int icb_alloc_resident_pages(icb_forest* f, const int32_t* trees, int32_t n, int32_t role, int32_t count,
+                             int32_t n_tokens, const int32_t* tokens, const float* keys, const float* values,
+                             void* stream) {
+  if (role != ICB_ROLE_SINK && role != ICB_ROLE_WINDOW) {
+    icb_set_error(ICB_E_INPUT, "resident pages are sink or window pages");
+    return ICB_E_INPUT;
+  }
+  if (n_tokens > count * f->cfg.page_size) {
+    icb_set_error(ICB_E_INPUT, "more tokens than resident page slots");
+    return ICB_E_INPUT;
+  }
+  return icb_resident_impl(f, trees, n, role, count, n_tokens, tokens, keys, values, S_(stream));
+}
+
+int icb_build(icb_forest* f, const int32_t* trees, int32_t n, int32_t n_points, const int32_t* tokens,
+              const float* keys, const float* values, const double* scales, void* stream) {
+  if (n_points < 1) { icb_set_error(ICB_E_INPUT, "cannot index an empty key set"); return ICB_E_INPUT; }
+  if ((long long)n_points >= (1ll << 23)) { icb_set_error(ICB_E_CONFIG, "at most 2^23 points per build"); return ICB_E_CONFIG; }
+  if (n >= 4096) { icb_set_error(ICB_E_CONFIG, "at most 4095 trees per build call"); return ICB_E_CONFIG; }
+  return icb_build_impl(f, trees, n, n_points, tokens, keys, values, scales, S_(stream));
+}
+
+int icb_query(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, const float* queries, int32_t lifted_input,
+              int32_t k, int64_t beam, int64_t visit_cap, int32_t target_level, int32_t* out_ids, int32_t k_out,
+              int32_t* out_counts, int32_t* out_pages, int32_t pages_cap, int32_t* out_npages, void* stream) {
+  if (k < 1) { icb_set_error(ICB_E_INPUT, "k must be >= 1"); return ICB_E_INPUT; }
+  if (beam < k || visit_cap < k) { icb_set_error(ICB_E_CONFIG, "beam and visit_cap must be >= k"); return ICB_E_CONFIG; }
+  if (target_level != ICB_SENTINEL_LEVEL && target_level < 1) {
+    icb_set_error(ICB_E_INPUT, "target level must be -1 or >= 1");
+    return ICB_E_INPUT;
+  }
+  return icb_query_impl(f, trees, n, G, queries, lifted_input, k, beam, visit_cap, target_level, out_ids, k_out,
+                        out_counts, out_pages, pages_cap, out_npages, S_(stream));
+}
+
+int icb_insert(icb_forest* f, const int32_t* trees, int32_t n, int32_t m, const int32_t* tokens, const float* keys,
+               const float* values, const int32_t* levels, int32_t* out_levels, void* stream) {
+  return icb_insert_impl(f, trees, n, m, tokens, keys, values, levels, out_levels, 0, 4, nullptr, S_(stream));
+}
+
+int icb_rotate_window(icb_forest* f, const int32_t* trees, int32_t n, int32_t scalar_bytes, int64_t* stats,
+                      void* stream) {
+  return icb_insert_impl(f, trees, n, 0, nullptr, nullptr, nullptr, nullptr, nullptr, 1, scalar_bytes, stats,
+                         S_(stream));
+}
+
+int icb_append_window(icb_forest* f, const int32_t* trees, int32_t n, int32_t token, const float* keys,
+                      const float* values, void* stream) {
+  return icb_append_impl(f, trees, n, token, keys, values, S_(stream));
+}
+
+int icb_sparse_attention(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, const float* queries,
+                         const int32_t* pages, int32_t pages_cap, const int32_t* npages, float* out, int64_t* stats,
+                         int32_t scalar_bytes, int32_t splits, void* stream) {
+  int min_splits = (pages_cap + ICB_MAX_SINK + ICB_MAX_WINDOW + 1023) / 1024;
+  if (splits > 0 && splits < min_splits) splits = min_splits;
+  if (splits <= 0) splits = -min_splits;   // auto, at least min_splits
+  if (splits < 0) {
+    int auto_s = std::max(1, std::min(8, (2 * 148 + n - 1) / std::max(n, 1)));
+    splits = std::max(auto_s, -splits);
+  }
+  return icb_attention_impl(f, trees, n, G, queries, pages, pages_cap, npages, out, stats, scalar_bytes, splits,
+                            S_(stream));
+}
+
+int icb_dense_attention(int32_t n, int32_t G, int32_t dim, int32_t dim_v, int32_t kv_dtype, const float* q,
+                        const void* k, const void* v, int64_t ld, int32_t n_tokens, float* out, int32_t splits,
+                        void* stream) {
+  if (dim % 4 || dim_v % 4) { icb_set_error(ICB_E_CONFIG, "dense attention needs dims divisible by 4"); return ICB_E_CONFIG; }
+  if (n_tokens < 1) { icb_set_error(ICB_E_INPUT, "empty key set"); return ICB_E_INPUT; }
+  return icb_dense_attention_impl(n, G, dim, dim_v, kv_dtype, q, k, v, ld, n_tokens, out, splits, S_(stream));
+}
+
+int icb_tree_info(icb_forest* f, int32_t tree, int64_t* out) {
+  if (tree < 0 || tree >= f->cfg.n_trees) { icb_set_error(ICB_E_INPUT, "tree index out of range"); return ICB_E_INPUT; }
+  TreeMeta m;
+  ICB_CUDA(cudaDeviceSynchronize());
+  ICB_CUDA(cudaMemcpy(&m, f->view.meta + tree, sizeof(TreeMeta), cudaMemcpyDeviceToHost));
+  int64_t v[16] = {m.levels, m.top_node, m.n_nodes, m.next_page, m.n_points, m.err, m.n_window, m.n_sink,
+                   (int64_t)m.query_count, (int64_t)m.distance_evals, (int64_t)m.scale_clamps, m.member_top,
+                   m.own_top, m.n_dirs, 0, 0};
+  std::memcpy(out, v, sizeof(v));
+  return ICB_OK;
+}
+
+int icb_errors(icb_forest* f, int32_t* out, int32_t clear) {
+  const int T = f->cfg.n_trees;
+  std::vector<TreeMeta> m(T);
+  ICB_CUDA(cudaDeviceSynchronize());
+  ICB_CUDA(cudaMemcpy(m.data(), f->view.meta, sizeof(TreeMeta) * T, cudaMemcpyDeviceToHost));
+  for (int t = 0; t < T; ++t) {
+    out[t] = m[t].err;
+    if (clear && m[t].err) {
+      int zero = 0;
+      ICB_CUDA(cudaMemcpy((char*)(f->view.meta + t) + offsetof(TreeMeta, err), &zero, sizeof(int),
+                          cudaMemcpyHostToDevice));
+    }
+  }
+  return ICB_OK;
+}
+
+int icb_clear_errors(icb_forest* f, int32_t tree) {
+  int zero = 0;
+  ICB_CUDA(cudaMemcpy((char*)(f->view.meta + tree) + offsetof(TreeMeta, err), &zero, sizeof(int),
+                      cudaMemcpyHostToDevice));
+  return ICB_OK;
+}
+
+int icb_read_meta_c(icb_forest* f, int32_t tree, double* c) {
+  ICB_CUDA(cudaMemcpy(c, (char*)(f->view.meta + tree) + offsetof(TreeMeta, c), sizeof(double),
+                      cudaMemcpyDeviceToHost));
+  return ICB_OK;
+}
+
+int icb_export_tree(icb_forest* f, int32_t tree, int32_t* node_level, int32_t* node_parent, int32_t* node_owner,
+                    int32_t* node_off, int32_t* node_size, int32_t* node_lastpage, int32_t* members,
+                    int32_t* page_fill, int8_t* page_role, int32_t* page_tok, int32_t* tok2page, int8_t* level,
+                    int32_t* own_base, int32_t* own_list, float* lift, float* tail, int32_t* win, int32_t* sink) {
+  if (tree < 0 || tree >= f->cfg.n_trees) { icb_set_error(ICB_E_INPUT, "tree index out of range"); return ICB_E_INPUT; }
+  const ForestView& F = f->view;
+  const auto& c = f->cfg;
+  ICB_CUDA(cudaDeviceSynchronize());
+  size_t t = tree;
+#define CP(dst, src, n) \
+  if (dst) ICB_CUDA(cudaMemcpy(dst, src, sizeof(*dst) * (size_t)(n), cudaMemcpyDeviceToHost))
+  CP(node_level, F.node_level + t * c.node_cap, c.node_cap);
+  CP(node_parent, F.node_parent + t * c.node_cap, c.node_cap);
+  CP(node_owner, F.node_owner + t * c.node_cap, c.node_cap);
+  CP(node_off, F.node_off + t * c.node_cap, c.node_cap);
+  CP(node_size, F.node_size + t * c.node_cap, c.node_cap);
+  CP(node_lastpage, F.node_lastpage + t * c.node_cap, c.node_cap);
+  CP(members, F.members + t * c.member_cap, c.member_cap);
+  CP(page_fill, F.page_fill + t * c.page_cap, c.page_cap);
+  CP(page_role, F.page_role + t * c.page_cap, c.page_cap);
+  CP(page_tok, F.page_tok + t * c.page_cap * c.page_size, (size_t)c.page_cap * c.page_size);
+  CP(tok2page, F.tok2page + t * c.tok_cap, c.tok_cap);
+  CP(level, F.level + t * c.tok_cap, c.tok_cap);
+  CP(own_base, F.own_base + t * c.tok_cap, c.tok_cap);
+  CP(own_list, F.own_list + t * c.own_cap, c.own_cap);
+  CP(lift, F.lift + t * c.tok_cap * ICB_DPAD, (size_t)c.tok_cap * ICB_DPAD);
+  CP(tail, F.tail + t * c.tok_cap, c.tok_cap);
+#undef CP
+  TreeMeta m;
+  ICB_CUDA(cudaMemcpy(&m, F.meta + t, sizeof(TreeMeta), cudaMemcpyDeviceToHost));
+  if (win) for (int i = 0; i < ICB_MAX_WINDOW; ++i) win[i] = i < m.n_window ? m.win[i] : -1;
+  if (sink) for (int i = 0; i < ICB_MAX_SINK; ++i) sink[i] = i < m.n_sink ? m.sink[i] : -1;
+  return ICB_OK;
+}
+
+int icb_read_pages(icb_forest* f, int32_t tree, const int32_t* pages, int32_t count, float* keys, float* values) {
+  const ForestView& F = f->view;
+  const auto& c = f->cfg;
+  ICB_CUDA(cudaDeviceSynchronize());
+  const size_t kvb = F.kv_bf16 ? 2 : 4;
+  std::vector<char> kbuf((size_t)c.page_size * F.dkp * kvb), vbuf((size_t)c.page_size * F.dvp * kvb);
+  for (int i = 0; i < count; ++i) {
+    size_t slot0 = ((size_t)tree * c.page_cap + pages[i]) * c.page_size;
+    ICB_CUDA(cudaMemcpy(kbuf.data(), (char*)F.page_k + slot0 * F.dkp * kvb, kbuf.size(), cudaMemcpyDeviceToHost));
+    ICB_CUDA(cudaMemcpy(vbuf.data(), (char*)F.page_v + slot0 * F.dvp * kvb, vbuf.size(), cudaMemcpyDeviceToHost));
+    for (int r = 0; r < c.page_size; ++r) {
+      for (int j = 0; j < c.dim; ++j) {
+        float x;
+        if (F.kv_bf16) { uint16_t h; std::memcpy(&h, kbuf.data() + ((size_t)r * F.dkp + j) * 2, 2); uint32_t u = (uint32_t)h << 16; std::memcpy(&x, &u, 4); }
+        else std::memcpy(&x, kbuf.data() + ((size_t)r * F.dkp + j) * 4, 4);
+        keys[((size_t)i * c.page_size + r) * c.dim + j] = x;
+      }
+      for (int j = 0; j < c.dim_v; ++j) {
+        float x;
+        if (F.kv_bf16) { uint16_t h; std::memcpy(&h, vbuf.data() + ((size_t)r * F.dvp + j) * 2, 2); uint32_t u = (uint32_t)h << 16; std::memcpy(&x, &u, 4); }
+        else std::memcpy(&x, vbuf.data() + ((size_t)r * F.dvp + j) * 4, 4);
+        values[((size_t)i * c.page_size + r) * c.dim_v + j] = x;
+      }
+    }
+  }
+  return ICB_OK;
+}
+
+// Host restatement self-check: PCG64/SeedSequence draws (for CPU tests).
+int icb_host_pcg_doubles(const uint32_t* words, int32_t n_words, const uint32_t* spawn, int32_t n_spawn, int32_t n,
+                         double* out) {
+  uint64_t st[4];
+  icb_seedseq_u64x4(words, n_words, spawn, n_spawn, st);
+  Pcg64 g = icb_pcg_seed(st);
+  for (int i = 0; i < n; ++i) out[i] = icb_pcg_double(g);
+  return ICB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,196 @@
+// Device-side layout of the DCI forest and shared numerics.
+//
+// One forest holds T independent DCI trees (one per (sequence, layer, kv
+// head)).  Everything lives in HBM as flat structure-of-arrays indexed
+// [tree][...]; rows of the lifted-key matrix are indexed by TOKEN ID, so a
+// 64-bit ranking key (d2 bits << 32 | token id) identifies a candidate and
+// its row at once.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include "rng.cuh"
+#include "../../include/icecache_b200.h"
+
+#define ICB_DPAD 128          // device row width; dims >= d are zero
+#define ICB_NPROJ 8           // NUM_PROJECTIONS (dci.py:44)
+#define ICB_EXHAUSTIVE 64     // EXHAUSTIVE_NODE_LIMIT (dci.py:41)
+#define ICB_MAX_WINDOW 8
+#define ICB_MAX_SINK 8
+#define ICB_MAX_G 8
+#define ICB_ROOT_OWNER (-1)
+
+// Sticky per-tree error bits (host maps them to the reference's exceptions).
+enum {
+  ICB_ERR_CAP_NODES = 1 << 0,
+  ICB_ERR_CAP_MEMBERS = 1 << 1,
+  ICB_ERR_CAP_PAGES = 1 << 2,
+  ICB_ERR_CAP_OWN = 1 << 3,
+  ICB_ERR_CAP_TOKENS = 1 << 4,
+  ICB_ERR_DUP_ID = 1 << 5,
+  ICB_ERR_EMPTY_TREE = 1 << 6,
+  ICB_ERR_ZERO_QUERY = 1 << 7,
+  ICB_ERR_UNMAPPED = 1 << 8,
+  ICB_ERR_CAP_SCRATCH = 1 << 9,
+  ICB_ERR_PDCI_SIZE = 1 << 10,
+  ICB_ERR_WINDOW = 1 << 11,
+};
+
+struct TreeMeta {
+  int levels;        // number of levels (0 = empty)
+  int top_node;
+  int n_nodes;
+  int next_page;     // TierStore page-id counter (pagestore.py:138-149)
+  int member_top;    // bump pointer into the member pool
+  int own_top;       // bump pointer into the own list
+  int n_points;
+  int n_dirs;        // P-DCI direction cache entries used
+  int n_window;      // window pages (oldest first in win[])
+  int n_sink;
+  int win[ICB_MAX_WINDOW];
+  int sink[ICB_MAX_SINK];
+  int err;
+  int n_entropy;
+  uint32_t entropy[8];   // SeedSequence run entropy words
+  double c;          // KeyScale.c
+  Pcg64 rng;         // level stream (spawn_key=(0,)), continues across inserts
+  unsigned long long query_count, distance_evals, scale_clamps;
+};
+
+struct ForestView {
+  int T, dim, dim_v, s, kv_bf16;
+  int dkp, dvp;       // page row strides (dim, dim_v rounded up to 4; padding stays zero)
+  int tok_cap, node_cap, page_cap, member_cap, own_cap, dirs_cap;
+  double r;
+  TreeMeta* meta;
+  float* lift;        // [T][tok_cap][128]
+  float* tail;        // [T][tok_cap]
+  int8_t* level;      // [T][tok_cap]  top level (0 = not indexed)
+  int* own_base;      // [T][tok_cap]  own(p, lv) = own_list[own_base[p] + lv - 1]
+  int* tok2page;      // [T][tok_cap]
+  int* own_list;      // [T][own_cap]
+  int* node_level;    // [T][node_cap]
+  int* node_parent;
+  int* node_owner;
+  int* node_off;      // offset into members
+  int* node_size;
+  int* node_capm;     // member capacity of the node's block
+  int* node_lastpage; // leaves: last page id (-1 none)
+  int* node_dirs;     // P-DCI direction cache slot (-1 none)
+  int* members;       // [T][member_cap] token ids
+  int* page_fill;     // [T][page_cap]
+  int8_t* page_role;  // [T][page_cap] 0 none, 1 sink, 2 window, 3 indexed
+  int* page_tok;      // [T][page_cap][s]
+  void* page_k;       // [T][page_cap][s][dim]  (fp32 or bf16)
+  void* page_v;       // [T][page_cap][s][dim_v]
+  double* dirs;       // [T][dirs_cap][8][dim+1]
+  uint32_t* prev_sel; // [T][page_cap/32 + 1] residency: previous step's selection
+
+  __device__ __forceinline__ size_t tk(int t, int tok) const { return (size_t)t * tok_cap + tok; }
+  __device__ __forceinline__ size_t nd(int t, int n) const { return (size_t)t * node_cap + n; }
+  __device__ __forceinline__ size_t pg(int t, int p) const { return (size_t)t * page_cap + p; }
+  __device__ __forceinline__ const float* row(int t, int tok) const {
+    return lift + ((size_t)t * tok_cap + tok) * ICB_DPAD;
+  }
+  __device__ __forceinline__ int own(int t, int p, int lv) const {
+    return own_list[(size_t)t * own_cap + own_base[tk(t, p)] + lv - 1];
+  }
+  __device__ __forceinline__ int* mem(int t) const { return members + (size_t)t * member_cap; }
+  __device__ __forceinline__ int pwords() const { return page_cap / 32 + 1; }
+};
+
+// ---------------------------------------------------------------------------
+// numerics
+
+// Squared lifted distance in fp32 with the fixed order the oracle restates
+// (oracle/numerics.py:d2_fp32): per-lane ((s0+s1)+s2)+s3 over dims 4l..4l+3,
+// xor butterfly 16,8,4,2,1, then + (tail - q_tail)^2.  No FMA contraction.
+__device__ __forceinline__ float lane_sq4(float4 p, float4 q) {
+  float a = __fsub_rn(p.x, q.x), b = __fsub_rn(p.y, q.y);
+  float c = __fsub_rn(p.z, q.z), d = __fsub_rn(p.w, q.w);
+  return __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(a, a), __fmul_rn(b, b)), __fmul_rn(c, c)),
+                   __fmul_rn(d, d));
+}
+__device__ __forceinline__ float warp_sum_butterfly(float s) {
+  s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 16));
+  s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 8));
+  s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
+  s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+  s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
+  return s;
+}
+__device__ __forceinline__ float d2_finish(float s, float pt, float qt) {
+  float dt = __fsub_rn(pt, qt);
+  return __fadd_rn(s, __fmul_rn(dt, dt));
+}
+
+__device__ __forceinline__ unsigned long long make_key(float d2, int id) {
+  return ((unsigned long long)__float_as_uint(d2) << 32) | (unsigned)id;
+}
+__device__ __forceinline__ int key_id(unsigned long long k) { return (int)(unsigned)(k & 0xffffffffu); }
+
+// NumPy pairwise summation (numpy/core/src/umath/loops_utils.h.src) for one
+// row held in memory, n <= 256.  Single thread.
+__device__ __forceinline__ double pairwise_block(const double* a, int n) {
+  if (n < 8) {
+    double r = n > 0 ? a[0] : 0.0;
+    for (int i = 1; i < n; ++i) r = __dadd_rn(r, a[i]);
+    return r;
+  }
+  double r[8];
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  int lim = n - (n % 8);
+  for (int i = 8; i < lim; i += 8)
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (int i = lim; i < n; ++i) res = __dadd_rn(res, a[i]);
+  return res;
+}
+__device__ __forceinline__ double pairwise_sum(const double* a, int n) {
+  if (n <= 128) return pairwise_block(a, n);
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pairwise_block(a, n2), pairwise_block(a + n2, n - n2));
+}
+
+// ---------------------------------------------------------------------------
+// block helpers
+
+template <int NT>
+__device__ __forceinline__ int block_exclusive_scan(int v, int* sm /* >= NT/32+1 */, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sm[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < NT / 32 ? sm[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < NT / 32) sm[lane] = w;
+  }
+  __syncthreads();
+  int before = (warp > 0 ? sm[warp - 1] : 0) + x - v;
+  total = sm[NT / 32 - 1];
+  __syncthreads();
+  return before;
+}
+
+__device__ __forceinline__ void set_err(TreeMeta* m, int bit) { atomicOr(&m->err, bit); }
+
+template <typename KT>
+__device__ __forceinline__ void store_kv(KT* dst, float v);
+template <>
+__device__ __forceinline__ void store_kv<float>(float* dst, float v) { *dst = v; }
+template <>
+__device__ __forceinline__ void store_kv<__nv_bfloat16>(__nv_bfloat16* dst, float v) {
+  *dst = __float2bfloat16_rn(v);
+}

@@ -1,0 +1,464 @@
+// Dynamic insertion and window rotation on the device.
+//
+//   insert_one      DciTree.insert (dci.py:385-431), _grow_top (:433-449),
+//                   _place_entry (:368-381); the parent search is the block
+//                   search with PARENT_BUDGET (k=1, beam=8, visit_cap=64;
+//                   dci.py:78) targeted at level+1.
+//   rotate          Engine._rotate_layer (engine.py:516-534): offload the
+//                   oldest window page, insert its entries in slot order,
+//                   release it, allocate a fresh window page.
+//   append          the decode token joins the first non-full window page
+//                   (engine.py:426-429).
+//   resident pages  sink / window allocation at prefill (engine.py:263-276).
+//
+// One CTA per tree; inserts of a tree are sequential (each must see the
+// previous), trees run in parallel.  Raw fp32 keys of window tokens are
+// stashed in the token's (not yet used) lifted row so the insert lifts the
+// exact input key even when pages store bf16.
+#include "search.cuh"
+#include "internal.h"
+
+namespace icb {
+
+struct SlotLayout;
+
+struct InsertArgs {
+  const int32_t* trees;
+  int n, m;
+  const int32_t* tokens;   // [n][m]
+  const float* keys;       // [n][m][dim]
+  const float* values;     // [n][m][dim_v] or null
+  const int32_t* levels;   // [n][m] or null
+  int32_t* out_levels;
+  int from_window;         // 1: rotate the oldest window page
+  int scalar_bytes;
+  int64_t* stats;          // [n][2] offload bytes, transactions (may be null)
+};
+
+__device__ int new_node(const ForestView& F, int t, int level, int parent, int owner, int first_member) {
+  TreeMeta* m = F.meta + t;
+  int id = m->n_nodes;
+  if (id >= F.node_cap) { set_err(m, ICB_ERR_CAP_NODES); return -1; }
+  m->n_nodes = id + 1;
+  size_t x = F.nd(t, id);
+  int cap = 4;
+  int off = m->member_top;
+  if (off + cap > F.member_cap) { set_err(m, ICB_ERR_CAP_MEMBERS); return -1; }
+  m->member_top = off + cap;
+  F.node_level[x] = level;
+  F.node_parent[x] = parent;
+  F.node_owner[x] = owner;
+  F.node_off[x] = off;
+  F.node_size[x] = 1;
+  F.node_capm[x] = cap;
+  F.node_lastpage[x] = -1;
+  F.node_dirs[x] = -1;
+  F.mem(t)[off] = first_member;
+  return id;
+}
+
+__device__ void add_member(const ForestView& F, int t, int node, int tok) {
+  TreeMeta* m = F.meta + t;
+  size_t x = F.nd(t, node);
+  int sz = F.node_size[x], cap = F.node_capm[x], off = F.node_off[x];
+  int* mem = F.mem(t);
+  if (sz == cap) {
+    int ncap = cap < 4 ? 4 : 2 * cap;
+    int noff = m->member_top;
+    if (noff + ncap > F.member_cap) { set_err(m, ICB_ERR_CAP_MEMBERS); return; }
+    m->member_top = noff + ncap;
+    for (int i = 0; i < sz; ++i) mem[noff + i] = mem[off + i];
+    off = noff;
+    F.node_off[x] = off;
+    F.node_capm[x] = ncap;
+  }
+  mem[off + sz] = tok;
+  F.node_size[x] = sz + 1;
+  // the node's P-DCI ladders are a function of its member set: nothing to update
+}
+
+__device__ __forceinline__ void set_own(const ForestView& F, int t, int tok, int lv, int node) {
+  F.own_list[(size_t)t * F.own_cap + F.own_base[F.tk(t, tok)] + lv - 1] = node;
+}
+
+// Copy one entry into a page slot.  K/V come either from fp32 arrays or from
+// another page slot of the same forest (window rotation).
+__device__ void write_slot(const ForestView& F, int t, int page, int slot, const float* kf, const float* vf,
+                           long long src_slot) {
+  const int lane = threadIdx.x & 31;
+  size_t dst = F.pg(t, page) * F.s + slot;
+  if (F.kv_bf16) {
+    __nv_bfloat16* K = (__nv_bfloat16*)F.page_k;
+    __nv_bfloat16* V = (__nv_bfloat16*)F.page_v;
+    for (int j = lane; j < F.dim; j += 32)
+      K[dst * F.dkp + j] = src_slot >= 0 ? K[(size_t)src_slot * F.dkp + j] : __float2bfloat16_rn(kf[j]);
+    for (int j = lane; j < F.dim_v; j += 32)
+      V[dst * F.dvp + j] = src_slot >= 0 ? V[(size_t)src_slot * F.dvp + j]
+                                           : __float2bfloat16_rn(vf ? vf[j] : 0.f);
+  } else {
+    float* K = (float*)F.page_k;
+    float* V = (float*)F.page_v;
+    for (int j = lane; j < F.dim; j += 32) K[dst * F.dkp + j] = src_slot >= 0 ? K[(size_t)src_slot * F.dkp + j] : kf[j];
+    for (int j = lane; j < F.dim_v; j += 32)
+      V[dst * F.dvp + j] = src_slot >= 0 ? V[(size_t)src_slot * F.dvp + j] : (vf ? vf[j] : 0.f);
+  }
+}
+
+// One insert; all threads of the block participate.  key: fp32 raw key
+// (global); returns the level (valid in thread 0).
+template <int NT>
+__device__ int insert_one(SearchSmem& S, const ForestView& F, const SearchScratch& SS, int t, int tok,
+                          const float* key, const float* val, long long src_slot, int given_level,
+                          double* dirs_tmp) {
+  TreeMeta* m = F.meta + t;
+  __shared__ int s_level, s_bad, s_leaf, s_container, s_chain_from;
+  __shared__ double s_norm;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    s_bad = 0;
+    if (tok < 0 || tok >= F.tok_cap) { set_err(m, ICB_ERR_CAP_TOKENS); s_bad = 1; }
+    else {
+      int old = atomicCAS(F.tok2page + F.tk(t, tok), -1, -2);
+      if (old != -1) { set_err(m, ICB_ERR_DUP_ID); s_bad = 1; }
+    }
+    int lv = given_level;
+    if (lv <= 0 && !s_bad) {
+      Pcg64 g = m->rng;
+      lv = icb_draw_level(g, F.r);
+      m->rng = g;
+    }
+    if (lv > 62) lv = 62;
+    s_level = lv;
+  }
+  // lift (dci.py:225-240): norm in pairwise order; clamp above c
+  for (int u = tid; u < F.dim; u += NT) {
+    double x = (double)key[u];
+    S.q64[u] = __dmul_rn(x, x);
+  }
+  __syncthreads();
+  if (s_bad) return -1;
+  if (tid == 0) s_norm = sqrt(pairwise_sum(S.q64, F.dim));
+  __syncthreads();
+  const double c = m->c, norm = s_norm;
+  const bool over = norm > c;
+  const double safe = over ? norm : c;
+  float* row = F.lift + F.tk(t, tok) * ICB_DPAD;
+  // read the raw key before overwriting (it may live in this very row)
+  float kv = tid < F.dim ? key[tid] : 0.f;
+  __syncthreads();
+  for (int u = tid; u < ICB_DPAD; u += NT) {
+    float v = u < F.dim ? __double2float_rn(__ddiv_rn((double)kv, safe)) : 0.0f;
+    row[u] = v;
+    S.q[0][u] = v;
+  }
+  if (tid == 0) {
+    double ratio = __ddiv_rn(norm, safe);
+    double rad = __dsub_rn(1.0, __dmul_rn(ratio, ratio));
+    float tl = __double2float_rn(sqrt(rad > 0.0 ? rad : 0.0));
+    F.tail[F.tk(t, tok)] = tl;
+    S.qt[0] = tl;
+    if (over) m->scale_clamps += 1;
+    F.level[F.tk(t, tok)] = (int8_t)s_level;
+    F.own_base[F.tk(t, tok)] = m->own_top;
+    if (m->own_top + s_level - 1 > F.own_cap) set_err(m, ICB_ERR_CAP_OWN);
+    m->own_top += s_level - 1;
+  }
+  __syncthreads();
+  const int level = s_level;
+  const int L = m->levels;
+  if (L == 0) {
+    if (tid == 0) {
+      int top = new_node(F, t, level, -1, ICB_ROOT_OWNER, tok);
+      m->top_node = top;
+      m->levels = level;
+      s_container = top;
+      s_chain_from = level - 1;
+    }
+  } else if (level > L) {
+    if (tid == 0) {
+      int old_top = m->top_node;
+      int top = new_node(F, t, level, -1, ICB_ROOT_OWNER, tok);
+      m->top_node = top;
+      int prev = top;
+      for (int lv = level - 1; lv > L; --lv) {
+        prev = new_node(F, t, lv, prev, tok, tok);
+        set_own(F, t, tok, lv, prev);
+      }
+      size_t x = F.nd(t, old_top);
+      F.node_owner[x] = tok;
+      F.node_parent[x] = prev;
+      set_own(F, t, tok, L, old_top);
+      add_member(F, t, old_top, tok);
+      m->levels = level;
+      s_container = old_top;   // membership at level L
+      s_chain_from = L - 1;
+    }
+  } else {
+    if (level == L) {
+      if (tid == 0) { s_container = m->top_node; s_chain_from = level - 1; }
+    } else {
+      SearchParams P;
+      P.G = 1; P.k = 1; P.beam = 8; P.visit_cap = 64; P.target = level + 1;
+      tree_search<NT>(S, F, SS, t, P, dirs_tmp);
+      int n = finalize_head<NT>(S, F, SS, 0, 1);
+      if (tid == 0) {
+        int parent = n > 0 ? key_id(S.sortbuf[0]) : -1;
+        s_container = parent >= 0 ? F.own(t, parent, level) : m->top_node;
+        s_chain_from = level - 1;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) add_member(F, t, s_container, tok);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int parent_node = s_container;   // node holding tok at chain_from + 1
+    for (int lv = s_chain_from; lv >= 1; --lv) {
+      int nn = new_node(F, t, lv, parent_node, tok, tok);
+      set_own(F, t, tok, lv, nn);
+      parent_node = nn;
+    }
+    int leaf = level >= 2 ? F.own(t, tok, 1) : s_container;
+    // page placement (dci.py:368-381)
+    size_t lx = F.nd(t, leaf);
+    int page = F.node_lastpage[lx];
+    if (page < 0 || F.page_fill[F.pg(t, page)] >= F.s) {
+      page = m->next_page;
+      if (page >= F.page_cap) { set_err(m, ICB_ERR_CAP_PAGES); page = -1; }
+      else {
+        m->next_page = page + 1;
+        F.page_fill[F.pg(t, page)] = 0;
+        F.page_role[F.pg(t, page)] = ICB_ROLE_INDEXED;
+        F.node_lastpage[lx] = page;
+      }
+    }
+    s_leaf = page;
+    if (page >= 0) {
+      int slot = F.page_fill[F.pg(t, page)];
+      F.page_tok[F.pg(t, page) * F.s + slot] = tok;
+      F.page_fill[F.pg(t, page)] = slot + 1;
+      F.tok2page[F.tk(t, tok)] = page;
+      S.misc[4] = slot;
+    }
+    m->n_points += 1;
+  }
+  __syncthreads();
+  if (s_leaf >= 0 && tid < 32) write_slot(F, t, s_leaf, S.misc[4], key, val, src_slot);
+  __syncthreads();
+  return level;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) insert_kernel(ForestView F, InsertArgs A, char* scratch, size_t slot_bytes,
+                                                    size_t off_cand, size_t off_pool, size_t off_surv,
+                                                    size_t off_ulist, size_t off_umask, size_t off_uoff,
+                                                    size_t off_nmask, size_t off_seen, size_t off_vis,
+                                                    size_t off_proj, size_t off_ekey, size_t off_dirs) {
+  __shared__ SearchSmem S;
+  const int b = blockIdx.x;
+  const int t = A.trees[b];
+  char* base = scratch + (size_t)b * slot_bytes;
+  SearchScratch SS;
+  SS.cand = (unsigned long long*)(base + off_cand);
+  SS.pool = (unsigned long long*)(base + off_pool);
+  SS.surv = (int*)(base + off_surv);
+  SS.ulist = (int*)(base + off_ulist);
+  SS.umask = (int*)(base + off_umask);
+  SS.uoff = (int*)(base + off_uoff);
+  SS.nmask = (unsigned*)(base + off_nmask);
+  SS.seen = (unsigned*)(base + off_seen);
+  SS.vis = (int*)(base + off_vis);
+  SS.proj = (double*)(base + off_proj);
+  SS.ekey = (unsigned long long*)(base + off_ekey);
+  SS.ccap = F.tok_cap;
+  double* dirs_tmp = (double*)(base + off_dirs);
+  TreeMeta* m = F.meta + t;
+  if (A.from_window) {
+    __shared__ int s_old, s_fill;
+    if (threadIdx.x == 0) {
+      s_old = m->n_window > 0 ? m->win[0] : -1;
+      s_fill = s_old >= 0 ? F.page_fill[F.pg(t, s_old)] : 0;
+      if (s_old < 0) set_err(m, ICB_ERR_WINDOW);
+      else if (A.stats) {
+        A.stats[(size_t)b * 2] += (int64_t)s_fill * (F.dim + F.dim_v) * A.scalar_bytes;
+        A.stats[(size_t)b * 2 + 1] += 1;
+      }
+    }
+    __syncthreads();
+    const int old = s_old;
+    if (old < 0) return;
+    for (int e = 0; e < s_fill; ++e) {
+      int tok = F.page_tok[F.pg(t, old) * F.s + e];
+      const float* raw = F.lift + F.tk(t, tok) * ICB_DPAD;   // stashed raw key
+      insert_one<NT>(S, F, SS, t, tok, raw, nullptr, (long long)(F.pg(t, old) * F.s + e), 0, dirs_tmp);
+    }
+    if (threadIdx.x == 0) {
+      // release (pagestore.py:157-162) then a fresh window page
+      F.page_role[F.pg(t, old)] = 0;
+      for (int i = 0; i + 1 < m->n_window; ++i) m->win[i] = m->win[i + 1];
+      int np = m->next_page;
+      if (np >= F.page_cap) { set_err(m, ICB_ERR_CAP_PAGES); }
+      else {
+        m->next_page = np + 1;
+        F.page_fill[F.pg(t, np)] = 0;
+        F.page_role[F.pg(t, np)] = ICB_ROLE_WINDOW;
+        m->win[m->n_window - 1] = np;
+      }
+    }
+    return;
+  }
+  for (int e = 0; e < A.m; ++e) {
+    size_t x = (size_t)b * A.m + e;
+    int tok = A.tokens[x];
+    int lv = A.levels ? A.levels[x] : 0;
+    int got = insert_one<NT>(S, F, SS, t, tok, A.keys + x * F.dim, A.values ? A.values + x * F.dim_v : nullptr,
+                             -1, lv, dirs_tmp);
+    if (threadIdx.x == 0 && A.out_levels) A.out_levels[x] = got;
+  }
+}
+
+// Append one decode token to the first non-full window page of each tree.
+__global__ void append_window_kernel(ForestView F, const int32_t* trees, int n, int token, const float* keys,
+                                     const float* values) {
+  const int b = blockIdx.x;
+  const int t = trees[b];
+  TreeMeta* m = F.meta + t;
+  __shared__ int s_page, s_slot;
+  if (threadIdx.x == 0) {
+    s_page = -1;
+    for (int i = 0; i < m->n_window; ++i) {
+      int p = m->win[i];
+      if (F.page_fill[F.pg(t, p)] < F.s) { s_page = p; break; }
+    }
+    if (s_page < 0 || token < 0 || token >= F.tok_cap) set_err(m, ICB_ERR_WINDOW);
+    else {
+      s_slot = F.page_fill[F.pg(t, s_page)];
+      F.page_fill[F.pg(t, s_page)] = s_slot + 1;
+      F.page_tok[F.pg(t, s_page) * F.s + s_slot] = token;
+    }
+  }
+  __syncthreads();
+  if (s_page < 0 || token < 0 || token >= F.tok_cap) return;
+  const float* k = keys + (size_t)b * F.dim;
+  float* stash = F.lift + F.tk(t, token) * ICB_DPAD;
+  for (int j = threadIdx.x; j < F.dim; j += blockDim.x) stash[j] = k[j];
+  if (threadIdx.x < 32) write_slot(F, t, s_page, s_slot, k, values + (size_t)b * F.dim_v, -1);
+}
+
+// Resident (sink/window) pages at prefill.
+__global__ void resident_pages_kernel(ForestView F, const int32_t* trees, int n, int role, int count,
+                                      int n_tokens, const int32_t* tokens, const float* keys,
+                                      const float* values) {
+  const int b = blockIdx.x;
+  const int t = trees[b];
+  TreeMeta* m = F.meta + t;
+  __shared__ int s_first;
+  if (threadIdx.x == 0) {
+    s_first = m->next_page;
+    if (s_first + count > F.page_cap) { set_err(m, ICB_ERR_CAP_PAGES); s_first = -1; }
+    else {
+      m->next_page = s_first + count;
+      for (int i = 0; i < count; ++i) {
+        int p = s_first + i;
+        F.page_role[F.pg(t, p)] = (int8_t)role;
+        F.page_fill[F.pg(t, p)] = max(0, min(F.s, n_tokens - i * F.s));
+        if (role == ICB_ROLE_SINK && m->n_sink < ICB_MAX_SINK) m->sink[m->n_sink++] = p;
+        if (role == ICB_ROLE_WINDOW && m->n_window < ICB_MAX_WINDOW) m->win[m->n_window++] = p;
+      }
+    }
+  }
+  __syncthreads();
+  if (s_first < 0) return;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int e = warp; e < n_tokens && e < count * F.s; e += nw) {
+    int page = s_first + e / F.s, slot = e % F.s;
+    int tok = tokens[(size_t)b * n_tokens + e];
+    const float* k = keys + ((size_t)b * n_tokens + e) * F.dim;
+    if ((threadIdx.x & 31) == 0) F.page_tok[F.pg(t, page) * F.s + slot] = tok;
+    if (tok >= 0 && tok < F.tok_cap) {
+      float* stash = F.lift + F.tk(t, tok) * ICB_DPAD;
+      for (int j = threadIdx.x & 31; j < F.dim; j += 32) stash[j] = k[j];
+    }
+    write_slot(F, t, page, slot, k, values + ((size_t)b * n_tokens + e) * F.dim_v, -1);
+  }
+}
+
+}  // namespace icb
+
+using namespace icb;
+
+// scratch layout shared with search.cu (same field order)
+struct InsLayout {
+  size_t cand, pool, surv, ulist, umask, uoff, nmask, seen, vis, proj, ekey, dirs, total;
+};
+static size_t al256h(size_t x) { return (x + 255) & ~(size_t)255; }
+static InsLayout ins_layout(const icb_forest_config& c) {
+  InsLayout L{};
+  size_t o = 0, cc = (size_t)c.tok_cap;
+  L.cand = o; o = al256h(o + cc * 8);
+  L.pool = o; o = al256h(o + cc * 8);
+  L.surv = o; o = al256h(o + cc * 4);
+  L.ulist = o; o = al256h(o + (size_t)c.node_cap * 4);
+  L.umask = o; o = al256h(o + (size_t)c.node_cap * 4);
+  L.uoff = o; o = al256h(o + (size_t)c.node_cap * 4);
+  L.nmask = o; o = al256h(o + (size_t)c.node_cap * 4);
+  L.seen = o; o = al256h(o + (size_t)(c.tok_cap / 32 + 1) * 4);
+  L.vis = o; o = al256h(o + cc * 4);
+  L.proj = o; o = al256h(o + cc * ICB_NPROJ * 8);
+  L.ekey = o; o = al256h(o + cc * 16);
+  L.dirs = o; o = al256h(o + (size_t)ICB_NPROJ * (c.dim + 1) * 8);
+  L.total = o;
+  return L;
+}
+
+int ensure_insert_scratch(icb_forest* f, int n, char** out, InsLayout* lay) {
+  InsLayout L = ins_layout(f->cfg);
+  size_t need = L.total * (size_t)n;
+  if (need > f->iscratch_bytes) {
+    if (f->iscratch) ICB_CUDA(cudaFree(f->iscratch));
+    f->iscratch = nullptr;
+    f->iscratch_bytes = 0;
+    ICB_CUDA(cudaMalloc(&f->iscratch, need));
+    ICB_CUDA(cudaMemset(f->iscratch, 0, need));
+    f->iscratch_bytes = need;
+  }
+  *out = (char*)f->iscratch;
+  *lay = L;
+  return ICB_OK;
+}
+
+int icb_insert_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t m, const int32_t* tokens,
+                    const float* keys, const float* values, const int32_t* levels, int32_t* out_levels,
+                    int from_window, int32_t scalar_bytes, int64_t* stats, cudaStream_t st) {
+  if (n <= 0) return ICB_OK;
+  char* scratch;
+  InsLayout L;
+  int rc = ensure_insert_scratch(f, n, &scratch, &L);
+  if (rc) return rc;
+  InsertArgs A{};
+  A.trees = trees; A.n = n; A.m = m; A.tokens = tokens; A.keys = keys; A.values = values;
+  A.levels = levels; A.out_levels = out_levels; A.from_window = from_window;
+  A.scalar_bytes = scalar_bytes; A.stats = stats;
+  insert_kernel<kSearchThreads><<<n, kSearchThreads, 0, st>>>(f->view, A, scratch, L.total, L.cand, L.pool,
+                                                              L.surv, L.ulist, L.umask, L.uoff, L.nmask,
+                                                              L.seen, L.vis, L.proj, L.ekey, L.dirs);
+  ICB_CUDA(cudaGetLastError());
+  return ICB_OK;
+}
+
+int icb_append_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t token, const float* keys,
+                    const float* values, cudaStream_t st) {
+  if (n <= 0) return ICB_OK;
+  append_window_kernel<<<n, 128, 0, st>>>(f->view, trees, n, token, keys, values);
+  ICB_CUDA(cudaGetLastError());
+  return ICB_OK;
+}
+
+int icb_resident_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t role, int32_t count,
+                      int32_t n_tokens, const int32_t* tokens, const float* keys, const float* values,
+                      cudaStream_t st) {
+  if (n <= 0) return ICB_OK;
+  resident_pages_kernel<<<n, 256, 0, st>>>(f->view, trees, n, role, count, n_tokens, tokens, keys, values);
+  ICB_CUDA(cudaGetLastError());
+  return ICB_OK;
+}

@@ -1,0 +1,220 @@
+// Decode-time query: DciTree.query for G heads per tree, find_page_index and
+// gqa_union fused into the epilogue (dci.py:318-364, pagestore.py:111-113,
+// attention.py:96-103, engine.py:436-447).
+#include "search.cuh"
+#include "internal.h"
+
+namespace icb {
+
+struct QueryArgs {
+  const int32_t* trees;
+  int n, G, lifted_input;
+  const float* queries;
+  SearchParams P;
+  int32_t* out_ids;
+  int k_out;
+  int32_t* out_counts;
+  int32_t* out_pages;
+  int pages_cap;
+  int32_t* out_npages;
+};
+
+// Scratch slot b carved from one buffer.
+struct SlotLayout {
+  size_t cand, pool, surv, ulist, umask, uoff, nmask, seen, vis, proj, ekey, pbits, dirs, total;
+};
+
+__host__ __device__ inline size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+__host__ __device__ inline SlotLayout slot_layout(int G, int tok_cap, int node_cap, int page_cap, int dim) {
+  SlotLayout L{};
+  size_t o = 0;
+  size_t cc = (size_t)tok_cap;
+  L.cand = o; o = al256(o + (size_t)G * cc * 8);
+  L.pool = o; o = al256(o + (size_t)G * cc * 8);
+  L.surv = o; o = al256(o + (size_t)G * cc * 4);
+  L.ulist = o; o = al256(o + (size_t)node_cap * 4);
+  L.umask = o; o = al256(o + (size_t)node_cap * 4);
+  L.uoff = o; o = al256(o + (size_t)G * node_cap * 4);
+  L.nmask = o; o = al256(o + (size_t)node_cap * 4);
+  L.seen = o; o = al256(o + (size_t)G * (tok_cap / 32 + 1) * 4);
+  L.vis = o; o = al256(o + cc * 4);
+  L.proj = o; o = al256(o + cc * ICB_NPROJ * 8);
+  L.ekey = o; o = al256(o + cc * 16);
+  L.pbits = o; o = al256(o + (size_t)(page_cap / 32 + 1) * 4);
+  L.dirs = o; o = al256(o + (size_t)ICB_NPROJ * (dim + 1) * 8);
+  L.total = o;
+  return L;
+}
+
+__device__ inline SearchScratch slot_scratch(char* base, const SlotLayout& L, int tok_cap, double** dirs,
+                                             unsigned** pbits) {
+  SearchScratch S;
+  S.cand = (unsigned long long*)(base + L.cand);
+  S.pool = (unsigned long long*)(base + L.pool);
+  S.surv = (int*)(base + L.surv);
+  S.ulist = (int*)(base + L.ulist);
+  S.umask = (int*)(base + L.umask);
+  S.uoff = (int*)(base + L.uoff);
+  S.nmask = (unsigned*)(base + L.nmask);
+  S.seen = (unsigned*)(base + L.seen);
+  S.vis = (int*)(base + L.vis);
+  S.proj = (double*)(base + L.proj);
+  S.ekey = (unsigned long long*)(base + L.ekey);
+  S.ccap = tok_cap;
+  *pbits = (unsigned*)(base + L.pbits);
+  *dirs = (double*)(base + L.dirs);
+  return S;
+}
+
+// Lift raw query g (geometry.py:89-98): fp64 norm in pairwise order, fp32 q/|q|.
+template <int NT>
+__device__ bool lift_query(SearchSmem& S, const ForestView& F, const float* q, int g) {
+  for (int u = threadIdx.x; u < F.dim; u += NT) {
+    double x = (double)q[u];
+    S.q64[u] = __dmul_rn(x, x);
+  }
+  __syncthreads();
+  __shared__ double s_norm;
+  if (threadIdx.x == 0) s_norm = sqrt(pairwise_sum(S.q64, F.dim));
+  __syncthreads();
+  const double nrm = s_norm;
+  for (int u = threadIdx.x; u < ICB_DPAD; u += NT)
+    S.q[g][u] = (u < F.dim && nrm != 0.0) ? __double2float_rn(__ddiv_rn((double)q[u], nrm)) : 0.0f;
+  if (threadIdx.x == 0) S.qt[g] = 0.0f;
+  __syncthreads();
+  return nrm != 0.0;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) query_kernel(ForestView F, QueryArgs A, char* scratch, SlotLayout SL) {
+  __shared__ SearchSmem S;
+  const int b = blockIdx.x;
+  const int t = A.trees[b];
+  const int G = A.G;
+  double* dirs_tmp;
+  unsigned* pbits;
+  SearchScratch SS = slot_scratch(scratch + (size_t)b * SL.total, SL, F.tok_cap, &dirs_tmp, &pbits);
+  const int L = F.meta[t].levels;
+  if (L == 0) {
+    if (threadIdx.x == 0) set_err(F.meta + t, ICB_ERR_EMPTY_TREE);
+    for (int g = threadIdx.x; g < G; g += NT) A.out_counts[(size_t)b * G + g] = 0;
+    if (threadIdx.x == 0 && A.out_npages) A.out_npages[b] = 0;
+    return;
+  }
+  // queries
+  bool ok = true;
+  for (int g = 0; g < G; ++g) {
+    const float* q = A.queries + ((size_t)b * G + g) * (F.dim + (A.lifted_input ? 1 : 0));
+    if (A.lifted_input) {
+      for (int u = threadIdx.x; u < ICB_DPAD; u += NT) S.q[g][u] = u < F.dim ? q[u] : 0.0f;
+      if (threadIdx.x == 0) S.qt[g] = q[F.dim];
+      __syncthreads();
+    } else {
+      ok = lift_query<NT>(S, F, q, g) && ok;
+    }
+  }
+  if (!ok) {
+    if (threadIdx.x == 0) set_err(F.meta + t, ICB_ERR_ZERO_QUERY);
+    for (int g = threadIdx.x; g < G; g += NT) A.out_counts[(size_t)b * G + g] = 0;
+    if (threadIdx.x == 0 && A.out_npages) A.out_npages[b] = 0;
+    return;
+  }
+  tree_search<NT>(S, F, SS, t, A.P, dirs_tmp);
+  if (F.meta[t].err & ICB_ERR_CAP_SCRATCH) return;
+  // final ranked top-k per head, token -> page bits
+  for (int g = 0; g < G; ++g) {
+    if (min((long long)S.npool[g], A.P.k) > kSortMax) {
+      if (threadIdx.x == 0) set_err(F.meta + t, ICB_ERR_CAP_SCRATCH);
+    }
+    int n = finalize_head<NT>(S, F, SS, g, A.P.k);
+    int nw = min(n, A.k_out);
+    for (int i = threadIdx.x; i < nw; i += NT)
+      A.out_ids[((size_t)b * G + g) * A.k_out + i] = key_id(S.sortbuf[i]);
+    if (threadIdx.x == 0) A.out_counts[(size_t)b * G + g] = nw;
+    if (A.out_pages) {
+      for (int i = threadIdx.x; i < n; i += NT) {
+        int id = key_id(S.sortbuf[i]);
+        int p = F.tok2page[F.tk(t, id)];
+        if (p < 0 || p >= F.page_cap) set_err(F.meta + t, ICB_ERR_UNMAPPED);
+        else atomicOr(pbits + (p >> 5), 1u << (p & 31));
+      }
+    }
+    __syncthreads();
+  }
+  if (!A.out_pages) return;
+  // ascending compaction of the page bitmap (gqa_union + sorted)
+  const int nwords = F.page_cap / 32 + 1;
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nwords; base += NT) {
+    int w = base + threadIdx.x;
+    unsigned bits = w < nwords ? pbits[w] : 0u;
+    int tot;
+    int ex = block_exclusive_scan<NT>(__popc(bits), S.wsum, tot);
+    int pos = carry + ex;
+    while (bits) {
+      int bit = __ffs(bits) - 1;
+      bits &= bits - 1;
+      if (pos < A.pages_cap) A.out_pages[(size_t)b * A.pages_cap + pos] = w * 32 + bit;
+      ++pos;
+    }
+    if (w < nwords) pbits[w] = 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) A.out_npages[b] = min(carry, A.pages_cap);
+}
+
+}  // namespace icb
+
+using namespace icb;
+
+// Per-call scratch: one slot per tree in the call (grown and zeroed on demand).
+int ensure_query_scratch(icb_forest* f, int n, int G, cudaStream_t st, char** out, SlotLayout* sl) {
+  const auto& c = f->cfg;
+  SlotLayout L = slot_layout(G, c.tok_cap, c.node_cap, c.page_cap, c.dim);
+  size_t need = L.total * (size_t)n;
+  if (need > f->qscratch_bytes) {
+    if (f->qscratch) ICB_CUDA(cudaFree(f->qscratch));
+    f->qscratch = nullptr;
+    f->qscratch_bytes = 0;
+    ICB_CUDA(cudaMalloc(&f->qscratch, need));
+    ICB_CUDA(cudaMemset(f->qscratch, 0, need));   // mark arrays must start zero
+    f->qscratch_bytes = need;
+    f->qscratch_G = G;
+  } else if (f->qscratch_G != G) {
+    // the slot layout depends on G: mark arrays move, so re-zero everything
+    ICB_CUDA(cudaMemsetAsync(f->qscratch, 0, f->qscratch_bytes, st));
+    f->qscratch_G = G;
+  }
+  *out = (char*)f->qscratch;
+  *sl = L;
+  (void)st;
+  return ICB_OK;
+}
+
+int icb_query_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, const float* queries,
+                   int32_t lifted_input, int32_t k, int64_t beam, int64_t visit_cap, int32_t target_level,
+                   int32_t* out_ids, int32_t k_out, int32_t* out_counts, int32_t* out_pages,
+                   int32_t pages_cap, int32_t* out_npages, cudaStream_t st) {
+  if (n <= 0) return ICB_OK;
+  if (G < 1 || G > ICB_MAX_G) {
+    icb_set_error(ICB_E_CONFIG, "query heads per tree must be in [1, 8]");
+    return ICB_E_CONFIG;
+  }
+  char* scratch;
+  SlotLayout SL;
+  int rc = ensure_query_scratch(f, n, G, st, &scratch, &SL);
+  if (rc) return rc;
+  QueryArgs A{};
+  A.trees = trees; A.n = n; A.G = G; A.lifted_input = lifted_input; A.queries = queries;
+  A.P.G = G; A.P.k = k; A.P.beam = beam; A.P.visit_cap = visit_cap; A.P.target = target_level;
+  A.out_ids = out_ids; A.k_out = k_out; A.out_counts = out_counts; A.out_pages = out_pages;
+  A.pages_cap = pages_cap; A.out_npages = out_npages;
+  query_kernel<kSearchThreads><<<n, kSearchThreads, 0, st>>>(f->view, A, scratch, SL);
+  ICB_CUDA(cudaGetLastError());
+  return ICB_OK;
+}
