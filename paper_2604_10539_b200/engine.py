@@ -1,0 +1,342 @@
+"""Decode engine on the device: the drop-in for Engine.prefill / page_select /
+decode_step (/root/reference/pkg/src/icecache/engine.py:226-514).
+
+Layout: indexed layers (layer >= skip_layers) x kv heads form one forest of
+T = (L - skip) * H trees, tree t = (layer - skip) * H + h.  Skip layers keep
+their full K/V token-major in HBM and attend densely.  All per-step work of
+every indexed tree runs in a handful of batched kernel launches (rotation,
+window append, search + page union, paged attention), which the reference's
+semantics allow: its layers are independent within a step (the engine is
+not a transformer; every layer's q/k/v come from the workload stream).
+`layer_serial=True` processes one layer at a time instead (the latency a
+real model would see, reported separately).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import asdict, dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ConfigError, InputError
+from .forest import DeviceForest, ForestCaps, dense_attention
+
+
+@dataclass
+class EngineConfig:
+    """Field names and validation follow engine.py:37-92 verbatim; the last
+    three fields are device options."""
+
+    layers: int = 4
+    kv_heads: int = 2
+    query_heads_per_group: int = 1
+    d: int = 64
+    d_prime: int = 64
+    page_size: int = 16
+    token_budget: int = 64
+    promotion_ratio: float = 0.1
+    sink_pages: int = 1
+    window_pages: int = 2
+    skip_layers: int = 2
+    reuse_stride: int = 0
+    beam: int | None = None
+    visit_cap: int | None = None
+    seed: int = 0
+    scalar_bytes: int = 4
+    evaluate: bool = False
+    compare_baseline: bool = False
+    workers: int = 1
+    kv_dtype: str = "fp32"        # page K/V storage: "fp32" | "bf16"
+    max_tokens: int | None = None  # token capacity (prefill + decode); default prefill + 1024
+    layer_serial: bool = False
+
+    def __post_init__(self) -> None:
+        if min(self.layers, self.kv_heads, self.query_heads_per_group, self.d, self.d_prime) < 1:
+            raise ConfigError("layers, head counts and dims must be >= 1")
+        if self.page_size < 2:
+            raise ConfigError("page_size must be >= 2")
+        if self.token_budget < 1:
+            raise ConfigError("token_budget must be >= 1")
+        if not 0.0 < self.promotion_ratio < 1.0:
+            raise ConfigError("promotion_ratio must lie in (0, 1)")
+        if self.sink_pages < 1 or self.window_pages < 1:
+            raise ConfigError("sink_pages and window_pages must be >= 1")
+        if self.skip_layers < 0:
+            raise ConfigError("skip_layers must be >= 0")
+        if self.reuse_stride == 1 or self.reuse_stride < 0:
+            raise ConfigError("reuse_stride must be 0 (off) or >= 2")
+        if self.workers < 1:
+            raise ConfigError("workers must be >= 1")
+        if self.scalar_bytes < 1:
+            raise ConfigError("scalar_bytes must be >= 1")
+        if self.kv_dtype not in ("fp32", "bf16"):
+            raise ConfigError("kv_dtype must be fp32 or bf16")
+
+    @property
+    def n_query_heads(self) -> int:
+        return self.kv_heads * self.query_heads_per_group
+
+    def budget(self):
+        k = self.token_budget
+        return (k, self.beam if self.beam is not None else 2 * k,
+                self.visit_cap if self.visit_cap is not None else 4 * k)
+
+
+@dataclass
+class StepMetrics:
+    """engine.py:95-111 (oracle-only fields keep their defaults unless evaluate)."""
+
+    step: int
+    token_id: int
+    recall_at_k: float
+    page_hit_rate: float
+    covered_attention_mass: float
+    approx_rel_error: float
+    pages_selected: int
+    pages_loaded: int
+    tokens_loaded: int
+    bytes_moved: int
+    transactions: int
+    dci_queries: int
+    baseline_hit_rate: float | None = None
+
+
+def _dev(x, device, dtype=torch.float32):
+    return torch.as_tensor(x, dtype=dtype, device=device)
+
+
+class Engine:
+    def __init__(self, cfg: EngineConfig, device=None):
+        self.cfg = cfg
+        self.device = torch.device(device or "cuda")
+        self.prefilled = False
+        self.fallback = False
+        self.n_prefill = 0
+        self.steps_done = 0
+        self.sink_tokens: list[int] = []
+        self.indexed_tokens: list[int] = []
+        self.selection_queries = 0
+        self.forest: DeviceForest | None = None
+        self._win_fills: list[int] = []
+        self.last_pages = None
+        self.last_npages = None
+
+    # -- prefill ---------------------------------------------------------------
+    def prefill(self, keys, values, n_prefill: int) -> "Engine":
+        """keys [n, L, H, d], values [n, L, H, d'] (numpy or tensors; only the
+        first n_prefill tokens are read)."""
+        if self.prefilled:
+            raise ConfigError("engine already prefilled")
+        if n_prefill < 1:
+            raise ConfigError("prefill needs at least one token")
+        cfg = self.cfg
+        dev = self.device
+        keys = _dev(keys[:n_prefill], dev)
+        values = _dev(values[:n_prefill], dev)
+        if tuple(keys.shape[1:]) != (cfg.layers, cfg.kv_heads, cfg.d) or \
+                tuple(values.shape[1:]) != (cfg.layers, cfg.kv_heads, cfg.d_prime):
+            raise ConfigError("workload dims do not match the engine config")
+        self.n_prefill = n_prefill
+        self.max_tokens = cfg.max_tokens or (n_prefill + 1024)
+        s = cfg.page_size
+        pages = math.ceil(n_prefill / s)
+        self.fallback = pages < cfg.sink_pages + cfg.window_pages + 1 or cfg.skip_layers >= cfg.layers
+        self.n_dense = cfg.layers if self.fallback else cfg.skip_layers
+        kvt = torch.bfloat16 if cfg.kv_dtype == "bf16" else torch.float32
+        # dense mirror of skip layers (or every layer in fallback): [L_dense*H, max_tokens, d]
+        dpad = (cfg.d + 3) // 4 * 4
+        dvpad = (cfg.d_prime + 3) // 4 * 4
+        nd = self.n_dense * cfg.kv_heads
+        self.dense_k = torch.zeros((max(nd, 1), self.max_tokens, dpad), dtype=kvt, device=dev)
+        self.dense_v = torch.zeros((max(nd, 1), self.max_tokens, dvpad), dtype=kvt, device=dev)
+        if nd:
+            k = keys[:, : self.n_dense].permute(1, 2, 0, 3).reshape(nd, n_prefill, cfg.d)
+            v = values[:, : self.n_dense].permute(1, 2, 0, 3).reshape(nd, n_prefill, cfg.d_prime)
+            self.dense_k[:, :n_prefill, : cfg.d] = k.to(kvt)
+            self.dense_v[:, :n_prefill, : cfg.d_prime] = v.to(kvt)
+        if self.fallback:
+            self.prefilled = True
+            return self
+        sink_end = cfg.sink_pages * s
+        win_start = (pages - cfg.window_pages) * s
+        self.sink_tokens = list(range(sink_end))
+        self.indexed_tokens = list(range(sink_end, win_start))
+        Li = cfg.layers - cfg.skip_layers
+        H = cfg.kv_heads
+        T = Li * H
+        self.T = T
+        self.forest = DeviceForest(T, cfg.d, cfg.d_prime, tok_cap=self.max_tokens,
+                                   promotion_ratio=cfg.promotion_ratio, page_size=s,
+                                   kv_dtype=cfg.kv_dtype, device=dev,
+                                   caps=ForestCaps.for_tokens(self.max_tokens, cfg.promotion_ratio, s,
+                                                              extra_pages=cfg.sink_pages + 4 * cfg.window_pages
+                                                              + self.max_tokens // s))
+        f = self.forest
+        trees = list(range(T))
+        f.seed(trees, [(cfg.seed, cfg.skip_layers + t // H, t % H) for t in trees])
+        self.trees_dev = torch.arange(T, dtype=torch.int32, device=dev)
+        ki = keys[:, cfg.skip_layers:].permute(1, 2, 0, 3).reshape(T, n_prefill, cfg.d)
+        vi = values[:, cfg.skip_layers:].permute(1, 2, 0, 3).reshape(T, n_prefill, cfg.d_prime)
+        tok = torch.arange(n_prefill, dtype=torch.int32, device=dev)
+        # pages: sink ids 0.., window next, then indexed (engine.py:263-281)
+        f.alloc_resident(self.trees_dev, N.ROLE_SINK, cfg.sink_pages,
+                         tok[:sink_end].expand(T, -1), ki[:, :sink_end], vi[:, :sink_end])
+        wn = n_prefill - win_start
+        f.alloc_resident(self.trees_dev, N.ROLE_WINDOW, cfg.window_pages,
+                         tok[win_start:].expand(T, -1), ki[:, win_start:], vi[:, win_start:])
+        self._win_fills = [min(s, max(0, wn - i * s)) for i in range(cfg.window_pages)]
+        self._win_start = [win_start + i * s for i in range(cfg.window_pages)]
+        chunk = max(1, min(T, (2 << 30) // max(1, (win_start - sink_end) * 1200)))
+        for c0 in range(0, T, chunk):
+            c1 = min(T, c0 + chunk)
+            f.build(self.trees_dev[c0:c1], tok[sink_end:win_start].expand(c1 - c0, -1),
+                    ki[c0:c1, sink_end:win_start], vi[c0:c1, sink_end:win_start])
+        f.check()
+        k, beam, cap = cfg.budget()
+        self.k_eff = int(min(k, self.max_tokens))
+        self.beam, self.visit_cap = int(min(beam, 2**62)), int(min(cap, 2**62))
+        G = cfg.query_heads_per_group
+        self.pages_cap = int(min(f.caps.page_cap, G * self.k_eff))
+        self._alloc_step_buffers()
+        self.prefilled = True
+        return self
+
+    def _alloc_step_buffers(self):
+        cfg, dev, T = self.cfg, self.device, self.T
+        G = cfg.query_heads_per_group
+        self.ids = torch.empty((T, G, self.k_eff), dtype=torch.int32, device=dev)
+        self.counts = torch.empty((T, G), dtype=torch.int32, device=dev)
+        self.pages = torch.empty((T, max(1, self.pages_cap)), dtype=torch.int32, device=dev)
+        self.npages = torch.empty((T,), dtype=torch.int32, device=dev)
+        self.stats = torch.zeros((T, 5), dtype=torch.int64, device=dev)
+        self.rot_stats = torch.zeros((T, 2), dtype=torch.int64, device=dev)
+
+    # -- selection -------------------------------------------------------------
+    def page_select(self, q, layer: int, kv_head: int, budget=None) -> list[int]:
+        """Pages holding the tree's top-budget tokens for one query (engine.py:305-310)."""
+        tokens = self.select_tokens(q, layer, kv_head, budget)
+        ex_t2p = self.forest.export(self._tree(layer, kv_head))["tok2page"]
+        return sorted({int(ex_t2p[t]) for t in tokens})
+
+    def select_tokens(self, q, layer: int, kv_head: int, budget=None) -> list[int]:
+        t = self._tree(layer, kv_head)
+        k, beam, cap = budget if budget is not None else self.cfg.budget()
+        self.selection_queries += 1
+        q = _dev(q, self.device).reshape(1, 1, self.cfg.d)
+        ids, counts, _, _ = self.forest.query([t], q, k, beam, cap, want_pages=False)
+        self.forest.check()
+        return [int(x) for x in ids[0, 0, : int(counts[0, 0])].cpu().tolist()]
+
+    def _tree(self, layer, kv_head):
+        if self.fallback or layer < self.cfg.skip_layers or layer >= self.cfg.layers:
+            raise ConfigError(f"no tree for layer {layer}, head {kv_head}")
+        return (layer - self.cfg.skip_layers) * self.cfg.kv_heads + kv_head
+
+    # -- decode ------------------------------------------------------------------
+    def rotation_due(self) -> bool:
+        """engine.py:408-411: newest window page at fill >= s - 1."""
+        return (not self.fallback) and self._win_fills[-1] >= self.cfg.page_size - 1
+
+    def decode_step(self, token_id: int, queries, keys, values, *, metrics: bool = True, out=None):
+        """One decode token through every layer (engine.py:383-514).
+        queries [L, Hq, d], keys [L, H, d], values [L, H, d'].
+        Returns (outputs [L, Hq, d'] fp32 device tensor, StepMetrics | None)."""
+        if not self.prefilled:
+            raise ConfigError("decode_step before prefill")
+        cfg = self.cfg
+        token = self.n_prefill + self.steps_done
+        if token_id != token:
+            raise InputError(f"stream misaligned: expected token {token}, got {token_id}")
+        if token >= self.max_tokens:
+            raise ConfigError("token capacity exhausted (raise EngineConfig.max_tokens)")
+        dev = self.device
+        q = _dev(queries, dev)
+        kk = _dev(keys, dev)
+        vv = _dev(values, dev)
+        L, H, G = cfg.layers, cfg.kv_heads, cfg.query_heads_per_group
+        if out is None:
+            out = torch.empty((L, H * G, cfg.d_prime), dtype=torch.float32, device=dev)
+        rotate = self.rotation_due()
+        self._dense_part(q, kk, vv, token, out)
+        if not self.fallback:
+            if metrics:
+                self.stats.zero_()
+            self._indexed_part(q, kk, vv, token, rotate, out)
+            if rotate:
+                start, fill = self._win_start[0], self._win_fills[0]
+                self.indexed_tokens.extend(range(start, start + fill))
+                self._win_fills = self._win_fills[1:] + [0]
+                self._win_start = self._win_start[1:] + [token]
+            i = next(j for j, fl in enumerate(self._win_fills) if fl < cfg.page_size)
+            if self._win_fills[i] == 0:
+                self._win_start[i] = token
+            self._win_fills[i] += 1
+        self.steps_done += 1
+        m = None
+        if metrics:
+            m = self._metrics(token)
+        return out, m
+
+    def _dense_part(self, q, kk, vv, token, out):
+        cfg = self.cfg
+        nd = self.n_dense
+        if nd == 0:
+            return
+        H, G = cfg.kv_heads, cfg.query_heads_per_group
+        kvt = self.dense_k.dtype
+        self.dense_k[:, token, : cfg.d] = kk[:nd].reshape(nd * H, cfg.d).to(kvt)
+        self.dense_v[:, token, : cfg.d_prime] = vv[:nd].reshape(nd * H, cfg.d_prime).to(kvt)
+        qd = q[:nd].reshape(nd * H, G, cfg.d)
+        if cfg.d % 4:
+            qd = torch.nn.functional.pad(qd, (0, (4 - cfg.d % 4) % 4))
+        res = dense_attention(qd.contiguous(), self.dense_k, self.dense_v, token + 1)
+        out[:nd] = res[:, :, : cfg.d_prime].reshape(nd, H * G, cfg.d_prime)
+
+    def _indexed_part(self, q, kk, vv, token, rotate, out):
+        cfg, f = self.cfg, self.forest
+        s0, H, G = cfg.skip_layers, cfg.kv_heads, cfg.query_heads_per_group
+        T = self.T
+        qi = q[s0:].reshape(T, G, cfg.d)
+        ki = kk[s0:].reshape(T, cfg.d)
+        vi = vv[s0:].reshape(T, cfg.d_prime)
+        k = self.k_eff
+        groups = [(0, T)] if not cfg.layer_serial else [(l * H, (l + 1) * H) for l in range(T // H)]
+        for a, b in groups:
+            trees = self.trees_dev[a:b]
+            if rotate:
+                f.rotate_window(trees, cfg.scalar_bytes, self.rot_stats[a:b])
+            f.append_window(trees, token, ki[a:b], vi[a:b])
+            f.query(trees, qi[a:b], k, self.beam, self.visit_cap, k_out=k, pages_cap=self.pages_cap,
+                    out=(self.ids[a:b], self.counts[a:b], self.pages[a:b], self.npages[a:b]))
+            o = f.attention(trees, qi[a:b], self.pages[a:b], self.npages[a:b], stats=self.stats[a:b],
+                            scalar_bytes=cfg.scalar_bytes)
+            out[s0 + a // H: s0 + b // H] = o.reshape((b - a) // H, H * G, cfg.d_prime)
+        self.selection_queries += T * G
+
+    def _metrics(self, token) -> StepMetrics:
+        cfg = self.cfg
+        if self.fallback:
+            st = [0] * 5
+            dq = 0
+        else:
+            self.forest.check()
+            st = self.stats.sum(0).tolist()
+            dq = self.T * cfg.query_heads_per_group
+        return StepMetrics(step=self.steps_done - 1, token_id=token, recall_at_k=1.0, page_hit_rate=1.0,
+                           covered_attention_mass=1.0, approx_rel_error=0.0, pages_selected=int(st[0]),
+                           pages_loaded=int(st[2]), tokens_loaded=int(st[1]), bytes_moved=int(st[3]),
+                           transactions=int(st[4]), dci_queries=dq)
+
+    def selected(self):
+        """Last step's per-tree (ranked ids per head, union pages) on the host."""
+        ids = self.ids.cpu().numpy()
+        counts = self.counts.cpu().numpy()
+        pages = self.pages.cpu().numpy()
+        npages = self.npages.cpu().numpy()
+        return ids, counts, pages, npages
+
+    def config_dict(self):
+        return asdict(self.cfg)

@@ -1,0 +1,76 @@
+"""End-to-end decode parity: the device Engine against the oracle engine
+(pinned to the reference's golden engine runs) -- ranked top-k per query
+head and union pages bit-exact, step metrics equal, outputs within the
+north-star tolerance.  Covers prefill layout, window rotation + device
+inserts, skip layers (dense) and GQA groups."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle.engine import OConfig, OracleEngine
+from oracle.workload import Spec, generate
+
+pytestmark = pytest.mark.gpu
+
+KEYS = ("pages_selected", "pages_loaded", "tokens_loaded", "bytes_moved", "transactions", "dci_queries")
+
+
+def _run(name, kv="fp32", tol=1e-3, layer_serial=False, steps=None):
+    from paper_2604_10539_b200.engine import Engine, EngineConfig
+    z, meta = load_golden(f"engine_{name}.npz")
+    sk, ck = meta["spec"], meta["cfg"]
+    keys, values, queries, _ = generate(Spec(kind="clustered", **sk))
+    shape = dict(layers=sk["layers"], kv_heads=sk["kv_heads"], query_heads_per_group=sk["query_heads_per_group"],
+                 d=sk["d"], d_prime=sk["d_prime"], seed=sk["seed"])
+    ocfg = OConfig(**shape, **ck)
+    n0 = meta["n_prefill"]
+    steps = steps or meta["steps"]
+    oeng = OracleEngine(ocfg).prefill(keys, values, n0)
+    eng = Engine(EngineConfig(**shape, **ck, kv_dtype=kv, max_tokens=n0 + steps + 1,
+                              layer_serial=layer_serial)).prefill(keys, values, n0)
+    G = ocfg.query_heads_per_group
+    H = ocfg.kv_heads
+    for t in range(steps):
+        tok = n0 + t
+        oout, om, trace = oeng.decode_step(tok, queries[tok], keys[tok], values[tok])
+        out, m = eng.decode_step(tok, queries[tok], keys[tok], values[tok])
+        for k in KEYS:
+            assert getattr(m, k) == om[k], (t, k)
+            assert om[k] == meta["rows"][t][k]       # oracle still on the reference's numbers
+        ids, counts, pages, npages = eng.selected()
+        for layer in range(ocfg.skip_layers, ocfg.layers):
+            for h in range(H):
+                tr = (layer - ocfg.skip_layers) * H + h
+                for g in range(G):
+                    want = trace["tokens"][(layer, h * G + g)]
+                    assert list(ids[tr, g, :counts[tr, g]]) == want, (t, layer, h, g)
+                assert list(pages[tr, :npages[tr]]) == trace["pages"][(layer, h)], (t, layer, h)
+        o = out.cpu().numpy()
+        err = np.linalg.norm(o - oout, axis=-1) / np.linalg.norm(oout, axis=-1)
+        assert err.max() < tol, (t, err.max())
+        ref = z["outputs"][t]
+        assert (np.linalg.norm(o - ref, axis=-1) / np.linalg.norm(ref, axis=-1)).max() < tol
+    return eng, oeng
+
+
+def test_engine_mini_fp32(cuda_ok):
+    _run("mini")
+
+
+def test_engine_mini_bf16(cuda_ok):
+    _run("mini", kv="bf16", tol=1e-2)
+
+
+def test_engine_mini_layer_serial(cuda_ok):
+    _run("mini", layer_serial=True, steps=18)
+
+
+def test_engine_c1(cuda_ok):
+    eng, oeng = _run("c1")
+    # tree structure after the step-0 rotation (16 device inserts per tree)
+    for h in range(8):
+        ex = eng.forest.export(h)
+        ot = oeng.heads[(0, h)].tree.export()
+        assert [tuple(n[:4]) + (n[4],) for n in ex["nodes"]] == \
+            [(i, lv, par, own, mem) for i, lv, par, own, mem, _ in ot["nodes"]]
