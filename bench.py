@@ -1,0 +1,403 @@
+"""IceCache decode hot path on B200 -- the driver's benchmark.
+
+Workload (BASELINE.json configs[1], "C2"): Llama-3.1-8B-shaped decode, 32
+layers (first 2 dense "skip" layers, 30 DCI-indexed), GQA 32 q / 8 kv heads,
+d = d' = 128, 32k-token context, 256-token budget (beam 512, visit cap 1024),
+page size 16, bf16 page K/V, fp32 lifted keys.  Synthetic clustered q/k/v
+streams drawn on the device (reference workload distribution, random init).
+
+A "step" = one decode token through every layer: window rotation (every 16
+tokens, 16 device inserts per tree), window append, DCI search for 32 query
+heads per layer + GQA page union, sparse paged attention, dense attention of
+the skip layers.  Metric: decode tokens/s.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+One process per GPU (torchrun for N > 1): each rank decodes its own sequence
+(sequence-parallel, no collective), value = tokens of all ranks / max rank
+time.  `--impl reference` times the CPU port of the reference algorithm
+(oracle/, NumPy + C) on the host cores on a bounded sample of the same
+workload and prints the same JSON line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+E2E_STEPS = 16
+METRIC = "decode tokens/s (TPOT) at 32k ctx, 256-token budget; DCI top-k query µs/head"
+C2 = dict(layers=32, kv_heads=8, query_heads_per_group=4, d=128, d_prime=128, page_size=16,
+          token_budget=256, promotion_ratio=0.1, sink_pages=1, window_pages=2, skip_layers=2)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=16)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ctx", type=int, default=32768)
+    ap.add_argument("--kv", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--layer-serial", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seed", type=int, default=0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for nm_, v in zip(names, p[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm_)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, rank, world):
+    import numpy as np
+    import torch
+
+    from paper_2604_10539_b200 import _native as N
+    from paper_2604_10539_b200.engine import Engine, EngineConfig
+    from paper_2604_10539_b200.workload import clustered_stream
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    K, W = args.steps, args.warmup
+    n0 = args.ctx
+    total_steps = W + K + E2E_STEPS + 1
+    stream = clustered_stream(n0, total_steps, C2["layers"], C2["kv_heads"], C2["query_heads_per_group"],
+                              C2["d"], C2["d_prime"], seed=args.seed + rank, device=dev)
+    cfg = EngineConfig(**C2, seed=args.seed + rank, kv_dtype=args.kv, max_tokens=n0 + total_steps + 1,
+                       layer_serial=args.layer_serial)
+    t0 = time.time()
+    eng = Engine(cfg, device=dev).prefill(stream.keys, stream.values, n0)
+    torch.cuda.synchronize()
+    prefill_s = time.time() - t0
+    # per-step inputs resident in HBM (value) / pinned host (e2e)
+    q_all = stream.queries
+    k_all = stream.keys[n0:]
+    v_all = stream.values[n0:]
+    cur = torch.cuda.current_stream()
+
+    ev_q0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev_q1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev_a1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    launches = [0]
+    timing = {"i": None}
+    f = eng.forest
+    orig_query, orig_attn = f.query, f.attention
+
+    def q_wrap(*a, **kw):
+        i = timing["i"]
+        if i is not None:
+            ev_q0[i].record(cur)
+        r = orig_query(*a, **kw)
+        if i is not None:
+            ev_q1[i].record(cur)
+        launches[0] += 1
+        return r
+
+    def a_wrap(*a, **kw):
+        r = orig_attn(*a, **kw)
+        i = timing["i"]
+        if i is not None:
+            ev_a1[i].record(cur)
+        launches[0] += 1
+        return r
+
+    f.query, f.attention = q_wrap, a_wrap
+    out = torch.empty((C2["layers"], C2["kv_heads"] * C2["query_heads_per_group"], C2["d_prime"]),
+                      dtype=torch.float32, device=dev)
+
+    def step(i):
+        tok = n0 + i
+        rot = eng.rotation_due()
+        eng.decode_step(tok, q_all[i], k_all[i], v_all[i], metrics=False, out=out)
+        launches[0] += 2 + (1 if rot else 0)     # append + dense (+ rotation insert kernel)
+        return rot
+
+    for i in range(W):
+        step(i)
+    torch.cuda.synchronize()
+    info0 = [f.info(t) for t in range(eng.T)]
+    launches[0] = 0
+    rotations = 0
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        e0.record(cur)
+        for j in range(K):
+            timing["i"] = j
+            rotations += step(W + j)
+        timing["i"] = None
+        e1.record(cur)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    gpu_launches = launches[0]
+    info1 = [f.info(t) for t in range(eng.T)]
+    f.check()
+    ms_t = torch.tensor([ms], dtype=torch.float64)
+    if world > 1:
+        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    q_ms = [ev_q0[j].elapsed_time(ev_q1[j]) for j in range(K)]
+    a_ms = [ev_q1[j].elapsed_time(ev_a1[j]) for j in range(K)]
+    # algorithmic bytes of the search kernel: 4(d+1) U + 4 E per tree-step
+    rows = sum(b["rows_read"] - a["rows_read"] for a, b in zip(info0, info1))
+    rere = sum(b["owner_rereads"] - a["owner_rereads"] for a, b in zip(info0, info1))
+    evals = sum(b["distance_evals"] - a["distance_evals"] for a, b in zip(info0, info1))
+    U = rows - rere
+    search_bytes = (4 * (C2["d"] + 1) * U + 4 * evals) / K
+    search_s = statistics.mean(q_ms) / 1e3
+    peak, peak_kind = peaks()
+    achieved = search_bytes / search_s / 1e9
+    # attention bytes: sink + window + selected tokens, K and V rows, + dense skip layers
+    # (selected token counts from the last step's stats are not kept in the timed path)
+    tokens_per_s = world * K / (ms_max / 1e3)
+    heads = eng.T * C2["query_heads_per_group"]
+
+    # ---- e2e: the next steps through the public API with host (pinned) inputs/outputs
+    f.query, f.attention = orig_query, orig_attn
+    e2e_val = run_e2e(eng, stream, n0, W + K, E2E_STEPS, dev)
+
+    traffic = read_ncu_traffic()
+    res = {
+        "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "fp32 search keys / bf16 KV / fp32 accum" if args.kv == "bf16" else "fp32",
+        "data": "synthetic clustered q/k/v (reference workload distribution), random init, drawn on device",
+        "config": {"workload": "C2: Llama-3.1-8B-shaped decode, 32 layers (2 dense skip + 30 DCI-indexed), "
+                               "GQA 32q/8kv, d=128, 32k ctx, budget 256, page 16",
+                   "context": n0, "budget": 256, "beam": 512, "visit_cap": 1024, "page_size": 16,
+                   "layers": 32, "kv_heads": 8, "q_heads": 32, "sequences_per_gpu": 1,
+                   "parallelism": f"sequence-parallel x{world} (no collective)",
+                   "layer_mode": "layer-serial" if args.layer_serial else "layers batched per step",
+                   "rotations_in_timed_region": rotations,
+                   "l2": "per-step working set ~1.4 GB > 126 MB L2; no flush",
+                   "prefill_s": round(prefill_s, 2)},
+        "roofline": {"bound": "hbm", "kernel": "query_kernel (DCI search + top-k + page union)",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "alg_bytes_per_launch": search_bytes, "launch_ms": search_s * 1e3,
+                     "unique_rows_per_step": U / K, "evals_per_step": evals / K},
+        "dci_topk_us_per_head": search_s * 1e6 / heads,
+        "attention_ms_per_step": statistics.mean(a_ms),
+        "gpu_launches": gpu_launches,
+        "clocks": clk.summary(),
+        "e2e": e2e_val,
+    }
+    return res
+
+
+def run_e2e(eng, stream, n0, start, K2, dev):
+    """Same metric through Engine.decode_step with pinned host inputs (H2D)
+    and the step's outputs read back (D2H) inside the timed region."""
+    import torch
+    qh = stream.queries[start:start + K2].cpu().pin_memory()
+    kh = stream.keys[n0 + start:n0 + start + K2].cpu().pin_memory()
+    vh = stream.values[n0 + start:n0 + start + K2].cpu().pin_memory()
+    outh = torch.empty((K2,) + (qh.shape[1], qh.shape[2], stream.values.shape[-1]), dtype=torch.float32).pin_memory()
+    if eng.steps_done != start:
+        return None
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(K2):
+        tok = n0 + start + i
+        q = qh[i].to(dev, non_blocking=True)
+        k = kh[i].to(dev, non_blocking=True)
+        v = vh[i].to(dev, non_blocking=True)
+        out, _ = eng.decode_step(tok, q, k, v, metrics=False)
+        outh[i].copy_(out, non_blocking=True)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    h2d = (qh[0].numel() + kh[0].numel() + vh[0].numel()) * 4
+    d2h = outh[0].numel() * 4
+    return {"value": K2 / dt, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "steps": K2}
+
+
+def read_ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "search_traffic.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ CPU legs
+def cpu_sample(n_idx=32720, steps=4, G=4, seed=0, n_trees=1):
+    """Bounded sample of the same workload on the CPU port (oracle): build
+    n_trees 32k trees, then time `steps` decode group-steps (G-head search +
+    union + sparse attention) per tree; extrapolate to the full model."""
+    import numpy as np
+
+    from oracle import numerics as nm
+    from oracle.dci import SENTINEL, build
+    from oracle.engine import full_attention
+    from oracle.store import OStore
+    rng = np.random.default_rng(seed)
+    d = 128
+    centers = rng.normal(size=(32, d))
+    centers /= np.linalg.norm(centers, axis=1, keepdims=True)
+    keys = (centers[rng.integers(0, 32, n_idx)] + rng.normal(size=(n_idx, d)) * 0.1 / np.sqrt(d)).astype(
+        np.float32).astype(np.float64)
+    vals = (rng.normal(size=(n_idx, d)) / np.sqrt(d)).astype(np.float32).astype(np.float64)
+    t0 = time.time()
+    store = OStore(d, d)
+    tree = build([(i, keys[i]) for i in range(n_idx)], 0.1, seed=(seed, 2, 0), values=list(vals), store=store)
+    build_s = time.time() - t0
+    qs = (centers[rng.integers(0, 32, (steps, 1))] + rng.normal(size=(steps, G, d)) * 0.1 / np.sqrt(d)) * np.sqrt(d)
+    t0 = time.time()
+    qtime = 0.0
+    for s in range(steps):
+        pages = set()
+        tq = time.time()
+        for g in range(G):
+            toks = tree.query(nm.lift_query32(qs[s, g]), SENTINEL, 256, 512, 1024)
+            pages |= {store.token_to_page[t] for t in toks}
+        qtime += time.time() - tq
+        ks, vs = [], []
+        for p in sorted(pages):
+            ks += store.pages[p].keys
+            vs += store.pages[p].values
+        for g in range(G):
+            full_attention(qs[s, g], ks, vs)
+    group_s = (time.time() - t0) / steps
+    # dense skip layers: 2 layers x 8 heads x 4 q heads over 32k tokens
+    kd = rng.normal(size=(32768, d))
+    vd = rng.normal(size=(32768, d))
+    t1 = time.time()
+    for _ in range(4):
+        full_attention(qs[0, 0], kd, vd)
+    dense_head_s = (time.time() - t1) / 4
+    per_token = group_s * 240 + dense_head_s * 64
+    return {"tokens_per_s": 1.0 / per_token, "group_s": group_s, "query_us_per_head": qtime / steps / G * 1e6,
+            "build_s": build_s, "dense_head_s": dense_head_s}
+
+
+def run_reference(args):
+    """--impl reference: the CPU port of the reference algorithm on all host
+    cores: one process per core, each owning one (layer, kv head) tree."""
+    import multiprocessing as mp
+    ncores = len(os.sched_getaffinity(0))
+    nproc = max(1, min(ncores, 8))
+    ctx = mp.get_context("fork")
+    with ctx.Pool(nproc) as pool:
+        t0 = time.time()
+        res = pool.starmap(cpu_sample, [(32720, max(1, min(args.steps, 2)), 4, args.seed + i) for i in range(nproc)])
+        wall = time.time() - t0
+    group_s = statistics.mean(r["group_s"] for r in res)
+    dense = statistics.mean(r["dense_head_s"] for r in res)
+    per_token = group_s * 240 / nproc + dense * 64 / nproc
+    value = 1.0 / per_token
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_token * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 search / fp64 attention",
+            "data": "synthetic clustered (reference workload distribution)",
+            "config": {"workload": "C2 (bounded sample: one 32k (layer, kv head) group per process, "
+                                   "extrapolated x240 indexed groups + 64 dense heads)", "context": 32768,
+                       "budget": 256},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": nproc, "kind": "port",
+                             "sample": f"{nproc} x one 32k-token tree: build + {min(args.steps, 2)} decode group-steps "
+                                       f"each (G=4 search+union+attention), wall {wall:.1f}s"},
+            "dci_topk_us_per_head": statistics.mean(r["query_us_per_head"] for r in res),
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        return
+    if world > 1:
+        import torch
+        torch.distributed.init_process_group("gloo")
+    res = run_ours(args, rank, world)
+    if rank == 0 and not args.no_cpu_baseline:
+        cb = cpu_sample()
+        res["cpu_baseline"] = {"value": cb["tokens_per_s"], "unit": "tokens/s", "cores": 1, "kind": "port",
+                               "sample": "one 32k-token (layer, kv head) tree built by the oracle, 4 decode "
+                                         "group-steps (G=4 search + union + attention) timed, x240 groups + "
+                                         f"64 dense heads; query {cb['query_us_per_head']:.0f} us/head, "
+                                         f"build {cb['build_s']:.1f}s"}
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -6,40 +6,66 @@
  * in fp64 with the operation order the device kernel `nn_parent_kernel`
  * uses: every dot product (and every squared norm) is one sequential chain of
  * fused multiply-adds over the lifted coordinates 0..dim-1, starting from +0.
- * Ties go to the first candidate (np.argmin).  Compile with -mfma
- * -ffp-contract=off so the only fusions are the explicit fma() calls.
+ * Ties go to the first candidate (np.argmin).  The loops run over candidates
+ * in the innermost position so the compiler vectorizes ACROSS independent
+ * dot products; each individual chain keeps its sequential order.
+ * Compile with -ffp-contract=off so the only fusions are the fma() calls.
  */
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 
-static double dot_fma(const double *a, const double *b, int dim) {
-    double acc = 0.0;
-    for (int t = 0; t < dim; ++t) acc = fma(a[t], b[t], acc);
-    return acc;
-}
+#define PB 4
 
-/* pts [np, dim], cands [nc, dim] row-major fp64 lifted rows (tail last). */
 void oracle_nn_parents(const double *pts, int64_t np_, const double *cands, int64_t nc,
                        int dim, int32_t *out) {
-    double *buf = (double *)malloc(sizeof(double) * (size_t)(nc > 0 ? nc : 1));
-    for (int64_t j = 0; j < nc; ++j) buf[j] = dot_fma(cands + j * dim, cands + j * dim, dim);
-    for (int64_t i = 0; i < np_; ++i) {
-        const double *p = pts + i * dim;
-        double best = 0.0; int32_t arg = -1;
-        for (int64_t j = 0; j < nc; ++j) {
-            double d2 = buf[j] - 2.0 * dot_fma(p, cands + j * dim, dim);
-            if (arg < 0 || d2 < best) { best = d2; arg = (int32_t)j; }
+    double *csq = (double *)malloc(sizeof(double) * (size_t)(nc > 0 ? nc : 1));
+    double *ct = (double *)malloc(sizeof(double) * (size_t)(nc > 0 ? nc : 1) * dim);
+    double *acc = (double *)malloc(sizeof(double) * (size_t)(nc > 0 ? nc : 1) * PB);
+    for (int64_t j = 0; j < nc; ++j) {
+        double a = 0.0;
+        for (int t = 0; t < dim; ++t) {
+            double c = cands[j * dim + t];
+            a = fma(c, c, a);
+            ct[(int64_t)t * nc + j] = c;
         }
-        out[i] = arg;
+        csq[j] = a;
     }
-    free(buf);
+    for (int64_t i0 = 0; i0 < np_; i0 += PB) {
+        int nb = (int)((np_ - i0) < PB ? (np_ - i0) : PB);
+        for (int b = 0; b < nb; ++b)
+            for (int64_t j = 0; j < nc; ++j) acc[b * nc + j] = 0.0;
+        for (int t = 0; t < dim; ++t) {
+            const double *crow = ct + (int64_t)t * nc;
+            for (int b = 0; b < nb; ++b) {
+                const double pv = pts[(i0 + b) * dim + t];
+                double *ab = acc + b * nc;
+                for (int64_t j = 0; j < nc; ++j) ab[j] = fma(pv, crow[j], ab[j]);
+            }
+        }
+        for (int b = 0; b < nb; ++b) {
+            double best = 0.0;
+            int32_t arg = -1;
+            for (int64_t j = 0; j < nc; ++j) {
+                double d2 = csq[j] - 2.0 * acc[b * nc + j];
+                if (arg < 0 || d2 < best) { best = d2; arg = (int32_t)j; }
+            }
+            out[i0 + b] = arg;
+        }
+    }
+    free(csq);
+    free(ct);
+    free(acc);
 }
 
 /* P-DCI projections dirs[m, dim] . vecs[n, dim] -> out[n, m]; same fma chain
- * as the device (`pdci_project`), restating `self.dirs @ vec` (dci.py:107,113). */
+ * as the device (`pdci_visit`), restating `self.dirs @ vec` (dci.py:107,113). */
 void oracle_project(const double *dirs, int m, const double *vecs, int64_t n, int dim,
                     double *out) {
     for (int64_t i = 0; i < n; ++i)
-        for (int j = 0; j < m; ++j) out[i * m + j] = dot_fma(dirs + (int64_t)j * dim, vecs + i * dim, dim);
+        for (int j = 0; j < m; ++j) {
+            double a = 0.0;
+            for (int t = 0; t < dim; ++t) a = fma(dirs[(int64_t)j * dim + t], vecs[i * dim + t], a);
+            out[i * m + j] = a;
+        }
 }

@@ -247,7 +247,7 @@ int icb_tree_info(icb_forest* f, int32_t tree, int64_t* out) {
   ICB_CUDA(cudaMemcpy(&m, f->view.meta + tree, sizeof(TreeMeta), cudaMemcpyDeviceToHost));
   int64_t v[16] = {m.levels, m.top_node, m.n_nodes, m.next_page, m.n_points, m.err, m.n_window, m.n_sink,
                    (int64_t)m.query_count, (int64_t)m.distance_evals, (int64_t)m.scale_clamps, m.member_top,
-                   m.own_top, m.n_dirs, 0, 0};
+                   m.own_top, m.n_dirs, (int64_t)m.rows_read, (int64_t)m.owner_rereads};
   std::memcpy(out, v, sizeof(v));
   return ICB_OK;
 }

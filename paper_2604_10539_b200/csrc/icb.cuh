@@ -55,6 +55,8 @@ struct TreeMeta {
   double c;          // KeyScale.c
   Pcg64 rng;         // level stream (spawn_key=(0,)), continues across inserts
   unsigned long long query_count, distance_evals, scale_clamps;
+  unsigned long long rows_read;      // lifted rows streamed by the search (union of heads)
+  unsigned long long owner_rereads;  // rows re-read because a survivor heads its own child node
 };
 
 struct ForestView {

@@ -376,12 +376,15 @@ __device__ void tree_search(SearchSmem& S, const ForestView& F, const SearchScra
     for (int g = 0; g < G; ++g)
       if (S.M[g] > SS.ccap) { if (tid == 0) set_err(F.meta + t, ICB_ERR_CAP_SCRATCH); return; }
     // (3) evaluate normal nodes: one warp per node, 4 rows in flight
+    if (tid == 0) S.misc[5] = 0;
+    __syncthreads();
     for (int i = warp; i < U; i += NT / 32) {
       const int node = SS.ulist[i];
       const unsigned mk = (unsigned)SS.umask[i];
       const size_t x = F.nd(t, node);
       const int sz = F.node_size[x];
       if (sz > ICB_EXHAUSTIVE && (long long)sz > P.visit_cap) continue;
+      if (lane == 0) atomicAdd(&S.misc[5], sz);
       const int off = F.node_off[x];
       int ob[ICB_MAX_G];
       for (int g = 0; g < G; ++g) ob[g] = SS.uoff[(size_t)g * F.node_cap + i];
@@ -423,7 +426,7 @@ __device__ void tree_search(SearchSmem& S, const ForestView& F, const SearchScra
           if (S.M[g] + cnt > SS.ccap) { if (tid == 0) set_err(F.meta + t, ICB_ERR_CAP_SCRATCH); return; }
           eval_list_one_head<NT>(S, F, t, SS.vis, cnt, g, SS.cand + (size_t)g * SS.ccap + S.M[g]);
           __syncthreads();
-          if (tid == 0) S.M[g] += cnt;
+          if (tid == 0) { S.M[g] += cnt; S.misc[5] += cnt; }
           __syncthreads();
         }
       }
@@ -433,6 +436,8 @@ __device__ void tree_search(SearchSmem& S, const ForestView& F, const SearchScra
       unsigned long long ev = 0;
       for (int g = 0; g < G; ++g) ev += S.M[g];
       atomicAdd(&F.meta[t].distance_evals, ev);
+      atomicAdd(&F.meta[t].rows_read, (unsigned long long)S.misc[5]);
+      if (lv < L) atomicAdd(&F.meta[t].owner_rereads, (unsigned long long)U);
     }
     if (lv < L)
       for (int i = tid; i < U; i += NT) SS.nmask[SS.ulist[i]] = 0u;

@@ -224,7 +224,8 @@ class DeviceForest:
         out = np.zeros(16, dtype=np.int64)
         N.check(N.lib().icb_tree_info(self.h, int(tree), out.ctypes.data_as(ctypes.c_void_p)))
         keys = ["levels", "top_node", "n_nodes", "next_page", "n_points", "err", "n_window", "n_sink",
-                "query_count", "distance_evals", "scale_clamps", "member_top", "own_top", "n_dirs"]
+                "query_count", "distance_evals", "scale_clamps", "member_top", "own_top", "n_dirs",
+                "rows_read", "owner_rereads"]
         return {k: int(v) for k, v in zip(keys, out)}
 
     def scale(self, tree: int) -> float:
