@@ -66,13 +66,17 @@ __global__ void build_lift_kernel(ForestView F, BuildArgs A, const double* nsq) 
   const bool over = norm > c;
   const double safe = over ? norm : c;
   const float* k = A.keys + ((size_t)b * A.n_points + i) * F.dim;
-  float* row = F.lift + F.tk(t, tok) * ICB_DPAD;
+  float* row = F.lift + F.tk(t, tok) * ICB_ROWF;
   for (int j = lane; j < ICB_DPAD; j += 32)
     row[j] = j < F.dim ? __double2float_rn(__ddiv_rn((double)k[j], safe)) : 0.0f;
+  if (lane < ICB_ROWF - ICB_DPAD) row[ICB_DPAD + lane] = 0.0f;
+  __syncwarp();
   if (lane == 0) {
     double ratio = __ddiv_rn(norm, safe);
     double rad = __dsub_rn(1.0, __dmul_rn(ratio, ratio));
-    F.tail[F.tk(t, tok)] = __double2float_rn(sqrt(rad > 0.0 ? rad : 0.0));
+    const float tl = __double2float_rn(sqrt(rad > 0.0 ? rad : 0.0));
+    F.tail[F.tk(t, tok)] = tl;
+    row[ICB_DPAD] = tl;
     if (over) atomicAdd(&m->scale_clamps, 1ull);
     int old = atomicCAS(F.tok2page + F.tk(t, tok), -1, -2);
     if (old != -1) set_err(m, ICB_ERR_DUP_ID);

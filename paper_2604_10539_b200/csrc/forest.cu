@@ -99,7 +99,7 @@ int icb_forest_create(const icb_forest_config* cfg, icb_forest** out) {
   int rc = ICB_OK;
 #define AL(ptr, n, fb) if (rc == ICB_OK) rc = falloc(f, &ptr, n, fb)
   AL(F.meta, T, 0);
-  AL(F.lift, T * c.tok_cap * ICB_DPAD, 0);
+  AL(F.lift, T * c.tok_cap * ICB_ROWF, 0);
   AL(F.tail, T * c.tok_cap, 0);
   AL(F.level, T * c.tok_cap, 0);
   AL(F.own_base, T * c.tok_cap, 0);
@@ -306,7 +306,7 @@ int icb_export_tree(icb_forest* f, int32_t tree, int32_t* node_level, int32_t* n
   CP(level, F.level + t * c.tok_cap, c.tok_cap);
   CP(own_base, F.own_base + t * c.tok_cap, c.tok_cap);
   CP(own_list, F.own_list + t * c.own_cap, c.own_cap);
-  CP(lift, F.lift + t * c.tok_cap * ICB_DPAD, (size_t)c.tok_cap * ICB_DPAD);
+  CP(lift, F.lift + t * c.tok_cap * ICB_ROWF, (size_t)c.tok_cap * ICB_ROWF);
   CP(tail, F.tail + t * c.tok_cap, c.tok_cap);
 #undef CP
   TreeMeta m;

@@ -12,7 +12,30 @@
 #include "rng.cuh"
 #include "../../include/icecache_b200.h"
 
-#define ICB_DPAD 128          // device row width; dims >= d are zero
+// Debug builds (-DICB_DEBUG=1, make debug) bounds-check every scratch index
+// and trap with a message; release builds compile the checks away.
+#ifndef ICB_DEBUG
+#define ICB_DEBUG 0
+#endif
+#if ICB_DEBUG
+#include <cstdio>
+#define ICB_CHECK(cond, ...)                                                   \
+  do {                                                                         \
+    if (!(cond)) {                                                             \
+      printf("ICB_CHECK %s:%d (%s) ", __FILE__, __LINE__, #cond);              \
+      printf(__VA_ARGS__);                                                     \
+      printf("\n");                                                            \
+      __trap();                                                                \
+    }                                                                          \
+  } while (0)
+#else
+#define ICB_CHECK(cond, ...) \
+  do {                       \
+  } while (0)
+#endif
+
+#define ICB_DPAD 128          // key dims held per row; dims >= d are zero
+#define ICB_ROWF 132          // row stride in floats: [128 dims | tail | 3 zero] = 528 B, one bulk copy
 #define ICB_NPROJ 8           // NUM_PROJECTIONS (dci.py:44)
 #define ICB_EXHAUSTIVE 64     // EXHAUSTIVE_NODE_LIMIT (dci.py:41)
 #define ICB_MAX_WINDOW 8
@@ -92,7 +115,7 @@ struct ForestView {
   __device__ __forceinline__ size_t nd(int t, int n) const { return (size_t)t * node_cap + n; }
   __device__ __forceinline__ size_t pg(int t, int p) const { return (size_t)t * page_cap + p; }
   __device__ __forceinline__ const float* row(int t, int tok) const {
-    return lift + ((size_t)t * tok_cap + tok) * ICB_DPAD;
+    return lift + ((size_t)t * tok_cap + tok) * ICB_ROWF;
   }
   __device__ __forceinline__ int own(int t, int p, int lv) const {
     return own_list[(size_t)t * own_cap + own_base[tk(t, p)] + lv - 1];
@@ -187,6 +210,43 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* sm /* >= NT/32+1
 }
 
 __device__ __forceinline__ void set_err(TreeMeta* m, int bit) { atomicOr(&m->err, bit); }
+
+// ---------------------------------------------------------------------------
+// mbarrier + TMA bulk copy (cp.async.bulk) helpers
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D TMA bulk copy global -> shared, completion counted on `bar` (bytes).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 
 template <typename KT>
 __device__ __forceinline__ void store_kv(KT* dst, float v);

@@ -20,7 +20,6 @@
 
 namespace icb {
 
-struct SlotLayout;
 
 struct InsertArgs {
   const int32_t* trees;
@@ -107,7 +106,7 @@ __device__ void write_slot(const ForestView& F, int t, int page, int slot, const
 // One insert; all threads of the block participate.  key: fp32 raw key
 // (global); returns the level (valid in thread 0).
 template <int NT>
-__device__ int insert_one(SearchSmem& S, const ForestView& F, const SearchScratch& SS, int t, int tok,
+__device__ int insert_one(SearchSmem& S, GroupSmem* GSA, const RingView& RG, const ForestView& F, const SearchScratch& SS, int t, int tok,
                           const float* key, const float* val, long long src_slot, int given_level,
                           double* dirs_tmp) {
   TreeMeta* m = F.meta + t;
@@ -142,7 +141,7 @@ __device__ int insert_one(SearchSmem& S, const ForestView& F, const SearchScratc
   const double c = m->c, norm = s_norm;
   const bool over = norm > c;
   const double safe = over ? norm : c;
-  float* row = F.lift + F.tk(t, tok) * ICB_DPAD;
+  float* row = F.lift + F.tk(t, tok) * ICB_ROWF;
   // read the raw key before overwriting (it may live in this very row)
   float kv = tid < F.dim ? key[tid] : 0.f;
   __syncthreads();
@@ -151,11 +150,13 @@ __device__ int insert_one(SearchSmem& S, const ForestView& F, const SearchScratc
     row[u] = v;
     S.q[0][u] = v;
   }
+  if (tid > 0 && tid < ICB_ROWF - ICB_DPAD) row[ICB_DPAD + tid] = 0.0f;
   if (tid == 0) {
     double ratio = __ddiv_rn(norm, safe);
     double rad = __dsub_rn(1.0, __dmul_rn(ratio, ratio));
     float tl = __double2float_rn(sqrt(rad > 0.0 ? rad : 0.0));
     F.tail[F.tk(t, tok)] = tl;
+    row[ICB_DPAD] = tl;
     S.qt[0] = tl;
     if (over) m->scale_clamps += 1;
     F.level[F.tk(t, tok)] = (int8_t)s_level;
@@ -199,10 +200,10 @@ __device__ int insert_one(SearchSmem& S, const ForestView& F, const SearchScratc
     } else {
       SearchParams P;
       P.G = 1; P.k = 1; P.beam = 8; P.visit_cap = 64; P.target = level + 1;
-      tree_search<NT>(S, F, SS, t, P, dirs_tmp);
-      int n = finalize_head<NT>(S, F, SS, 0, 1);
+      tree_search<NT, 1>(S, GSA, RG, F, SS, t, P, dirs_tmp);
+      int n = finalize_groups<NT, 1>(S, GSA, F, SS, 1, 1);
       if (tid == 0) {
-        int parent = n > 0 ? key_id(S.sortbuf[0]) : -1;
+        int parent = n > 0 ? key_id(GSA[0].buf[0]) : -1;
         s_container = parent >= 0 ? F.own(t, parent, level) : m->top_node;
         s_chain_from = level - 1;
       }
@@ -249,29 +250,18 @@ __device__ int insert_one(SearchSmem& S, const ForestView& F, const SearchScratc
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT) insert_kernel(ForestView F, InsertArgs A, char* scratch, size_t slot_bytes,
-                                                    size_t off_cand, size_t off_pool, size_t off_surv,
-                                                    size_t off_ulist, size_t off_umask, size_t off_uoff,
-                                                    size_t off_nmask, size_t off_seen, size_t off_vis,
-                                                    size_t off_proj, size_t off_ekey, size_t off_dirs) {
+__global__ void __launch_bounds__(NT, 1) insert_kernel(ForestView F, InsertArgs A, char* scratch, SlotLayout SL) {
   __shared__ SearchSmem S;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  GroupSmem* GSA = reinterpret_cast<GroupSmem*>(dsm);
+  const RingView RG = ring_view(dsm, 1);
+  if (threadIdx.x == 0) S.sortbuf = reinterpret_cast<unsigned long long*>(RG.ring);
+  ring_init(RG);
   const int b = blockIdx.x;
   const int t = A.trees[b];
-  char* base = scratch + (size_t)b * slot_bytes;
-  SearchScratch SS;
-  SS.cand = (unsigned long long*)(base + off_cand);
-  SS.pool = (unsigned long long*)(base + off_pool);
-  SS.surv = (int*)(base + off_surv);
-  SS.ulist = (int*)(base + off_ulist);
-  SS.umask = (int*)(base + off_umask);
-  SS.uoff = (int*)(base + off_uoff);
-  SS.nmask = (unsigned*)(base + off_nmask);
-  SS.seen = (unsigned*)(base + off_seen);
-  SS.vis = (int*)(base + off_vis);
-  SS.proj = (double*)(base + off_proj);
-  SS.ekey = (unsigned long long*)(base + off_ekey);
-  SS.ccap = F.tok_cap;
-  double* dirs_tmp = (double*)(base + off_dirs);
+  double* dirs_tmp;
+  unsigned* pbits;
+  SearchScratch SS = slot_scratch(scratch + (size_t)b * SL.total, SL, F.tok_cap, &dirs_tmp, &pbits);
   TreeMeta* m = F.meta + t;
   if (A.from_window) {
     __shared__ int s_old, s_fill;
@@ -289,8 +279,8 @@ __global__ void __launch_bounds__(NT) insert_kernel(ForestView F, InsertArgs A, 
     if (old < 0) return;
     for (int e = 0; e < s_fill; ++e) {
       int tok = F.page_tok[F.pg(t, old) * F.s + e];
-      const float* raw = F.lift + F.tk(t, tok) * ICB_DPAD;   // stashed raw key
-      insert_one<NT>(S, F, SS, t, tok, raw, nullptr, (long long)(F.pg(t, old) * F.s + e), 0, dirs_tmp);
+      const float* raw = F.lift + F.tk(t, tok) * ICB_ROWF;   // stashed raw key
+      insert_one<NT>(S, GSA, RG, F, SS, t, tok, raw, nullptr, (long long)(F.pg(t, old) * F.s + e), 0, dirs_tmp);
     }
     if (threadIdx.x == 0) {
       // release (pagestore.py:157-162) then a fresh window page
@@ -311,7 +301,7 @@ __global__ void __launch_bounds__(NT) insert_kernel(ForestView F, InsertArgs A, 
     size_t x = (size_t)b * A.m + e;
     int tok = A.tokens[x];
     int lv = A.levels ? A.levels[x] : 0;
-    int got = insert_one<NT>(S, F, SS, t, tok, A.keys + x * F.dim, A.values ? A.values + x * F.dim_v : nullptr,
+    int got = insert_one<NT>(S, GSA, RG, F, SS, t, tok, A.keys + x * F.dim, A.values ? A.values + x * F.dim_v : nullptr,
                              -1, lv, dirs_tmp);
     if (threadIdx.x == 0 && A.out_levels) A.out_levels[x] = got;
   }
@@ -340,7 +330,7 @@ __global__ void append_window_kernel(ForestView F, const int32_t* trees, int n, 
   __syncthreads();
   if (s_page < 0 || token < 0 || token >= F.tok_cap) return;
   const float* k = keys + (size_t)b * F.dim;
-  float* stash = F.lift + F.tk(t, token) * ICB_DPAD;
+  float* stash = F.lift + F.tk(t, token) * ICB_ROWF;
   for (int j = threadIdx.x; j < F.dim; j += blockDim.x) stash[j] = k[j];
   if (threadIdx.x < 32) write_slot(F, t, s_page, s_slot, k, values + (size_t)b * F.dim_v, -1);
 }
@@ -376,7 +366,7 @@ __global__ void resident_pages_kernel(ForestView F, const int32_t* trees, int n,
     const float* k = keys + ((size_t)b * n_tokens + e) * F.dim;
     if ((threadIdx.x & 31) == 0) F.page_tok[F.pg(t, page) * F.s + slot] = tok;
     if (tok >= 0 && tok < F.tok_cap) {
-      float* stash = F.lift + F.tk(t, tok) * ICB_DPAD;
+      float* stash = F.lift + F.tk(t, tok) * ICB_ROWF;
       for (int j = threadIdx.x & 31; j < F.dim; j += 32) stash[j] = k[j];
     }
     write_slot(F, t, page, slot, k, values + ((size_t)b * n_tokens + e) * F.dim_v, -1);
@@ -387,32 +377,9 @@ __global__ void resident_pages_kernel(ForestView F, const int32_t* trees, int n,
 
 using namespace icb;
 
-// scratch layout shared with search.cu (same field order)
-struct InsLayout {
-  size_t cand, pool, surv, ulist, umask, uoff, nmask, seen, vis, proj, ekey, dirs, total;
-};
-static size_t al256h(size_t x) { return (x + 255) & ~(size_t)255; }
-static InsLayout ins_layout(const icb_forest_config& c) {
-  InsLayout L{};
-  size_t o = 0, cc = (size_t)c.tok_cap;
-  L.cand = o; o = al256h(o + cc * 8);
-  L.pool = o; o = al256h(o + cc * 8);
-  L.surv = o; o = al256h(o + cc * 4);
-  L.ulist = o; o = al256h(o + (size_t)c.node_cap * 4);
-  L.umask = o; o = al256h(o + (size_t)c.node_cap * 4);
-  L.uoff = o; o = al256h(o + (size_t)c.node_cap * 4);
-  L.nmask = o; o = al256h(o + (size_t)c.node_cap * 4);
-  L.seen = o; o = al256h(o + (size_t)(c.tok_cap / 32 + 1) * 4);
-  L.vis = o; o = al256h(o + cc * 4);
-  L.proj = o; o = al256h(o + cc * ICB_NPROJ * 8);
-  L.ekey = o; o = al256h(o + cc * 16);
-  L.dirs = o; o = al256h(o + (size_t)ICB_NPROJ * (c.dim + 1) * 8);
-  L.total = o;
-  return L;
-}
-
-int ensure_insert_scratch(icb_forest* f, int n, char** out, InsLayout* lay) {
-  InsLayout L = ins_layout(f->cfg);
+int ensure_insert_scratch(icb_forest* f, int n, char** out, SlotLayout* lay) {
+  const auto& c = f->cfg;
+  SlotLayout L = slot_layout(1, c.tok_cap, c.node_cap, c.page_cap, c.dim);
   size_t need = L.total * (size_t)n;
   if (need > f->iscratch_bytes) {
     if (f->iscratch) ICB_CUDA(cudaFree(f->iscratch));
@@ -432,16 +399,16 @@ int icb_insert_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t m, c
                     int from_window, int32_t scalar_bytes, int64_t* stats, cudaStream_t st) {
   if (n <= 0) return ICB_OK;
   char* scratch;
-  InsLayout L;
+  SlotLayout L;
   int rc = ensure_insert_scratch(f, n, &scratch, &L);
   if (rc) return rc;
   InsertArgs A{};
   A.trees = trees; A.n = n; A.m = m; A.tokens = tokens; A.keys = keys; A.values = values;
   A.levels = levels; A.out_levels = out_levels; A.from_window = from_window;
   A.scalar_bytes = scalar_bytes; A.stats = stats;
-  insert_kernel<kSearchThreads><<<n, kSearchThreads, 0, st>>>(f->view, A, scratch, L.total, L.cand, L.pool,
-                                                              L.surv, L.ulist, L.umask, L.uoff, L.nmask,
-                                                              L.seen, L.vis, L.proj, L.ekey, L.dirs);
+  ICB_CUDA(cudaFuncSetAttribute(insert_kernel<kSearchThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)search_dsm_bytes(1)));
+  insert_kernel<kSearchThreads><<<n, kSearchThreads, search_dsm_bytes(1), st>>>(f->view, A, scratch, L);
   ICB_CUDA(cudaGetLastError());
   return ICB_OK;
 }

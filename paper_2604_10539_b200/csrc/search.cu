@@ -19,54 +19,6 @@ struct QueryArgs {
   int32_t* out_npages;
 };
 
-// Scratch slot b carved from one buffer.
-struct SlotLayout {
-  size_t cand, pool, surv, ulist, umask, uoff, nmask, seen, vis, proj, ekey, pbits, dirs, total;
-};
-
-__host__ __device__ inline size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
-
-__host__ __device__ inline SlotLayout slot_layout(int G, int tok_cap, int node_cap, int page_cap, int dim) {
-  SlotLayout L{};
-  size_t o = 0;
-  size_t cc = (size_t)tok_cap;
-  L.cand = o; o = al256(o + (size_t)G * cc * 8);
-  L.pool = o; o = al256(o + (size_t)G * cc * 8);
-  L.surv = o; o = al256(o + (size_t)G * cc * 4);
-  L.ulist = o; o = al256(o + (size_t)node_cap * 4);
-  L.umask = o; o = al256(o + (size_t)node_cap * 4);
-  L.uoff = o; o = al256(o + (size_t)G * node_cap * 4);
-  L.nmask = o; o = al256(o + (size_t)node_cap * 4);
-  L.seen = o; o = al256(o + (size_t)G * (tok_cap / 32 + 1) * 4);
-  L.vis = o; o = al256(o + cc * 4);
-  L.proj = o; o = al256(o + cc * ICB_NPROJ * 8);
-  L.ekey = o; o = al256(o + cc * 16);
-  L.pbits = o; o = al256(o + (size_t)(page_cap / 32 + 1) * 4);
-  L.dirs = o; o = al256(o + (size_t)ICB_NPROJ * (dim + 1) * 8);
-  L.total = o;
-  return L;
-}
-
-__device__ inline SearchScratch slot_scratch(char* base, const SlotLayout& L, int tok_cap, double** dirs,
-                                             unsigned** pbits) {
-  SearchScratch S;
-  S.cand = (unsigned long long*)(base + L.cand);
-  S.pool = (unsigned long long*)(base + L.pool);
-  S.surv = (int*)(base + L.surv);
-  S.ulist = (int*)(base + L.ulist);
-  S.umask = (int*)(base + L.umask);
-  S.uoff = (int*)(base + L.uoff);
-  S.nmask = (unsigned*)(base + L.nmask);
-  S.seen = (unsigned*)(base + L.seen);
-  S.vis = (int*)(base + L.vis);
-  S.proj = (double*)(base + L.proj);
-  S.ekey = (unsigned long long*)(base + L.ekey);
-  S.ccap = tok_cap;
-  *pbits = (unsigned*)(base + L.pbits);
-  *dirs = (double*)(base + L.dirs);
-  return S;
-}
-
 // Lift raw query g (geometry.py:89-98): fp64 norm in pairwise order, fp32 q/|q|.
 template <int NT>
 __device__ bool lift_query(SearchSmem& S, const ForestView& F, const float* q, int g) {
@@ -86,9 +38,14 @@ __device__ bool lift_query(SearchSmem& S, const ForestView& F, const float* q, i
   return nrm != 0.0;
 }
 
-template <int NT>
-__global__ void __launch_bounds__(NT) query_kernel(ForestView F, QueryArgs A, char* scratch, SlotLayout SL) {
+template <int NT, int GP>
+__global__ void __launch_bounds__(NT, 1) query_kernel(ForestView F, QueryArgs A, char* scratch, SlotLayout SL) {
   __shared__ SearchSmem S;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  GroupSmem* GSA = reinterpret_cast<GroupSmem*>(dsm);
+  const RingView RG = ring_view(dsm, GP);
+  if (threadIdx.x == 0) S.sortbuf = reinterpret_cast<unsigned long long*>(RG.ring);
+  ring_init(RG);
   const int b = blockIdx.x;
   const int t = A.trees[b];
   const int G = A.G;
@@ -120,10 +77,29 @@ __global__ void __launch_bounds__(NT) query_kernel(ForestView F, QueryArgs A, ch
     if (threadIdx.x == 0 && A.out_npages) A.out_npages[b] = 0;
     return;
   }
-  tree_search<NT>(S, F, SS, t, A.P, dirs_tmp);
+  tree_search<NT, GP>(S, GSA, RG, F, SS, t, A.P, dirs_tmp);
   if (F.meta[t].err & ICB_ERR_CAP_SCRATCH) return;
   // final ranked top-k per head, token -> page bits
-  for (int g = 0; g < G; ++g) {
+  if (A.P.k <= kBuf) {
+    constexpr int NTG = NT / GP;
+    const int grp = threadIdx.x / NTG, gtid = threadIdx.x % NTG;
+    const int n = finalize_groups<NT, GP>(S, GSA, F, SS, G, A.P.k);
+    if (grp < G) {
+      const GroupSmem& GS = GSA[grp];
+      const int nw = min(n, A.k_out);
+      for (int i = gtid; i < nw; i += NTG) A.out_ids[((size_t)b * G + grp) * A.k_out + i] = key_id(GS.buf[i]);
+      if (gtid == 0) A.out_counts[(size_t)b * G + grp] = nw;
+      if (A.out_pages) {
+        for (int i = gtid; i < n; i += NTG) {
+          int id = key_id(GS.buf[i]);
+          int p = F.tok2page[F.tk(t, id)];
+          if (p < 0 || p >= F.page_cap) set_err(F.meta + t, ICB_ERR_UNMAPPED);
+          else atomicOr(pbits + (p >> 5), 1u << (p & 31));
+        }
+      }
+    }
+    __syncthreads();
+  } else for (int g = 0; g < G; ++g) {
     if (min((long long)S.npool[g], A.P.k) > kSortMax) {
       if (threadIdx.x == 0) set_err(F.meta + t, ICB_ERR_CAP_SCRATCH);
     }
@@ -214,7 +190,22 @@ int icb_query_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, co
   A.P.G = G; A.P.k = k; A.P.beam = beam; A.P.visit_cap = visit_cap; A.P.target = target_level;
   A.out_ids = out_ids; A.k_out = k_out; A.out_counts = out_counts; A.out_pages = out_pages;
   A.pages_cap = pages_cap; A.out_npages = out_npages;
-  query_kernel<kSearchThreads><<<n, kSearchThreads, 0, st>>>(f->view, A, scratch, SL);
+  const int GP = G <= 1 ? 1 : G <= 2 ? 2 : G <= 4 ? 4 : 8;
+  size_t dsm = search_dsm_bytes(GP);
+  if (const char* e = getenv("ICB_QUERY_DSM_EXTRA")) dsm += (size_t)atol(e);   // debug knob: occupancy
+  switch (GP) {
+#define ICB_LAUNCH_Q(gp)                                                                                  \
+  case gp:                                                                                                \
+    ICB_CUDA(cudaFuncSetAttribute(query_kernel<kSearchThreads, gp>,                                       \
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));                \
+    query_kernel<kSearchThreads, gp><<<n, kSearchThreads, dsm, st>>>(f->view, A, scratch, SL);            \
+    break;
+    ICB_LAUNCH_Q(1)
+    ICB_LAUNCH_Q(2)
+    ICB_LAUNCH_Q(4)
+    ICB_LAUNCH_Q(8)
+#undef ICB_LAUNCH_Q
+  }
   ICB_CUDA(cudaGetLastError());
   return ICB_OK;
 }

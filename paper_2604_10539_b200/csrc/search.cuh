@@ -31,8 +31,63 @@ struct SearchScratch {
   int* vis;                   // [tok_cap]  P-DCI visit list
   double* proj;               // [tok_cap][8] P-DCI projections
   unsigned long long* ekey;   // [tok_cap][2] P-DCI emission keys
+  int* upre;                  // [node_cap] union prefix of streamed rows
+  int* rlist;                 // [tok_cap][2] (token, union index) rows of a level
   int ccap;
 };
+
+// Per-CTA scratch slot carved from one buffer (same layout for queries and
+// inserts; G = heads per tree of the call).
+struct SlotLayout {
+  size_t cand, pool, surv, ulist, umask, uoff, nmask, seen, vis, proj, ekey, upre, rlist, pbits, dirs, total;
+};
+
+__host__ __device__ inline size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+__host__ __device__ inline SlotLayout slot_layout(int G, int tok_cap, int node_cap, int page_cap, int dim) {
+  SlotLayout L{};
+  size_t o = 0;
+  size_t cc = (size_t)tok_cap;
+  L.cand = o; o = al256(o + (size_t)G * cc * 8);
+  L.pool = o; o = al256(o + (size_t)G * cc * 8);
+  L.surv = o; o = al256(o + (size_t)G * cc * 4);
+  L.ulist = o; o = al256(o + (size_t)node_cap * 4);
+  L.umask = o; o = al256(o + (size_t)node_cap * 4);
+  L.uoff = o; o = al256(o + (size_t)G * node_cap * 4);
+  L.nmask = o; o = al256(o + (size_t)node_cap * 4);
+  L.seen = o; o = al256(o + (size_t)G * (tok_cap / 32 + 1) * 4);
+  L.vis = o; o = al256(o + cc * 4);
+  L.proj = o; o = al256(o + cc * ICB_NPROJ * 8);
+  L.ekey = o; o = al256(o + cc * 16);
+  L.upre = o; o = al256(o + (size_t)node_cap * 4);
+  L.rlist = o; o = al256(o + cc * 8);
+  L.pbits = o; o = al256(o + (size_t)(page_cap / 32 + 1) * 4);
+  L.dirs = o; o = al256(o + (size_t)ICB_NPROJ * (dim + 1) * 8);
+  L.total = o;
+  return L;
+}
+
+__device__ inline SearchScratch slot_scratch(char* base, const SlotLayout& L, int tok_cap, double** dirs,
+                                             unsigned** pbits) {
+  SearchScratch S;
+  S.cand = (unsigned long long*)(base + L.cand);
+  S.pool = (unsigned long long*)(base + L.pool);
+  S.surv = (int*)(base + L.surv);
+  S.ulist = (int*)(base + L.ulist);
+  S.umask = (int*)(base + L.umask);
+  S.uoff = (int*)(base + L.uoff);
+  S.nmask = (unsigned*)(base + L.nmask);
+  S.seen = (unsigned*)(base + L.seen);
+  S.vis = (int*)(base + L.vis);
+  S.proj = (double*)(base + L.proj);
+  S.ekey = (unsigned long long*)(base + L.ekey);
+  S.upre = (int*)(base + L.upre);
+  S.rlist = (int*)(base + L.rlist);
+  S.ccap = tok_cap;
+  *pbits = (unsigned*)(base + L.pbits);
+  *dirs = (double*)(base + L.dirs);
+  return S;
+}
 
 struct SearchSmem {
   float q[ICB_MAX_G][ICB_DPAD];
@@ -47,9 +102,9 @@ struct SearchSmem {
   int npool[ICB_MAX_G];
   int cnt;
   unsigned long long thr;
-  int scan_carry[ICB_MAX_G];
+  int scan_carry[ICB_MAX_G + 1];
   int misc[8];
-  unsigned long long sortbuf[kSortMax];
+  unsigned long long* sortbuf;   // fallback sort buffer (aliases the idle row ring, >= kSortMax keys)
 };
 
 // ------------------------------------------------------------------ select
@@ -181,6 +236,282 @@ __device__ void block_sort(SearchSmem& S, int n) {
   }
 }
 
+// ------------------------------------------------------------------ per-head groups
+// With G heads the CTA splits into G warp groups (NT / GP threads each) that
+// run the selections of their head concurrently, synchronizing on named
+// barrier 1 + group.
+constexpr int kBins = 1024;
+constexpr int kBuf = 512;
+constexpr int kSub = 8;                                  // ring slots per consumer warp
+constexpr int kRing = (kSearchThreads / 32 - 1) * kSub;  // 120 slots x 528 B = 63 KB
+
+struct GroupSmem {
+  int hist[kBins];
+  unsigned long long buf[kBuf];
+  int wsum[32];
+  int misc[8];
+  unsigned lo, hi;          // d2-bit range of the head's current candidate list
+  unsigned plo, phi;        // d2-bit range of the head's pool
+};
+
+// Dynamic shared memory: [GroupSmem x GP][ring kRing x 528 B][full][empty][q]
+struct RingView {
+  float* ring;
+  unsigned long long* full;
+  unsigned long long* empty;
+  unsigned* qp;     // per consumer warp: running row count (slot = c*kSub + q % kSub, phase = q / kSub)
+};
+
+__host__ __device__ inline size_t search_dsm_bytes(int GP) {
+  return sizeof(GroupSmem) * GP + (size_t)kRing * ICB_ROWF * 4 + 2 * kRing * 8 + 4 * 32;
+}
+
+__device__ inline RingView ring_view(unsigned char* dsm, int GP) {
+  RingView R;
+  unsigned char* p = dsm + sizeof(GroupSmem) * GP;
+  R.ring = reinterpret_cast<float*>(p);
+  p += (size_t)kRing * ICB_ROWF * 4;
+  R.full = reinterpret_cast<unsigned long long*>(p);
+  R.empty = R.full + kRing;
+  R.qp = reinterpret_cast<unsigned*>(R.empty + kRing);
+  return R;
+}
+
+__device__ inline void ring_init(const RingView& R) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRing; ++s) {
+      mbar_init(R.full + s, 1);
+      mbar_init(R.empty + s, 1);
+    }
+    for (int c = 0; c < 32; ++c) R.qp[c] = 0;
+    mbar_fence_init();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void gsync(int bar, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(n) : "memory");
+}
+
+// exclusive scan of one int per thread within the group
+template <int NTG>
+__device__ __forceinline__ int group_scan(GroupSmem& GS, int gtid, int bar, int v, int& total) {
+  const int lane = gtid & 31, w = gtid >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) GS.wsum[w] = x;
+  gsync(bar, NTG);
+  if (w == 0) {
+    int s = lane < NTG / 32 ? GS.wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < NTG / 32) GS.wsum[lane] = s;
+  }
+  gsync(bar, NTG);
+  int before = (w > 0 ? GS.wsum[w - 1] : 0) + x - v;
+  total = GS.wsum[NTG / 32 - 1];
+  gsync(bar, NTG);
+  return before;
+}
+
+// Output keys <= thr (and boundary handling done by the caller) with the
+// pool's seen-mark dedup; returns the count written.
+template <int NTG>
+__device__ int group_emit(GroupSmem& GS, int gtid, int bar, const unsigned long long* keys, int M,
+                          unsigned long long thr, unsigned long long* out_keys, int* out_ids, int out_base,
+                          unsigned* seen, unsigned* plo, unsigned* phi) {
+  const int lane = gtid & 31;
+  if (gtid == 0) GS.misc[0] = 0;
+  gsync(bar, NTG);
+  unsigned mn = 0xffffffffu, mx = 0u;
+  for (int i = gtid; i < M + (NTG - (M % NTG)) % NTG; i += NTG) {
+    bool take = false;
+    unsigned long long k = 0;
+    if (i < M) {
+      k = keys[i];
+      take = k <= thr;
+      if (take && seen) {
+        int id = key_id(k);
+        unsigned bit = 1u << (id & 31);
+        unsigned old = atomicOr(seen + (id >> 5), bit);
+        take = !(old & bit);
+      }
+    }
+    unsigned bal = __ballot_sync(0xffffffffu, take);
+    int base = 0;
+    if (lane == 0 && bal) base = atomicAdd(&GS.misc[0], __popc(bal));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (take) {
+      int pos = out_base + base + __popc(bal & ((1u << lane) - 1));
+      if (out_keys) out_keys[pos] = k;
+      if (out_ids) out_ids[pos] = key_id(k);
+      unsigned hb = (unsigned)(k >> 32);
+      mn = min(mn, hb);
+      mx = max(mx, hb);
+    }
+  }
+  if (plo) {
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) { atomicMin(plo, mn); atomicMax(phi, mx); }
+  }
+  gsync(bar, NTG);
+  int r = GS.misc[0];
+  gsync(bar, NTG);
+  return r;
+}
+
+// Exact threshold (the B-th smallest key) by 8-bit MSB radix passes over the
+// list; used for lists whose boundary bin is too crowded for the fast path.
+template <int NTG>
+__device__ unsigned long long group_radix_threshold(GroupSmem& GS, int gtid, int bar, const unsigned long long* keys,
+                                                    int M, long long B) {
+  const int lane = gtid & 31, w = gtid >> 5;
+  unsigned long long prefix = 0, pmask = 0;
+  long long remaining = B;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = gtid; i < 256; i += NTG) GS.hist[i] = 0;
+    gsync(bar, NTG);
+    for (int i = gtid; i < M + (NTG - (M % NTG)) % NTG; i += NTG) {
+      bool valid = i < M;
+      unsigned long long k = valid ? keys[i] : 0;
+      valid = valid && ((k & pmask) == prefix);
+      int dig = (int)((k >> shift) & 0xff);
+      unsigned act = __ballot_sync(0xffffffffu, valid);
+      if (valid) {
+        unsigned peers = __match_any_sync(act, dig);
+        if ((__ffs(peers) - 1) == lane) atomicAdd(&GS.hist[dig], __popc(peers));
+      }
+    }
+    gsync(bar, NTG);
+    if (w == 0) {
+      int c[8], local = 0;
+      for (int u = 0; u < 8; ++u) { c[u] = GS.hist[lane * 8 + u]; local += c[u]; }
+      int incl = local;
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int excl = incl - local;
+      bool mine = (excl < remaining) && (incl >= remaining);
+      unsigned who = __ballot_sync(0xffffffffu, mine);
+      int src = __ffs(who) - 1;
+      int digit = 0, before = 0, inb = 0;
+      if (lane == src) {
+        int run = excl;
+        for (int u = 0; u < 8; ++u) {
+          if (run + c[u] >= remaining) { digit = lane * 8 + u; before = run; inb = c[u]; break; }
+          run += c[u];
+        }
+      }
+      if (lane == src) { GS.misc[1] = digit; GS.misc[2] = before; GS.misc[3] = inb; }
+    }
+    gsync(bar, NTG);
+    int digit = GS.misc[1], before = GS.misc[2], inb = GS.misc[3];
+    gsync(bar, NTG);
+    remaining -= before;
+    prefix |= (unsigned long long)digit << shift;
+    pmask |= 0xffull << shift;
+    if (inb == remaining || shift == 0) return prefix | ~pmask;
+  }
+  return ~0ull;
+}
+
+// bitonic sort of n <= kBuf keys in GS.buf (ascending), group-wide
+template <int NTG>
+__device__ void group_sort(GroupSmem& GS, int gtid, int bar, int n) {
+  int P = 1;
+  while (P < n) P <<= 1;
+  for (int i = n + gtid; i < P; i += NTG) GS.buf[i] = ~0ull;
+  gsync(bar, NTG);
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = gtid; i < P; i += NTG) {
+        int ixj = i ^ j;
+        if (ixj > i) {
+          unsigned long long a = GS.buf[i], b = GS.buf[ixj];
+          bool upw = (i & k) == 0;
+          if ((a > b) == upw) { GS.buf[i] = b; GS.buf[ixj] = a; }
+        }
+      }
+      gsync(bar, NTG);
+    }
+  }
+}
+
+// Threshold of the B smallest of M unique keys (d2 bits of every key within
+// [lo, hi]): the B-th smallest key, so `key <= thr` selects exactly B.  One
+// adaptive histogram pass over kBins bins spanning [lo, hi] finds the
+// boundary bin, which is resolved exactly (bitonic sort in smem, or radix
+// passes if crowded).
+template <int NTG>
+__device__ unsigned long long group_threshold(GroupSmem& GS, int gtid, int bar, const unsigned long long* keys, int M,
+                                              long long B, unsigned lo, unsigned hi) {
+  if (B >= M) return ~0ull;
+  const unsigned range = hi - lo;
+  const int nbits = range ? 32 - __clz(range) : 0;
+  constexpr int kBinBits = 10;   // kBins = 1 << kBinBits
+  static_assert((1 << kBinBits) == kBins, "bin count");
+  const int shift = nbits > kBinBits ? nbits - kBinBits : 0;
+  for (int i = gtid; i < kBins; i += NTG) GS.hist[i] = 0;
+  gsync(bar, NTG);
+  for (int i = gtid; i < M; i += NTG) {
+    unsigned hb = (unsigned)(keys[i] >> 32);
+    ICB_CHECK(hb >= lo && hb <= hi && ((hb - lo) >> shift) < kBins, "hb %u lo %u hi %u shift %d M %d", hb, lo, hi,
+              shift, M);
+    atomicAdd(&GS.hist[(hb - lo) >> shift], 1);
+  }
+  gsync(bar, NTG);
+  // locate the boundary bin: each thread owns kBins / NTG consecutive bins
+  constexpr int PER = kBins / NTG;
+  int c[PER], local = 0;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) { c[u] = GS.hist[gtid * PER + u]; local += c[u]; }
+  int tot;
+  int excl = group_scan<NTG>(GS, gtid, bar, local, tot);
+  if (excl < B && excl + local >= B) {
+    int run = excl;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      if (run + c[u] >= B) { GS.misc[4] = gtid * PER + u; GS.misc[5] = run; GS.misc[6] = c[u]; break; }
+      run += c[u];
+    }
+  }
+  gsync(bar, NTG);
+  const int bstar = GS.misc[4], below = GS.misc[5], nb = GS.misc[6];
+  const long long need = B - below;
+  unsigned long long thr;
+  if (nb <= kBuf) {
+    // gather the boundary bin and sort it
+    if (gtid == 0) GS.misc[7] = 0;
+    gsync(bar, NTG);
+    for (int i = gtid; i < M; i += NTG) {
+      unsigned long long k = keys[i];
+      if ((int)(((unsigned)(k >> 32) - lo) >> shift) == bstar) {
+        const int at = atomicAdd(&GS.misc[7], 1);
+        ICB_CHECK(at < nb, "boundary gather %d >= %d", at, nb);
+        GS.buf[at] = k;
+      }
+    }
+    gsync(bar, NTG);
+    group_sort<NTG>(GS, gtid, bar, nb);
+    thr = GS.buf[need - 1];
+    gsync(bar, NTG);
+  } else {
+    thr = group_radix_threshold<NTG>(GS, gtid, bar, keys, M, B);
+  }
+  return thr;
+}
+
 // ------------------------------------------------------------------ P-DCI
 // Per-node unit directions, generated on the device from the tree's seed
 // (SeedSequence(entropy, spawn_key=(1, node_id)), normal, row-normalized with
@@ -297,7 +628,7 @@ struct SearchParams {
 // P-DCI path) writing keys to dst.
 template <int NT>
 __device__ void eval_list_one_head(SearchSmem& S, const ForestView& F, int t, const int* ids, int n, int g,
-                                   unsigned long long* dst) {
+                                   unsigned long long* dst, unsigned* lo = nullptr, unsigned* hi = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float4 qv = reinterpret_cast<const float4*>(S.q[g])[lane];
   for (int i = warp; i < n; i += NT / 32) {
@@ -305,17 +636,77 @@ __device__ void eval_list_one_head(SearchSmem& S, const ForestView& F, int t, co
     float4 p = reinterpret_cast<const float4*>(F.row(t, id))[lane];
     float s = warp_sum_butterfly(lane_sq4(p, qv));
     float d2 = d2_finish(s, F.tail[F.tk(t, id)], S.qt[g]);
-    if (lane == 0) dst[i] = make_key(d2, id);
+    if (lane == 0) {
+      dst[i] = make_key(d2, id);
+      if (lo) { atomicMin(lo, __float_as_uint(d2)); atomicMax(hi, __float_as_uint(d2)); }
+    }
   }
 }
 
 // The multi-level search.  On entry S.q/S.qt hold the lifted queries.  On
 // exit SS.pool[g][0..S.npool[g]) holds the unique candidate keys eligible for
 // the final top-k (sentinel: top-k of every level; else: top-k of the floor).
-template <int NT>
-__device__ void tree_search(SearchSmem& S, const ForestView& F, const SearchScratch& SS, int t,
+// Sum of each head's lane partials with the xor-butterfly pairing of
+// warp_sum_butterfly, transposed across heads: at offset 16 the lower half of
+// the warp keeps heads [0, G/2) and the upper half [G/2, G), at 8 the halves
+// split again, ...; lane l ends with the full sum of head l / (32 / G).
+// Every head's sum is the same pairing tree as the plain butterfly, so the
+// result is bit-identical (IEEE addition is commutative).
+template <int G>
+__device__ __forceinline__ float reduce_heads(float (&v)[G], int lane) {
+  if constexpr (G == 1) {
+    return warp_sum_butterfly(v[0]);
+  } else {
+    constexpr int H2 = G / 2;
+    float w[H2];
+    const bool up = lane & 16;
+#pragma unroll
+    for (int i = 0; i < H2; ++i) {
+      float send = up ? v[i] : v[i + H2];
+      float keep = up ? v[i + H2] : v[i];
+      w[i] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 16));
+    }
+    if constexpr (G == 2) {
+      float s = w[0];
+      s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 8));
+      s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
+      s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+      return __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
+    } else {
+      constexpr int H4 = G / 4;
+      float x[H4];
+      const bool up8 = lane & 8;
+#pragma unroll
+      for (int i = 0; i < H4; ++i) {
+        float send = up8 ? w[i] : w[i + H4];
+        float keep = up8 ? w[i + H4] : w[i];
+        x[i] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 8));
+      }
+      float s;
+      if constexpr (G == 4) {
+        s = x[0];
+        s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
+      } else {
+        const bool up4 = lane & 4;
+        float send = up4 ? x[0] : x[1];
+        float keep = up4 ? x[1] : x[0];
+        s = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 4));
+      }
+      s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+      return __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
+    }
+  }
+}
+
+// GP: padded head count (power of two >= P.G) fixing register arrays.
+template <int NT, int GP>
+__device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, const ForestView& F,
+                            const SearchScratch& SS, int t,
                             const SearchParams& P, double* dirs_tmp) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NTG = NT / GP;
+  const int grp = tid / NTG, gtid = tid % NTG, gbar = 1 + grp;
+  GroupSmem& GS = GSA[grp];
   const int G = P.G;
   const int L = F.meta[t].levels;
   const bool collect_all = P.target < 0;
@@ -325,8 +716,10 @@ __device__ void tree_search(SearchSmem& S, const ForestView& F, const SearchScra
   if (tid < G) { S.npool[tid] = 0; S.nsurv[tid] = 0; }
   if (tid == 0) atomicAdd(&F.meta[t].query_count, (unsigned long long)G);
   __syncthreads();
-  float4 qv[ICB_MAX_G];
-  for (int g = 0; g < G; ++g) qv[g] = reinterpret_cast<const float4*>(S.q[g])[lane];
+  float4 qv[GP];
+#pragma unroll
+  for (int g = 0; g < GP; ++g)
+    qv[g] = g < G ? reinterpret_cast<const float4*>(S.q[g])[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
 
   for (int lv = L; lv >= floor; --lv) {
     // (1) union of the nodes requested by the heads' survivors
@@ -341,6 +734,7 @@ __device__ void tree_search(SearchSmem& S, const ForestView& F, const SearchScra
         const int* sv = SS.surv + (size_t)g * SS.ccap;
         for (int i = tid; i < ns; i += NT) {
           int node = F.own(t, sv[i], lv);
+          ICB_CHECK(node >= 0 && node < F.node_cap, "own(%d, %d) = %d", sv[i], lv, node);
           unsigned old = atomicOr(SS.nmask + node, 1u << g);
           if (old == 0) SS.ulist[atomicAdd(&S.U, 1)] = node;
         }
@@ -350,8 +744,9 @@ __device__ void tree_search(SearchSmem& S, const ForestView& F, const SearchScra
       __syncthreads();
     }
     const int U = S.U;
-    // (2) per-head offsets over the union (normal nodes only)
-    if (tid < G) S.scan_carry[tid] = 0;
+    // (2) union prefix (rows to stream) and per-head output offsets over the
+    //     union (normal nodes only)
+    if (tid <= G) S.scan_carry[tid] = 0;
     if (tid == 0) S.nbig = 0;
     __syncthreads();
     for (int base = 0; base < U; base += NT) {
@@ -361,58 +756,134 @@ __device__ void tree_search(SearchSmem& S, const ForestView& F, const SearchScra
       bool big = sz > ICB_EXHAUSTIVE && (long long)sz > P.visit_cap;
       unsigned mk = i < U ? (unsigned)SS.umask[i] : 0u;
       if (i < U && big) atomicAdd(&S.nbig, 1);
-      for (int g = 0; g < G; ++g) {
-        int v = (i < U && !big && ((mk >> g) & 1)) ? sz : 0;
+      for (int g = 0; g <= G; ++g) {
+        int v = (i < U && !big && (g == G || ((mk >> g) & 1))) ? sz : 0;
         int tot;
         int ex = block_exclusive_scan<NT>(v, S.wsum, tot);
-        if (i < U) SS.uoff[(size_t)g * F.node_cap + i] = S.scan_carry[g] + ex;
+        if (i < U) {
+          if (g < G) SS.uoff[(size_t)g * F.node_cap + i] = S.scan_carry[g] + ex;
+          else SS.upre[i] = S.scan_carry[G] + ex;
+        }
         __syncthreads();
         if (tid == 0) S.scan_carry[g] += tot;
         __syncthreads();
       }
     }
     if (tid < G) S.M[tid] = S.scan_carry[tid];
+    if (tid == 0) S.misc[6] = S.scan_carry[G];
     __syncthreads();
     for (int g = 0; g < G; ++g)
       if (S.M[g] > SS.ccap) { if (tid == 0) set_err(F.meta + t, ICB_ERR_CAP_SCRATCH); return; }
-    // (3) evaluate normal nodes: one warp per node, 4 rows in flight
-    if (tid == 0) S.misc[5] = 0;
-    __syncthreads();
+    // (3a) flatten the union's member rows into one list (coalesced copies of
+    //      the contiguous member arrays): entry = (token, union index)
+    const int R = S.misc[6];
+    if (tid < GP) { GSA[tid].lo = 0xffffffffu; GSA[tid].hi = 0u; }
     for (int i = warp; i < U; i += NT / 32) {
       const int node = SS.ulist[i];
-      const unsigned mk = (unsigned)SS.umask[i];
       const size_t x = F.nd(t, node);
       const int sz = F.node_size[x];
       if (sz > ICB_EXHAUSTIVE && (long long)sz > P.visit_cap) continue;
-      if (lane == 0) atomicAdd(&S.misc[5], sz);
-      const int off = F.node_off[x];
-      int ob[ICB_MAX_G];
-      for (int g = 0; g < G; ++g) ob[g] = SS.uoff[(size_t)g * F.node_cap + i];
-      for (int j0 = 0; j0 < sz; j0 += 4) {
-        int myid = (lane < 4 && j0 + lane < sz) ? mem[off + j0 + lane] : 0;
-        float mytail = (lane < 4 && j0 + lane < sz) ? F.tail[F.tk(t, myid)] : 0.f;
-        int ids[4];
-        float tl[4];
-        float4 rows[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          ids[u] = __shfl_sync(0xffffffffu, myid, u);
-          tl[u] = __shfl_sync(0xffffffffu, mytail, u);
-          if (j0 + u < sz) rows[u] = __ldg(reinterpret_cast<const float4*>(F.row(t, ids[u])) + lane);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (j0 + u >= sz) break;
-          for (int g = 0; g < G; ++g) {
-            if (!((mk >> g) & 1)) continue;
-            float s = warp_sum_butterfly(lane_sq4(rows[u], qv[g]));
-            float d2 = d2_finish(s, tl[u], S.qt[g]);
-            if (lane == 0) SS.cand[(size_t)g * SS.ccap + ob[g] + j0 + u] = make_key(d2, ids[u]);
-          }
-        }
+      const int off = F.node_off[x], base = SS.upre[i];
+      for (int j = lane; j < sz; j += 32) {
+        SS.rlist[2 * (size_t)(base + j)] = mem[off + j];
+        SS.rlist[2 * (size_t)(base + j) + 1] = i;
       }
     }
     __syncthreads();
+    // (3b) stream the rows through a shared-memory ring: warp 0 is the TMA
+    //      producer (one 528-byte cp.async.bulk per row, completion on the
+    //      slot's mbarrier), warps 1.. consume batches of 8 rows from smem,
+    //      score every row against all heads with the head-transposed
+    //      butterfly (same pairing tree as warp_sum_butterfly) and release
+    //      the slot.  In-flight bytes = ring size, independent of registers.
+    //      Each consumer warp owns kSub slots and consumes them strictly in
+    //      order (its own running row count qp[c]), so no mbarrier can be
+    //      tested two phases ahead.
+    constexpr int NCW = NT / 32 - 1;
+    if (warp == 0) {
+      for (int i0 = 0; i0 < R; i0 += 32) {
+        const int i = i0 + lane;
+        if (i < R) {
+          const int c = (i >> 3) % NCW, k = (i >> 3) / NCW;
+          const unsigned rc = RG.qp[c] + (unsigned)(k * 8 + (i & 7));
+          const int slot = c * kSub + (int)(rc % kSub);
+          const unsigned use = rc / kSub;
+          if (use > 0) mbar_wait(RG.empty + slot, (use - 1) & 1u);
+          const int tok = SS.rlist[2 * (size_t)i];
+          mbar_expect_tx(RG.full + slot, ICB_ROWF * 4);
+          bulk_g2s(RG.ring + (size_t)slot * ICB_ROWF, F.row(t, tok), ICB_ROWF * 4, RG.full + slot);
+        }
+      }
+    } else {
+      constexpr int LPG = 32 / GP;              // lanes holding one head's sum
+      constexpr int SLOTS = (8 + LPG - 1) / LPG;
+      const int myh = lane / LPG;
+      const float qt_my = S.qt[myh];
+      const int cw = warp - 1;
+      const unsigned qc = RG.qp[cw];
+      unsigned mn = 0xffffffffu, mx = 0u;
+      for (int base = cw * 8, kb = 0; base < R; base += NCW * 8, ++kb) {
+        const int nrow = min(8, R - base);
+        int e_tok = 0, e_idx = 0;
+        if (lane < nrow) {
+          e_tok = SS.rlist[2 * (size_t)(base + lane)];
+          e_idx = SS.rlist[2 * (size_t)(base + lane) + 1];
+        }
+        float keep[SLOTS];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (u >= nrow) break;
+          const unsigned rc = qc + (unsigned)(kb * 8 + u);
+          const int slot = cw * kSub + (int)(rc % kSub);
+          mbar_wait(RG.full + slot, (rc / kSub) & 1u);
+          const float* srow = RG.ring + (size_t)slot * ICB_ROWF;
+          const float4 p = reinterpret_cast<const float4*>(srow)[lane];
+          const float tl = srow[ICB_DPAD];
+          float v[GP];
+#pragma unroll
+          for (int g = 0; g < GP; ++g) v[g] = lane_sq4(p, qv[g]);
+          float f = reduce_heads<GP>(v, lane);
+          float d2 = d2_finish(f, tl, qt_my);
+          // every lane's smem reads have retired (the butterfly consumed them)
+          __syncwarp();
+          if (lane == 0) mbar_arrive(RG.empty + slot);
+          if ((u % LPG) == (lane % LPG)) keep[u / LPG] = d2;
+        }
+#pragma unroll
+        for (int sl = 0; sl < SLOTS; ++sl) {
+          const int u = sl * LPG + (lane % LPG);
+          const int src = u < 8 ? u : 0;
+          const int tok = __shfl_sync(0xffffffffu, e_tok, src);
+          const int idx = __shfl_sync(0xffffffffu, e_idx, src);
+          if (u < nrow && myh < G && ((SS.umask[idx] >> myh) & 1)) {
+            const int pos = SS.uoff[(size_t)myh * F.node_cap + idx] + (base + u - SS.upre[idx]);
+            ICB_CHECK(pos >= 0 && pos < S.M[myh], "cand pos %d M %d", pos, S.M[myh]);
+            SS.cand[(size_t)myh * SS.ccap + pos] = make_key(keep[sl], tok);
+            const unsigned hb = __float_as_uint(keep[sl]);
+            mn = min(mn, hb);
+            mx = max(mx, hb);
+          }
+        }
+      }
+      // per-head d2 range of this level's candidates (feeds the selection bins)
+#pragma unroll
+      for (int o = 1; o < LPG; o <<= 1) {
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      }
+      if ((lane % LPG) == 0 && myh < G && mx >= mn) {
+        atomicMin(&GSA[myh].lo, mn);
+        atomicMax(&GSA[myh].hi, mx);
+      }
+    }
+    if (tid == 0) S.misc[5] = R;
+    __syncthreads();
+    if (tid < NCW) {   // advance every consumer's running row count by its rows of this level
+      const int nb = (R + 7) / 8;
+      int rows = 0;
+      for (int j = tid; j < nb; j += NCW) rows += min(8, R - 8 * j);
+      RG.qp[tid] += (unsigned)rows;
+    }
     // (4) P-DCI truncated nodes (rare): block-wide, per node and head
     if (S.nbig > 0) {
       for (int i = 0; i < U; ++i) {
@@ -424,7 +895,8 @@ __device__ void tree_search(SearchSmem& S, const ForestView& F, const SearchScra
           if (!((mk >> g) & 1)) continue;
           int cnt = pdci_visit<NT>(S, F, SS, t, node, g, P.visit_cap, dirs_tmp);
           if (S.M[g] + cnt > SS.ccap) { if (tid == 0) set_err(F.meta + t, ICB_ERR_CAP_SCRATCH); return; }
-          eval_list_one_head<NT>(S, F, t, SS.vis, cnt, g, SS.cand + (size_t)g * SS.ccap + S.M[g]);
+          eval_list_one_head<NT>(S, F, t, SS.vis, cnt, g, SS.cand + (size_t)g * SS.ccap + S.M[g], &GSA[g].lo,
+                                 &GSA[g].hi);
           __syncthreads();
           if (tid == 0) { S.M[g] += cnt; S.misc[5] += cnt; }
           __syncthreads();
@@ -442,31 +914,64 @@ __device__ void tree_search(SearchSmem& S, const ForestView& F, const SearchScra
     if (lv < L)
       for (int i = tid; i < U; i += NT) SS.nmask[SS.ulist[i]] = 0u;
     __syncthreads();
-    // (7) per-head selection
-    for (int g = 0; g < G; ++g) {
+    // (7) per-head selection, heads in parallel (one warp group per head).
+    //     Survivors = top-beam (dci.py:359-361).  The pool collects, without
+    //     duplicates, every survivor (a superset of the level's top-k since
+    //     beam >= k) and the floor level's top-k (dci.py:355-358).
+    if (grp < G) {
+      const int g = grp;
       unsigned long long* cg = SS.cand + (size_t)g * SS.ccap;
       unsigned long long* pg = SS.pool + (size_t)g * SS.ccap;
       unsigned* sg = SS.seen + (size_t)g * (F.tok_cap / 32 + 1);
       const int M = S.M[g];
+      if (lv == L && gtid == 0) { GS.plo = 0xffffffffu; GS.phi = 0u; }
+      gsync(gbar, NTG);
       if (lv > floor) {
-        int ns = block_select<NT>(S, cg, M, P.beam, nullptr, SS.surv + (size_t)g * SS.ccap, 0, nullptr);
-        if (tid == 0) S.nsurv[g] = ns;
-        __syncthreads();
+        unsigned long long thr = group_threshold<NTG>(GS, gtid, gbar, cg, M, P.beam, GS.lo, GS.hi);
+        int ns = group_emit<NTG>(GS, gtid, gbar, cg, M, thr, nullptr, SS.surv + (size_t)g * SS.ccap, 0,
+                                 nullptr, nullptr, nullptr);
         if (collect_all) {
-          // top-k of this level = top-k of its survivors (beam >= k)
-          // survivors' keys: re-select from candidates with B = k
-          int np = block_select<NT>(S, cg, M, P.k, pg, nullptr, S.npool[g], sg);
-          if (tid == 0) S.npool[g] += np;
-          __syncthreads();
+          int np = group_emit<NTG>(GS, gtid, gbar, cg, M, thr, pg, nullptr, S.npool[g], sg, &GS.plo, &GS.phi);
+          if (gtid == 0) S.npool[g] += np;
         }
+        if (gtid == 0) S.nsurv[g] = ns;
       } else {
-        int np = block_select<NT>(S, cg, M, P.k, pg, nullptr, S.npool[g], sg);
-        if (tid == 0) S.npool[g] += np;
-        __syncthreads();
+        unsigned long long thr = group_threshold<NTG>(GS, gtid, gbar, cg, M, P.k, GS.lo, GS.hi);
+        int np = group_emit<NTG>(GS, gtid, gbar, cg, M, thr, pg, nullptr, S.npool[g], sg, &GS.plo, &GS.phi);
+        if (gtid == 0) S.npool[g] += np;
       }
     }
-    (void)warp;
+    __syncthreads();
   }
+}
+
+// Final ranked top-k (k <= kBuf) of every head, in parallel: the pool's
+// top-k lands sorted in GSA[g].buf[0..n); seen marks are cleared.  Returns n
+// for the calling thread's head (all threads must call).
+template <int NT, int GP>
+__device__ int finalize_groups(SearchSmem& S, GroupSmem* GSA, const ForestView& F, const SearchScratch& SS, int G,
+                               long long k) {
+  constexpr int NTG = NT / GP;
+  const int tid = threadIdx.x, grp = tid / NTG, gtid = tid % NTG, gbar = 1 + grp;
+  int n = 0;
+  if (grp < G) {
+    GroupSmem& GS = GSA[grp];
+    unsigned long long* pg = SS.pool + (size_t)grp * SS.ccap;
+    unsigned* sg = SS.seen + (size_t)grp * (F.tok_cap / 32 + 1);
+    const int np = S.npool[grp];
+    for (int i = gtid; i < np; i += NTG) {
+      int id = key_id(pg[i]);
+      atomicAnd(sg + (id >> 5), ~(1u << (id & 31)));
+    }
+    gsync(gbar, NTG);
+    const long long want = min((long long)np, k);
+    unsigned long long thr = group_threshold<NTG>(GS, gtid, gbar, pg, np, want, GS.plo, GS.phi);
+    // emit into a scratch region (the threshold pass may have used buf)
+    n = group_emit<NTG>(GS, gtid, gbar, pg, np, thr, GS.buf, nullptr, 0, nullptr, nullptr, nullptr);
+    group_sort<NTG>(GS, gtid, gbar, n);
+  }
+  __syncthreads();
+  return n;
 }
 
 // Final ranked top-k of head g from its pool into S.sortbuf[0..n) (sorted).

@@ -19,6 +19,7 @@ from . import _native as N
 from .errors import ConfigError, InputError
 
 DPAD = 128
+ROWF = 132   # device row stride in floats: 128 dims, the lifted tail, 3 zeros
 
 
 def entropy_words(seed) -> list[int]:
@@ -245,7 +246,7 @@ class DeviceForest:
             page_role=np.zeros(cp.page_cap, np.int8), page_tok=np.zeros(cp.page_cap * s, np.int32),
             tok2page=np.zeros(cp.tok_cap, np.int32), level=np.zeros(cp.tok_cap, np.int8),
             own_base=np.zeros(cp.tok_cap, np.int32), own_list=np.zeros(cp.own_cap, np.int32))
-        lift = np.zeros(cp.tok_cap * DPAD, np.float32) if with_rows else None
+        lift = np.zeros(cp.tok_cap * ROWF, np.float32) if with_rows else None
         tail = np.zeros(cp.tok_cap, np.float32) if with_rows else None
         win = np.zeros(8, np.int32)
         sink = np.zeros(8, np.int32)
@@ -282,7 +283,9 @@ class DeviceForest:
                    tok2page=t2p, win=[int(x) for x in win if x >= 0], sink=[int(x) for x in sink if x >= 0],
                    own_base=arrs["own_base"], own_list=arrs["own_list"])
         if with_rows:
-            out["lift"] = lift.reshape(cp.tok_cap, DPAD)
+            rows = lift.reshape(cp.tok_cap, ROWF)
+            out["lift"] = rows[:, :DPAD]
+            out["row_tail"] = rows[:, DPAD]
             out["tail"] = tail
         return out
 
