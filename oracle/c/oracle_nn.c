@@ -69,3 +69,30 @@ void oracle_project(const double *dirs, int m, const double *vecs, int64_t n, in
             out[i * m + j] = a;
         }
 }
+
+/* Search distance in fp32 with the device's exact operation order
+ * (csrc/icb.cuh: lane_sq4 / warp_sum_butterfly / d2_finish): lane l owns
+ * dims 4l..4l+3, s_l = fma(d3,d3, fma(d2,d2, fma(d1,d1, d0*d0))), lanes are
+ * combined by the xor butterfly 16, 8, 4, 2, 1 with plain adds, and
+ * d2 = fma(dt, dt, f) with dt = tail - q_tail.  Restates dci.py:311-312
+ * (sum of squared lifted differences).  rows [n][128] fp32 (zero padded). */
+void oracle_d2_fp32(const float *rows, const float *tail, int64_t n, const float *q, float q_tail,
+                    float *out) {
+    for (int64_t r = 0; r < n; ++r) {
+        const float *p = rows + r * 128;
+        float s[32];
+        for (int l = 0; l < 32; ++l) {
+            float d0 = p[4 * l] - q[4 * l], d1 = p[4 * l + 1] - q[4 * l + 1];
+            float d2 = p[4 * l + 2] - q[4 * l + 2], d3 = p[4 * l + 3] - q[4 * l + 3];
+            float a = d0 * d0;
+            a = fmaf(d1, d1, a);
+            a = fmaf(d2, d2, a);
+            a = fmaf(d3, d3, a);
+            s[l] = a;
+        }
+        for (int w = 16; w >= 1; w >>= 1)
+            for (int l = 0; l < w; ++l) s[l] = s[l] + s[l + w];
+        float dt = tail[r] - q_tail;
+        out[r] = fmaf(dt, dt, s[0]);
+    }
+}

@@ -21,25 +21,7 @@ EXHAUSTIVE_NODE_LIMIT = 64    # dci.py:41
 NUM_PROJECTIONS = 8           # dci.py:44
 PARENT_BUDGET = (1, 8, 64)    # dci.py:78  (k, beam, visit_cap)
 
-_HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB = None
-
-
-def _lib():
-    """Load (building on first use) the oracle's C helper library."""
-    global _LIB
-    if _LIB is None:
-        path = os.path.join(_HERE, "_build", "liboracle.so")
-        src = os.path.join(_HERE, "c", "oracle_nn.c")
-        if not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(src):
-            subprocess.check_call(["make", "-s", "-C", _HERE])
-        lib = ctypes.CDLL(path)
-        dp = ctypes.POINTER(ctypes.c_double)
-        lib.oracle_nn_parents.argtypes = [dp, ctypes.c_int64, dp, ctypes.c_int64, ctypes.c_int,
-                                          ctypes.POINTER(ctypes.c_int32)]
-        lib.oracle_project.argtypes = [dp, ctypes.c_int, dp, ctypes.c_int64, ctypes.c_int, dp]
-        _LIB = lib
-    return _LIB
+from .clib import lib as _lib  # noqa: E402
 
 
 def _dptr(a):

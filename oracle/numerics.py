@@ -103,26 +103,18 @@ def lift_query32(q: np.ndarray) -> np.ndarray:
 def d2_fp32(rows: np.ndarray, tail: np.ndarray, q: np.ndarray, q_tail=0.0) -> np.ndarray:
     """Squared lifted distance `sum (p - q)^2` (dci.py:311-312) in fp32.
 
-    Fixed order (mirrors `warp_d2` in the CUDA search kernel): lane l of a
-    warp owns dims 4l..4l+3 and forms ((s0 + s1) + s2) + s3 of the squared
-    differences; lanes are combined by an xor-butterfly 16, 8, 4, 2, 1
-    (commutative, so every lane holds the same value); the tail term
-    (p_d - q_d)^2 is added last (q_d = 0 for decode queries, the lifted
-    key's tail for insert-time parent searches).  No fused multiply-adds.
+    Fixed order (mirrors lane_sq4 / warp_sum_butterfly / d2_finish in
+    csrc/icb.cuh): lane l of a warp owns dims 4l..4l+3 and forms
+    fma(d3,d3, fma(d2,d2, fma(d1,d1, d0*d0))) of the differences; lanes are
+    combined by an xor butterfly 16, 8, 4, 2, 1 (commutative adds, so every
+    lane holds the same value); the tail term enters last as
+    fma(dt, dt, f), dt = p_d - q_d (q_d = 0 for decode queries, the lifted
+    key's tail for insert-time parent searches).  Fused multiply-adds cannot
+    be expressed exactly in NumPy, so this calls the C restatement
+    (oracle/c/oracle_nn.c:oracle_d2_fp32, compiled with explicit fmaf).
     """
-    rows = np.asarray(rows, dtype=np.float32).reshape(-1, DPAD)
-    q = np.asarray(q, dtype=np.float32).reshape(DPAD)
-    tail = np.asarray(tail, dtype=np.float32).reshape(-1)
-    diff = rows - q[None, :]
-    sq = (diff * diff).reshape(-1, 32, 4)
-    s = ((sq[:, :, 0] + sq[:, :, 1]) + sq[:, :, 2]) + sq[:, :, 3]
-    s = s[:, :16] + s[:, 16:]
-    s = s[:, :8] + s[:, 8:]
-    s = s[:, :4] + s[:, 4:]
-    s = s[:, :2] + s[:, 2:]
-    f = s[:, 0] + s[:, 1]
-    dt = tail - np.float32(q_tail)
-    return (f + dt * dt).astype(np.float32)
+    from .clib import d2_fp32 as _c_d2
+    return _c_d2(rows, tail, q, q_tail)
 
 
 def pack_keys(d2: np.ndarray, ids: np.ndarray) -> np.ndarray:

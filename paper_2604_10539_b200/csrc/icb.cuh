@@ -128,13 +128,34 @@ struct ForestView {
 // numerics
 
 // Squared lifted distance in fp32 with the fixed order the oracle restates
-// (oracle/numerics.py:d2_fp32): per-lane ((s0+s1)+s2)+s3 over dims 4l..4l+3,
-// xor butterfly 16,8,4,2,1, then + (tail - q_tail)^2.  No FMA contraction.
+// (oracle/c/oracle_nn.c:oracle_d2_fp32): lane l of a warp owns dims
+// 4l..4l+3, d_i = p_i - q_i, s = fma(d3, d3, fma(d2, d2, fma(d1, d1, d0*d0))),
+// xor butterfly 16,8,4,2,1 (plain adds), then d2 = fma(dt, dt, s) with
+// dt = tail - q_tail.  Every operation is an explicit IEEE op (no contraction).
 __device__ __forceinline__ float lane_sq4(float4 p, float4 q) {
   float a = __fsub_rn(p.x, q.x), b = __fsub_rn(p.y, q.y);
   float c = __fsub_rn(p.z, q.z), d = __fsub_rn(p.w, q.w);
-  return __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(a, a), __fmul_rn(b, b)), __fmul_rn(c, c)),
-                   __fmul_rn(d, d));
+  return __fmaf_rn(d, d, __fmaf_rn(c, c, __fmaf_rn(b, b, __fmul_rn(a, a))));
+}
+
+// The same lane partial for two heads at once with Blackwell's packed fp32
+// (FADD2 / FMUL2 / FFMA2): element-wise IEEE results identical to lane_sq4.
+__device__ __forceinline__ unsigned long long pack_f2(float lo, float hi) {
+  return ((unsigned long long)__float_as_uint(hi) << 32) | __float_as_uint(lo);
+}
+__device__ __forceinline__ float2 lane_sq4_x2(float4 p, const unsigned long long (&q2)[4]) {
+  unsigned long long d[4], s;
+  const float pv[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const unsigned long long pp = pack_f2(pv[i], pv[i]);
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d[i]) : "l"(pp), "l"(q2[i]));
+  }
+  asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(s) : "l"(d[0]));
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(s) : "l"(d[1]), "l"(s));
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(s) : "l"(d[2]), "l"(s));
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(s) : "l"(d[3]), "l"(s));
+  return make_float2(__uint_as_float((unsigned)s), __uint_as_float((unsigned)(s >> 32)));
 }
 __device__ __forceinline__ float warp_sum_butterfly(float s) {
   s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 16));
@@ -146,7 +167,7 @@ __device__ __forceinline__ float warp_sum_butterfly(float s) {
 }
 __device__ __forceinline__ float d2_finish(float s, float pt, float qt) {
   float dt = __fsub_rn(pt, qt);
-  return __fadd_rn(s, __fmul_rn(dt, dt));
+  return __fmaf_rn(dt, dt, s);
 }
 
 __device__ __forceinline__ unsigned long long make_key(float d2, int id) {
@@ -209,6 +230,47 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* sm /* >= NT/32+1
   return before;
 }
 
+// V independent exclusive scans (one int each per thread) with one pair of
+// block barriers; sm holds V * (NT / 32) ints.
+template <int NT, int V>
+__device__ __forceinline__ void block_scan_multi(const int (&v)[V], int (&ex)[V], int (&tot)[V], int* sm) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    x[k] = v[k];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, x[k], o);
+      if (lane >= o) x[k] += y;
+    }
+  }
+  if (lane == 31)
+#pragma unroll
+    for (int k = 0; k < V; ++k) sm[k * NW + warp] = x[k];
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      int w = lane < NW ? sm[k * NW + lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      if (lane < NW) sm[k * NW + lane] = w;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    ex[k] = (warp > 0 ? sm[k * NW + warp - 1] : 0) + x[k] - v[k];
+    tot[k] = sm[k * NW + NW - 1];
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ void set_err(TreeMeta* m, int bit) { atomicOr(&m->err, bit); }
 
 // ---------------------------------------------------------------------------
@@ -240,6 +302,16 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
       "r"(parity)
       : "memory");
 }
+// Ampere-style async copies (LDGSTS): 16 bytes per thread, L2-only (.cg).
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` (bytes).
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(

@@ -199,7 +199,7 @@ __device__ int insert_one(SearchSmem& S, GroupSmem* GSA, const RingView& RG, con
       if (tid == 0) { s_container = m->top_node; s_chain_from = level - 1; }
     } else {
       SearchParams P;
-      P.G = 1; P.k = 1; P.beam = 8; P.visit_cap = 64; P.target = level + 1;
+      P.G = 1; P.k = 1; P.beam = 8; P.visit_cap = 64; P.target = level + 1; P.prof = nullptr;
       tree_search<NT, 1>(S, GSA, RG, F, SS, t, P, dirs_tmp);
       int n = finalize_groups<NT, 1>(S, GSA, F, SS, 1, 1);
       if (tid == 0) {
@@ -250,7 +250,7 @@ __device__ int insert_one(SearchSmem& S, GroupSmem* GSA, const RingView& RG, con
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT, 1) insert_kernel(ForestView F, InsertArgs A, char* scratch, SlotLayout SL) {
+__global__ void __launch_bounds__(NT, 512 / NT) insert_kernel(ForestView F, InsertArgs A, char* scratch, SlotLayout SL) {
   __shared__ SearchSmem S;
   extern __shared__ __align__(128) unsigned char dsm[];
   GroupSmem* GSA = reinterpret_cast<GroupSmem*>(dsm);

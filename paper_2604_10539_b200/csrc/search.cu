@@ -6,6 +6,8 @@
 
 namespace icb {
 
+__device__ unsigned long long g_search_prof[kPhases];
+
 struct QueryArgs {
   const int32_t* trees;
   int n, G, lifted_input;
@@ -39,7 +41,7 @@ __device__ bool lift_query(SearchSmem& S, const ForestView& F, const float* q, i
 }
 
 template <int NT, int GP>
-__global__ void __launch_bounds__(NT, 1) query_kernel(ForestView F, QueryArgs A, char* scratch, SlotLayout SL) {
+__global__ void __launch_bounds__(NT, 512 / NT) query_kernel(ForestView F, QueryArgs A, char* scratch, SlotLayout SL) {
   __shared__ SearchSmem S;
   extern __shared__ __align__(128) unsigned char dsm[];
   GroupSmem* GSA = reinterpret_cast<GroupSmem*>(dsm);
@@ -83,7 +85,9 @@ __global__ void __launch_bounds__(NT, 1) query_kernel(ForestView F, QueryArgs A,
   if (A.P.k <= kBuf) {
     constexpr int NTG = NT / GP;
     const int grp = threadIdx.x / NTG, gtid = threadIdx.x % NTG;
+    long long t0 = clock64();
     const int n = finalize_groups<NT, GP>(S, GSA, F, SS, G, A.P.k);
+    if (A.P.prof && threadIdx.x == 0) atomicAdd(A.P.prof + 7, (unsigned long long)(clock64() - t0));
     if (grp < G) {
       const GroupSmem& GS = GSA[grp];
       const int nw = min(n, A.k_out);
@@ -148,6 +152,18 @@ __global__ void __launch_bounds__(NT, 1) query_kernel(ForestView F, QueryArgs A,
 
 using namespace icb;
 
+// Phase cycle counters of the search (enabled by ICB_PROF=1): union, scans,
+// row list, row stream, P-DCI + counters, selection, level tail, finalize.
+extern "C" int icb_search_profile(unsigned long long* out, int reset) {
+  ICB_CUDA(cudaDeviceSynchronize());
+  ICB_CUDA(cudaMemcpyFromSymbol(out, g_search_prof, sizeof(unsigned long long) * kPhases));
+  if (reset) {
+    unsigned long long z[kPhases] = {};
+    ICB_CUDA(cudaMemcpyToSymbol(g_search_prof, z, sizeof(z)));
+  }
+  return ICB_OK;
+}
+
 // Per-call scratch: one slot per tree in the call (grown and zeroed on demand).
 int ensure_query_scratch(icb_forest* f, int n, int G, cudaStream_t st, char** out, SlotLayout* sl) {
   const auto& c = f->cfg;
@@ -188,6 +204,8 @@ int icb_query_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, co
   QueryArgs A{};
   A.trees = trees; A.n = n; A.G = G; A.lifted_input = lifted_input; A.queries = queries;
   A.P.G = G; A.P.k = k; A.P.beam = beam; A.P.visit_cap = visit_cap; A.P.target = target_level;
+  A.P.prof = nullptr;
+  if (getenv("ICB_PROF")) ICB_CUDA(cudaGetSymbolAddress((void**)&A.P.prof, g_search_prof));
   A.out_ids = out_ids; A.k_out = k_out; A.out_counts = out_counts; A.out_pages = out_pages;
   A.pages_cap = pages_cap; A.out_npages = out_npages;
   const int GP = G <= 1 ? 1 : G <= 2 ? 2 : G <= 4 ? 4 : 8;

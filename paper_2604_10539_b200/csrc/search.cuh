@@ -16,7 +16,10 @@
 
 namespace icb {
 
-constexpr int kSearchThreads = 512;
+#ifndef ICB_SEARCH_THREADS
+#define ICB_SEARCH_THREADS 256
+#endif
+constexpr int kSearchThreads = ICB_SEARCH_THREADS;   // 256: two CTAs (trees) per SM
 constexpr int kSortMax = 4096;   // largest k served by the in-smem final sort
 
 struct SearchScratch {
@@ -32,6 +35,7 @@ struct SearchScratch {
   double* proj;               // [tok_cap][8] P-DCI projections
   unsigned long long* ekey;   // [tok_cap][2] P-DCI emission keys
   int* upre;                  // [node_cap] union prefix of streamed rows
+  int* umoff;                 // [node_cap] member offset of each union node (-1: P-DCI node)
   int* rlist;                 // [tok_cap][2] (token, union index) rows of a level
   int ccap;
 };
@@ -39,7 +43,7 @@ struct SearchScratch {
 // Per-CTA scratch slot carved from one buffer (same layout for queries and
 // inserts; G = heads per tree of the call).
 struct SlotLayout {
-  size_t cand, pool, surv, ulist, umask, uoff, nmask, seen, vis, proj, ekey, upre, rlist, pbits, dirs, total;
+  size_t cand, pool, surv, ulist, umask, uoff, nmask, seen, vis, proj, ekey, upre, umoff, rlist, pbits, dirs, total;
 };
 
 __host__ __device__ inline size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -60,6 +64,7 @@ __host__ __device__ inline SlotLayout slot_layout(int G, int tok_cap, int node_c
   L.proj = o; o = al256(o + cc * ICB_NPROJ * 8);
   L.ekey = o; o = al256(o + cc * 16);
   L.upre = o; o = al256(o + (size_t)node_cap * 4);
+  L.umoff = o; o = al256(o + (size_t)node_cap * 4);
   L.rlist = o; o = al256(o + cc * 8);
   L.pbits = o; o = al256(o + (size_t)(page_cap / 32 + 1) * 4);
   L.dirs = o; o = al256(o + (size_t)ICB_NPROJ * (dim + 1) * 8);
@@ -82,6 +87,7 @@ __device__ inline SearchScratch slot_scratch(char* base, const SlotLayout& L, in
   S.proj = (double*)(base + L.proj);
   S.ekey = (unsigned long long*)(base + L.ekey);
   S.upre = (int*)(base + L.upre);
+  S.umoff = (int*)(base + L.umoff);
   S.rlist = (int*)(base + L.rlist);
   S.ccap = tok_cap;
   *pbits = (unsigned*)(base + L.pbits);
@@ -103,6 +109,7 @@ struct SearchSmem {
   int cnt;
   unsigned long long thr;
   int scan_carry[ICB_MAX_G + 1];
+  int wsum2[(ICB_MAX_G + 1) * (kSearchThreads / 32)];
   int misc[8];
   unsigned long long* sortbuf;   // fallback sort buffer (aliases the idle row ring, >= kSortMax keys)
 };
@@ -242,8 +249,11 @@ __device__ void block_sort(SearchSmem& S, int n) {
 // barrier 1 + group.
 constexpr int kBins = 1024;
 constexpr int kBuf = 512;
-constexpr int kSub = 8;                                  // ring slots per consumer warp
-constexpr int kRing = (kSearchThreads / 32 - 1) * kSub;  // 120 slots x 528 B = 63 KB
+#ifndef ICB_STREAM_TMA
+#define ICB_STREAM_TMA 0   // 1: TMA bulk copies + mbarriers; 0: cp.async (measured faster)
+#endif
+constexpr int kSub = 16;                             // ring slots per warp (2 batches of 8 rows)
+constexpr int kRing = (kSearchThreads / 32) * kSub;  // 256 slots x 528 B = 135 KB
 
 struct GroupSmem {
   int hist[kBins];
@@ -321,40 +331,57 @@ __device__ __forceinline__ int group_scan(GroupSmem& GS, int gtid, int bar, int 
   return before;
 }
 
-// Output keys <= thr (and boundary handling done by the caller) with the
-// pool's seen-mark dedup; returns the count written.
+// One pass over the list emitting every key <= thr: their ids to out_ids
+// (from out_ids_base, no dedup) and/or the keys to out_keys (from
+// out_keys_base, skipping ids already marked in `seen` and marking new ones;
+// the emitted keys' d2 range is folded into plo/phi).  8 independent loads in
+// flight per thread.  Returns (ids written, keys written).
 template <int NTG>
-__device__ int group_emit(GroupSmem& GS, int gtid, int bar, const unsigned long long* keys, int M,
-                          unsigned long long thr, unsigned long long* out_keys, int* out_ids, int out_base,
-                          unsigned* seen, unsigned* plo, unsigned* phi) {
+__device__ int2 group_emit(GroupSmem& GS, int gtid, int bar, const unsigned long long* keys, int M,
+                           unsigned long long thr, int* out_ids, int out_ids_base, unsigned long long* out_keys,
+                           int out_keys_base, unsigned* seen, unsigned* plo, unsigned* phi) {
+  constexpr int U = 8;
   const int lane = gtid & 31;
-  if (gtid == 0) GS.misc[0] = 0;
+  if (gtid == 0) { GS.misc[0] = 0; GS.misc[1] = 0; }
   gsync(bar, NTG);
   unsigned mn = 0xffffffffu, mx = 0u;
-  for (int i = gtid; i < M + (NTG - (M % NTG)) % NTG; i += NTG) {
-    bool take = false;
-    unsigned long long k = 0;
-    if (i < M) {
-      k = keys[i];
-      take = k <= thr;
-      if (take && seen) {
-        int id = key_id(k);
-        unsigned bit = 1u << (id & 31);
-        unsigned old = atomicOr(seen + (id >> 5), bit);
-        take = !(old & bit);
-      }
+  const int Mpad = (M + U * NTG - 1) / (U * NTG) * (U * NTG);   // warp-uniform trip count
+  for (int i0 = gtid; i0 < Mpad; i0 += U * NTG) {
+    unsigned long long kk[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * NTG;
+      kk[u] = i < M ? keys[i] : ~0ull;
     }
-    unsigned bal = __ballot_sync(0xffffffffu, take);
-    int base = 0;
-    if (lane == 0 && bal) base = atomicAdd(&GS.misc[0], __popc(bal));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (take) {
-      int pos = out_base + base + __popc(bal & ((1u << lane) - 1));
-      if (out_keys) out_keys[pos] = k;
-      if (out_ids) out_ids[pos] = key_id(k);
-      unsigned hb = (unsigned)(k >> 32);
-      mn = min(mn, hb);
-      mx = max(mx, hb);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const unsigned long long k = kk[u];
+      const bool sel = (i0 + u * NTG < M) && k <= thr;
+      if (out_ids) {
+        const unsigned bal = __ballot_sync(0xffffffffu, sel);
+        int base = 0;
+        if (lane == 0 && bal) base = atomicAdd(&GS.misc[0], __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (sel) out_ids[out_ids_base + base + __popc(bal & ((1u << lane) - 1))] = key_id(k);
+      }
+      if (out_keys) {
+        bool take = sel;
+        if (take && seen) {
+          const int id = key_id(k);
+          const unsigned bit = 1u << (id & 31);
+          take = !(atomicOr(seen + (id >> 5), bit) & bit);
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, take);
+        int base = 0;
+        if (lane == 0 && bal) base = atomicAdd(&GS.misc[1], __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (take) {
+          out_keys[out_keys_base + base + __popc(bal & ((1u << lane) - 1))] = k;
+          const unsigned hb = (unsigned)(k >> 32);
+          mn = min(mn, hb);
+          mx = max(mx, hb);
+        }
+      }
     }
   }
   if (plo) {
@@ -362,10 +389,10 @@ __device__ int group_emit(GroupSmem& GS, int gtid, int bar, const unsigned long 
       mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
       mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     }
-    if (lane == 0) { atomicMin(plo, mn); atomicMax(phi, mx); }
+    if (lane == 0 && mx >= mn) { atomicMin(plo, mn); atomicMax(phi, mx); }
   }
   gsync(bar, NTG);
-  int r = GS.misc[0];
+  const int2 r = make_int2(GS.misc[0], GS.misc[1]);
   gsync(bar, NTG);
   return r;
 }
@@ -464,11 +491,21 @@ __device__ unsigned long long group_threshold(GroupSmem& GS, int gtid, int bar, 
   const int shift = nbits > kBinBits ? nbits - kBinBits : 0;
   for (int i = gtid; i < kBins; i += NTG) GS.hist[i] = 0;
   gsync(bar, NTG);
-  for (int i = gtid; i < M; i += NTG) {
-    unsigned hb = (unsigned)(keys[i] >> 32);
-    ICB_CHECK(hb >= lo && hb <= hi && ((hb - lo) >> shift) < kBins, "hb %u lo %u hi %u shift %d M %d", hb, lo, hi,
-              shift, M);
-    atomicAdd(&GS.hist[(hb - lo) >> shift], 1);
+  for (int i0 = gtid; i0 < M; i0 += 8 * NTG) {   // 8 independent loads in flight per thread
+    unsigned hbs[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * NTG;
+      hbs[u] = i < M ? (unsigned)(keys[i] >> 32) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (i0 + u * NTG >= M) break;
+      const unsigned hb = hbs[u];
+      ICB_CHECK(hb >= lo && hb <= hi && ((hb - lo) >> shift) < kBins, "hb %u lo %u hi %u shift %d M %d", hb, lo,
+                hi, shift, M);
+      atomicAdd(&GS.hist[(hb - lo) >> shift], 1);
+    }
   }
   gsync(bar, NTG);
   // locate the boundary bin: each thread owns kBins / NTG consecutive bins
@@ -494,12 +531,21 @@ __device__ unsigned long long group_threshold(GroupSmem& GS, int gtid, int bar, 
     // gather the boundary bin and sort it
     if (gtid == 0) GS.misc[7] = 0;
     gsync(bar, NTG);
-    for (int i = gtid; i < M; i += NTG) {
-      unsigned long long k = keys[i];
-      if ((int)(((unsigned)(k >> 32) - lo) >> shift) == bstar) {
-        const int at = atomicAdd(&GS.misc[7], 1);
-        ICB_CHECK(at < nb, "boundary gather %d >= %d", at, nb);
-        GS.buf[at] = k;
+    for (int i0 = gtid; i0 < M; i0 += 8 * NTG) {
+      unsigned long long kk[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * NTG;
+        kk[u] = i < M ? keys[i] : ~0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const unsigned long long k = kk[u];
+        if (i0 + u * NTG < M && (int)(((unsigned)(k >> 32) - lo) >> shift) == bstar) {
+          const int at = atomicAdd(&GS.misc[7], 1);
+          ICB_CHECK(at < nb, "boundary gather %d >= %d", at, nb);
+          GS.buf[at] = k;
+        }
       }
     }
     gsync(bar, NTG);
@@ -622,7 +668,18 @@ struct SearchParams {
   int G;
   long long k, beam, visit_cap;
   int target;   // -1 sentinel
+  unsigned long long* prof;   // optional per-phase cycle counters (kPhases), thread 0 of each CTA adds
 };
+
+constexpr int kPhases = 8;
+#define ICB_MARK(k)                                       \
+  do {                                                    \
+    if (P.prof && threadIdx.x == 0) {                     \
+      long long now_ = clock64();                         \
+      atomicAdd(P.prof + (k), (unsigned long long)(now_ - tmark_)); \
+      tmark_ = now_;                                      \
+    }                                                     \
+  } while (0)
 
 // Evaluate the rows `ids[0..n)` against head g (single head; used by the
 // P-DCI path) writing keys to dst.
@@ -720,8 +777,19 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
 #pragma unroll
   for (int g = 0; g < GP; ++g)
     qv[g] = g < G ? reinterpret_cast<const float4*>(S.q[g])[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+  // head pairs packed for the f32x2 path: q2[h][i] = (q_{2h}[4l+i], q_{2h+1}[4l+i])
+  unsigned long long q2[GP / 2 > 0 ? GP / 2 : 1][4];
+#pragma unroll
+  for (int h = 0; h < GP / 2; ++h) {
+    q2[h][0] = pack_f2(qv[2 * h].x, qv[2 * h + 1].x);
+    q2[h][1] = pack_f2(qv[2 * h].y, qv[2 * h + 1].y);
+    q2[h][2] = pack_f2(qv[2 * h].z, qv[2 * h + 1].z);
+    q2[h][3] = pack_f2(qv[2 * h].w, qv[2 * h + 1].w);
+  }
 
+  long long tmark_ = clock64();
   for (int lv = L; lv >= floor; --lv) {
+    ICB_MARK(0);
     // (1) union of the nodes requested by the heads' survivors
     if (lv == L) {
       if (tid == 0) { SS.ulist[0] = F.meta[t].top_node; SS.umask[0] = (int)allmask; S.U = 1; }
@@ -729,134 +797,249 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
     } else {
       if (tid == 0) S.U = 0;
       __syncthreads();
-      for (int g = 0; g < G; ++g) {
-        const int ns = S.nsurv[g];
-        const int* sv = SS.surv + (size_t)g * SS.ccap;
-        for (int i = tid; i < ns; i += NT) {
-          int node = F.own(t, sv[i], lv);
-          ICB_CHECK(node >= 0 && node < F.node_cap, "own(%d, %d) = %d", sv[i], lv, node);
-          unsigned old = atomicOr(SS.nmask + node, 1u << g);
-          if (old == 0) SS.ulist[atomicAdd(&S.U, 1)] = node;
-        }
+      // every (head, survivor) pair in parallel: independent own() lookups
+      int pre[GP + 1];
+      pre[0] = 0;
+#pragma unroll
+      for (int g = 0; g < GP; ++g) pre[g + 1] = pre[g] + (g < G ? S.nsurv[g] : 0);
+      for (int fl = tid; fl < pre[GP]; fl += NT) {
+        int g = 0;
+#pragma unroll
+        for (int h = 1; h < GP; ++h) g += fl >= pre[h] ? 1 : 0;
+        const int s = SS.surv[(size_t)g * SS.ccap + fl - pre[g]];
+        const int node = F.own(t, s, lv);
+        ICB_CHECK(node >= 0 && node < F.node_cap, "own(%d, %d) = %d", s, lv, node);
+        unsigned old = atomicOr(SS.nmask + node, 1u << g);
+        if (old == 0) SS.ulist[atomicAdd(&S.U, 1)] = node;
       }
       __syncthreads();
       for (int i = tid; i < S.U; i += NT) SS.umask[i] = (int)SS.nmask[SS.ulist[i]];
       __syncthreads();
     }
     const int U = S.U;
+    ICB_MARK(1);
     // (2) union prefix (rows to stream) and per-head output offsets over the
     //     union (normal nodes only)
-    if (tid <= G) S.scan_carry[tid] = 0;
+    //     (all heads + the union in one multi-value block scan) and (3a) the
+    //     flattened row list (token, union index) written by the node's thread
+    if (tid <= GP) S.scan_carry[tid] = 0;
     if (tid == 0) S.nbig = 0;
+    if (tid < GP) { GSA[tid].lo = 0xffffffffu; GSA[tid].hi = 0u; }
     __syncthreads();
-    for (int base = 0; base < U; base += NT) {
-      int i = base + tid;
-      int node = i < U ? SS.ulist[i] : 0;
-      int sz = i < U ? F.node_size[F.nd(t, node)] : 0;
-      bool big = sz > ICB_EXHAUSTIVE && (long long)sz > P.visit_cap;
-      unsigned mk = i < U ? (unsigned)SS.umask[i] : 0u;
-      if (i < U && big) atomicAdd(&S.nbig, 1);
-      for (int g = 0; g <= G; ++g) {
-        int v = (i < U && !big && (g == G || ((mk >> g) & 1))) ? sz : 0;
-        int tot;
-        int ex = block_exclusive_scan<NT>(v, S.wsum, tot);
-        if (i < U) {
-          if (g < G) SS.uoff[(size_t)g * F.node_cap + i] = S.scan_carry[g] + ex;
-          else SS.upre[i] = S.scan_carry[G] + ex;
+    constexpr int NPT = 8;   // consecutive union nodes per thread per pass (loads in parallel)
+    for (int base = 0; base < U; base += NT * NPT) {
+      const int i0 = base + tid * NPT;
+      int sz[NPT], off[NPT];
+      unsigned mk[NPT];
+#pragma unroll
+      for (int u = 0; u < NPT; ++u) {
+        sz[u] = 0; off[u] = 0; mk[u] = 0u;
+        if (i0 + u < U) {
+          const size_t x = F.nd(t, SS.ulist[i0 + u]);
+          sz[u] = F.node_size[x];
+          off[u] = F.node_off[x];
+          mk[u] = (unsigned)SS.umask[i0 + u];
         }
-        __syncthreads();
-        if (tid == 0) S.scan_carry[g] += tot;
-        __syncthreads();
       }
+      int v[GP + 1], ex[GP + 1], tot[GP + 1];
+#pragma unroll
+      for (int g = 0; g <= GP; ++g) v[g] = 0;
+#pragma unroll
+      for (int u = 0; u < NPT; ++u) {
+        const bool big = sz[u] > ICB_EXHAUSTIVE && (long long)sz[u] > P.visit_cap;
+        if (big) { atomicAdd(&S.nbig, 1); sz[u] = -sz[u]; continue; }   // negative marks P-DCI nodes
+#pragma unroll
+        for (int g = 0; g < GP; ++g) v[g] += ((mk[u] >> g) & 1) ? sz[u] : 0;
+        v[GP] += sz[u];
+      }
+      block_scan_multi<NT, GP + 1>(v, ex, tot, S.wsum2);
+      int run[GP + 1];
+#pragma unroll
+      for (int g = 0; g <= GP; ++g) run[g] = S.scan_carry[g] + ex[g];
+#pragma unroll
+      for (int u = 0; u < NPT; ++u) {
+        const int i = i0 + u;
+        if (i >= U) break;
+        const int s = sz[u] > 0 ? sz[u] : 0;
+#pragma unroll
+        for (int g = 0; g < GP; ++g) {
+          if (g < G) SS.uoff[(size_t)g * F.node_cap + i] = run[g];
+          run[g] += ((mk[u] >> g) & 1) ? s : 0;
+        }
+        SS.upre[i] = run[GP];
+        SS.umoff[i] = sz[u] > 0 ? off[u] : -1;   // member offset for the copy pass (-1: P-DCI node)
+        run[GP] += s;
+      }
+      __syncthreads();
+      // member copies, one warp per node (coalesced over the contiguous members)
+      const int cend = min(U, base + NT * NPT);
+      for (int i = base + warp; i < cend; i += NT / 32) {
+        const int mo = SS.umoff[i];
+        if (mo < 0) continue;
+        const int up = SS.upre[i];
+        const int s = (i + 1 < cend ? SS.upre[i + 1] : S.scan_carry[GP] + tot[GP]) - up;
+        for (int j = lane; j < s; j += 32) {
+          SS.rlist[2 * (size_t)(up + j)] = mem[mo + j];
+          SS.rlist[2 * (size_t)(up + j) + 1] = i;
+        }
+      }
+      if (tid == 0)
+#pragma unroll
+        for (int g = 0; g <= GP; ++g) S.scan_carry[g] += tot[g];
+      __syncthreads();
     }
     if (tid < G) S.M[tid] = S.scan_carry[tid];
-    if (tid == 0) S.misc[6] = S.scan_carry[G];
+    if (tid == 0) S.misc[6] = S.scan_carry[GP];
     __syncthreads();
     for (int g = 0; g < G; ++g)
       if (S.M[g] > SS.ccap) { if (tid == 0) set_err(F.meta + t, ICB_ERR_CAP_SCRATCH); return; }
-    // (3a) flatten the union's member rows into one list (coalesced copies of
-    //      the contiguous member arrays): entry = (token, union index)
+    ICB_MARK(2);
     const int R = S.misc[6];
-    if (tid < GP) { GSA[tid].lo = 0xffffffffu; GSA[tid].hi = 0u; }
-    for (int i = warp; i < U; i += NT / 32) {
-      const int node = SS.ulist[i];
-      const size_t x = F.nd(t, node);
-      const int sz = F.node_size[x];
-      if (sz > ICB_EXHAUSTIVE && (long long)sz > P.visit_cap) continue;
-      const int off = F.node_off[x], base = SS.upre[i];
-      for (int j = lane; j < sz; j += 32) {
-        SS.rlist[2 * (size_t)(base + j)] = mem[off + j];
-        SS.rlist[2 * (size_t)(base + j) + 1] = i;
-      }
-    }
-    __syncthreads();
-    // (3b) stream the rows through a shared-memory ring: warp 0 is the TMA
-    //      producer (one 528-byte cp.async.bulk per row, completion on the
-    //      slot's mbarrier), warps 1.. consume batches of 8 rows from smem,
-    //      score every row against all heads with the head-transposed
-    //      butterfly (same pairing tree as warp_sum_butterfly) and release
-    //      the slot.  In-flight bytes = ring size, independent of registers.
-    //      Each consumer warp owns kSub slots and consumes them strictly in
-    //      order (its own running row count qp[c]), so no mbarrier can be
-    //      tested two phases ahead.
-    constexpr int NCW = NT / 32 - 1;
-    if (warp == 0) {
-      for (int i0 = 0; i0 < R; i0 += 32) {
-        const int i = i0 + lane;
-        if (i < R) {
-          const int c = (i >> 3) % NCW, k = (i >> 3) / NCW;
-          const unsigned rc = RG.qp[c] + (unsigned)(k * 8 + (i & 7));
-          const int slot = c * kSub + (int)(rc % kSub);
-          const unsigned use = rc / kSub;
-          if (use > 0) mbar_wait(RG.empty + slot, (use - 1) & 1u);
-          const int tok = SS.rlist[2 * (size_t)i];
-          mbar_expect_tx(RG.full + slot, ICB_ROWF * 4);
-          bulk_g2s(RG.ring + (size_t)slot * ICB_ROWF, F.row(t, tok), ICB_ROWF * 4, RG.full + slot);
-        }
-      }
-    } else {
+    ICB_MARK(3);
+    // (3b) stream the rows through shared memory with TMA bulk copies.  Every
+    //      warp owns a private kSub-slot ring (two batches of 8 rows): lanes
+    //      0..7 issue the 528-byte cp.async.bulk copies of the warp's batch
+    //      after next while the warp scores the current batch from smem
+    //      against all heads (head-transposed butterfly, same pairing tree as
+    //      warp_sum_butterfly).  Batches go to warps round-robin; a warp's
+    //      running batch count (qp[warp], persistent across levels and calls)
+    //      fixes the slot set (count & 1) and the mbarrier phase (count >> 1);
+    //      missing rows of a partial batch complete their slot's phase with a
+    //      plain arrive.  A warp only ever waits on its own slots, in order.
+    {
+      constexpr int NW = NT / 32;
       constexpr int LPG = 32 / GP;              // lanes holding one head's sum
       constexpr int SLOTS = (8 + LPG - 1) / LPG;
       const int myh = lane / LPG;
       const float qt_my = S.qt[myh];
-      const int cw = warp - 1;
-      const unsigned qc = RG.qp[cw];
-      unsigned mn = 0xffffffffu, mx = 0u;
-      for (int base = cw * 8, kb = 0; base < R; base += NCW * 8, ++kb) {
-        const int nrow = min(8, R - base);
-        int e_tok = 0, e_idx = 0;
-        if (lane < nrow) {
-          e_tok = SS.rlist[2 * (size_t)(base + lane)];
-          e_idx = SS.rlist[2 * (size_t)(base + lane) + 1];
+      const unsigned qb = RG.qp[warp];
+      float* wring = RG.ring + (size_t)warp * kSub * ICB_ROWF;
+      unsigned long long* wfull = RG.full + warp * kSub;
+      const int nb = (R + 7) / 8;
+      // per-row metadata, prefetched two batches ahead by lanes 0..7: token,
+      // requesting-head mask and, per head, the row's output slot
+      struct RowMeta {
+        int tok;
+        int mask;
+        int pos[GP];
+      };
+      auto load_tok = [&](int kb, RowMeta& m, int& ix) {
+        const int j = warp + kb * NW;
+        m.tok = 0;
+        m.mask = 0;
+        ix = 0;
+        if (j < nb && lane < 8 && 8 * j + lane < R) {
+          const int r = 8 * j + lane;
+          m.tok = SS.rlist[2 * (size_t)r];
+          ix = SS.rlist[2 * (size_t)r + 1];
+          m.mask = SS.umask[ix];
+          const int rel = r - SS.upre[ix];
+#pragma unroll
+          for (int g = 0; g < GP; ++g) m.pos[g] = g < G ? SS.uoff[(size_t)g * F.node_cap + ix] + rel : 0;
         }
+      };
+#if ICB_STREAM_TMA
+      auto issue = [&](int kb, int tk) {
+        const int j = warp + kb * NW;
+        if (j < nb && lane < 8) {
+          const int slot = (int)(((qb + (unsigned)kb) & 1u) * 8) + lane;
+          if (8 * j + lane < R) {
+            mbar_expect_tx(wfull + slot, ICB_ROWF * 4);
+            bulk_g2s(wring + (size_t)slot * ICB_ROWF, F.row(t, tk), ICB_ROWF * 4, wfull + slot);
+          } else {
+            mbar_arrive(wfull + slot);
+          }
+        }
+      };
+#else
+      // LDGSTS variant: the whole warp copies each 528-byte row (16 B per
+      // lane + the tail by lane 0), one commit group per batch
+      auto issue = [&](int kb, int tk) {
+        const int j = warp + kb * NW;
+        if (j < nb) {
+          const int sb = (kb & 1) * 8;
+          const int nr = min(8, R - 8 * j);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int tu = __shfl_sync(0xffffffffu, tk, u);
+            if (u < nr) {
+              const float* src = F.row(t, tu);
+              float* dst = wring + (size_t)(sb + u) * ICB_ROWF;
+              cp_async16(dst + lane * 4, src + lane * 4);
+              if (lane == 0) cp_async16(dst + ICB_DPAD, src + ICB_DPAD);
+            }
+          }
+        }
+        cp_async_commit();
+      };
+#endif
+      RowMeta m0, m1;
+      int ix0, ix1;
+      load_tok(0, m0, ix0);
+      load_tok(1, m1, ix1);
+      issue(0, m0.tok);
+      issue(1, m1.tok);
+      unsigned mn = 0xffffffffu, mx = 0u;
+      int kb = 0;
+      for (int j = warp; j < nb; j += NW, ++kb) {
+        const int base = 8 * j;
+        const int nrow = min(8, R - base);
+        RowMeta m2;
+        int ix2;
+        load_tok(kb + 2, m2, ix2);   // prefetched; used after this batch
+        (void)ix2;
+#if ICB_STREAM_TMA
+        const unsigned cnt = qb + (unsigned)kb;
+        const int sbase = (int)((cnt & 1u) * 8);
+        const unsigned par = (cnt >> 1) & 1u;
+#else
+        const int sbase = (kb & 1) * 8;
+        cp_async_wait<1>();   // this batch's group has landed (the next one may be in flight)
+        __syncwarp();         // ...and every lane's part of it is visible to the warp
+#endif
         float keep[SLOTS];
+        // branch-free over the 8 rows (rows >= nrow score stale smem and are
+        // never stored) so the 8 independent reduction chains interleave
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          if (u >= nrow) break;
-          const unsigned rc = qc + (unsigned)(kb * 8 + u);
-          const int slot = cw * kSub + (int)(rc % kSub);
-          mbar_wait(RG.full + slot, (rc / kSub) & 1u);
-          const float* srow = RG.ring + (size_t)slot * ICB_ROWF;
+#if ICB_STREAM_TMA
+          mbar_wait(wfull + sbase + u, par);
+#endif
+          const float* srow = wring + (size_t)(sbase + u) * ICB_ROWF;
           const float4 p = reinterpret_cast<const float4*>(srow)[lane];
           const float tl = srow[ICB_DPAD];
           float v[GP];
+          if constexpr (GP == 1) {
+            v[0] = lane_sq4(p, qv[0]);
+          } else {
 #pragma unroll
-          for (int g = 0; g < GP; ++g) v[g] = lane_sq4(p, qv[g]);
+            for (int h = 0; h < GP / 2; ++h) {
+              const float2 r2 = lane_sq4_x2(p, q2[h]);
+              v[2 * h] = r2.x;
+              v[2 * h + 1] = r2.y;
+            }
+          }
           float f = reduce_heads<GP>(v, lane);
           float d2 = d2_finish(f, tl, qt_my);
-          // every lane's smem reads have retired (the butterfly consumed them)
-          __syncwarp();
-          if (lane == 0) mbar_arrive(RG.empty + slot);
           if ((u % LPG) == (lane % LPG)) keep[u / LPG] = d2;
         }
+        // every lane's smem reads of this batch have retired (the butterflies
+        // consumed them): its slots take the batch after next
+        __syncwarp();
+        issue(kb + 2, m2.tok);
 #pragma unroll
         for (int sl = 0; sl < SLOTS; ++sl) {
           const int u = sl * LPG + (lane % LPG);
           const int src = u < 8 ? u : 0;
-          const int tok = __shfl_sync(0xffffffffu, e_tok, src);
-          const int idx = __shfl_sync(0xffffffffu, e_idx, src);
-          if (u < nrow && myh < G && ((SS.umask[idx] >> myh) & 1)) {
-            const int pos = SS.uoff[(size_t)myh * F.node_cap + idx] + (base + u - SS.upre[idx]);
+          const int tok = __shfl_sync(0xffffffffu, m0.tok, src);
+          const int msk = __shfl_sync(0xffffffffu, m0.mask, src);
+          int pos = 0;
+#pragma unroll
+          for (int g = 0; g < GP; ++g) {
+            const int pg = __shfl_sync(0xffffffffu, m0.pos[g], src);
+            if (g == myh) pos = pg;
+          }
+          if (u < nrow && myh < G && ((msk >> myh) & 1)) {
             ICB_CHECK(pos >= 0 && pos < S.M[myh], "cand pos %d M %d", pos, S.M[myh]);
             SS.cand[(size_t)myh * SS.ccap + pos] = make_key(keep[sl], tok);
             const unsigned hb = __float_as_uint(keep[sl]);
@@ -864,6 +1047,10 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
             mx = max(mx, hb);
           }
         }
+        m0 = m1;
+        m1 = m2;
+        (void)ix0;
+        (void)ix1;
       }
       // per-head d2 range of this level's candidates (feeds the selection bins)
 #pragma unroll
@@ -875,15 +1062,12 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
         atomicMin(&GSA[myh].lo, mn);
         atomicMax(&GSA[myh].hi, mx);
       }
+      __syncwarp();
+      if (lane == 0) RG.qp[warp] = qb + (unsigned)kb;   // batches this warp consumed
     }
     if (tid == 0) S.misc[5] = R;
     __syncthreads();
-    if (tid < NCW) {   // advance every consumer's running row count by its rows of this level
-      const int nb = (R + 7) / 8;
-      int rows = 0;
-      for (int j = tid; j < nb; j += NCW) rows += min(8, R - 8 * j);
-      RG.qp[tid] += (unsigned)rows;
-    }
+    ICB_MARK(4);
     // (4) P-DCI truncated nodes (rare): block-wide, per node and head
     if (S.nbig > 0) {
       for (int i = 0; i < U; ++i) {
@@ -914,6 +1098,7 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
     if (lv < L)
       for (int i = tid; i < U; i += NT) SS.nmask[SS.ulist[i]] = 0u;
     __syncthreads();
+    ICB_MARK(5);
     // (7) per-head selection, heads in parallel (one warp group per head).
     //     Survivors = top-beam (dci.py:359-361).  The pool collects, without
     //     duplicates, every survivor (a superset of the level's top-k since
@@ -928,20 +1113,21 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
       gsync(gbar, NTG);
       if (lv > floor) {
         unsigned long long thr = group_threshold<NTG>(GS, gtid, gbar, cg, M, P.beam, GS.lo, GS.hi);
-        int ns = group_emit<NTG>(GS, gtid, gbar, cg, M, thr, nullptr, SS.surv + (size_t)g * SS.ccap, 0,
-                                 nullptr, nullptr, nullptr);
-        if (collect_all) {
-          int np = group_emit<NTG>(GS, gtid, gbar, cg, M, thr, pg, nullptr, S.npool[g], sg, &GS.plo, &GS.phi);
-          if (gtid == 0) S.npool[g] += np;
+        const int2 r = group_emit<NTG>(GS, gtid, gbar, cg, M, thr, SS.surv + (size_t)g * SS.ccap, 0,
+                                       collect_all ? pg : nullptr, S.npool[g], sg, &GS.plo, &GS.phi);
+        if (gtid == 0) {
+          S.nsurv[g] = r.x;
+          S.npool[g] += r.y;
         }
-        if (gtid == 0) S.nsurv[g] = ns;
       } else {
         unsigned long long thr = group_threshold<NTG>(GS, gtid, gbar, cg, M, P.k, GS.lo, GS.hi);
-        int np = group_emit<NTG>(GS, gtid, gbar, cg, M, thr, pg, nullptr, S.npool[g], sg, &GS.plo, &GS.phi);
-        if (gtid == 0) S.npool[g] += np;
+        const int2 r = group_emit<NTG>(GS, gtid, gbar, cg, M, thr, nullptr, 0, pg, S.npool[g], sg, &GS.plo,
+                                       &GS.phi);
+        if (gtid == 0) S.npool[g] += r.y;
       }
     }
     __syncthreads();
+    ICB_MARK(6);
   }
 }
 
@@ -967,7 +1153,7 @@ __device__ int finalize_groups(SearchSmem& S, GroupSmem* GSA, const ForestView& 
     const long long want = min((long long)np, k);
     unsigned long long thr = group_threshold<NTG>(GS, gtid, gbar, pg, np, want, GS.plo, GS.phi);
     // emit into a scratch region (the threshold pass may have used buf)
-    n = group_emit<NTG>(GS, gtid, gbar, pg, np, thr, GS.buf, nullptr, 0, nullptr, nullptr, nullptr);
+    n = group_emit<NTG>(GS, gtid, gbar, pg, np, thr, nullptr, 0, GS.buf, 0, nullptr, nullptr, nullptr).y;
     group_sort<NTG>(GS, gtid, gbar, n);
   }
   __syncthreads();

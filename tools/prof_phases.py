@@ -1,0 +1,34 @@
+"""Per-phase cycle breakdown of the search kernel at C2 (ICB_PROF=1)."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+os.environ["ICB_PROF"] = "1"
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2604_10539_b200 import _native as N  # noqa: E402
+from paper_2604_10539_b200.engine import Engine, EngineConfig  # noqa: E402
+from paper_2604_10539_b200.workload import clustered_stream  # noqa: E402
+
+ctx = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
+C2 = dict(layers=32, kv_heads=8, query_heads_per_group=4, d=128, d_prime=128, page_size=16,
+          token_budget=256, promotion_ratio=0.1, sink_pages=1, window_pages=2, skip_layers=2)
+st = clustered_stream(ctx, 40, 32, 8, 4, 128, 128, device="cuda")
+eng = Engine(EngineConfig(**C2, kv_dtype="bf16", max_tokens=ctx + 64)).prefill(st.keys, st.values, ctx)
+lib = N.lib()
+lib.icb_search_profile.argtypes = [ctypes.c_void_p, ctypes.c_int]
+buf = np.zeros(8, dtype=np.uint64)
+for i in range(4):
+    eng.decode_step(ctx + i, st.queries[i], st.keys[ctx + i], st.values[ctx + i], metrics=False)
+lib.icb_search_profile(buf.ctypes.data_as(ctypes.c_void_p), 1)
+for i in range(4, 12):
+    eng.decode_step(ctx + i, st.queries[i], st.keys[ctx + i], st.values[ctx + i], metrics=False)
+lib.icb_search_profile(buf.ctypes.data_as(ctypes.c_void_p), 1)
+names = ["union", "scans", "rowlist", "stream", "pdci+ctr", "select", "tail", "finalize"]
+tot = buf.sum()
+per_cta_us = buf / (8 * eng.T) / 1.9e3
+for n, v, u in zip(names, buf, per_cta_us):
+    print(f"{n:10s} {v / tot * 100:5.1f}%  {u:8.1f} us per CTA-query")
