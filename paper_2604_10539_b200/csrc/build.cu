@@ -76,7 +76,7 @@ __global__ void build_lift_kernel(ForestView F, BuildArgs A, const double* nsq) 
     double rad = __dsub_rn(1.0, __dmul_rn(ratio, ratio));
     const float tl = __double2float_rn(sqrt(rad > 0.0 ? rad : 0.0));
     F.tail[F.tk(t, tok)] = tl;
-    row[ICB_DPAD] = tl;
+    if (ICB_ROWF > ICB_DPAD) row[ICB_DPAD] = tl;
     if (over) atomicAdd(&m->scale_clamps, 1ull);
     int old = atomicCAS(F.tok2page + F.tk(t, tok), -1, -2);
     if (old != -1) set_err(m, ICB_ERR_DUP_ID);

@@ -35,7 +35,7 @@
 #endif
 
 #define ICB_DPAD 128          // key dims held per row; dims >= d are zero
-#define ICB_ROWF 132          // row stride in floats: [128 dims | tail | 3 zero] = 528 B, one bulk copy
+#define ICB_ROWF 128          // row stride in floats: 512 B = exactly four 128-B lines (tail kept in F.tail)
 #define ICB_NPROJ 8           // NUM_PROJECTIONS (dci.py:44)
 #define ICB_EXHAUSTIVE 64     // EXHAUSTIVE_NODE_LIMIT (dci.py:41)
 #define ICB_MAX_WINDOW 8

@@ -156,7 +156,7 @@ __device__ int insert_one(SearchSmem& S, GroupSmem* GSA, const RingView& RG, con
     double rad = __dsub_rn(1.0, __dmul_rn(ratio, ratio));
     float tl = __double2float_rn(sqrt(rad > 0.0 ? rad : 0.0));
     F.tail[F.tk(t, tok)] = tl;
-    row[ICB_DPAD] = tl;
+    if (ICB_ROWF > ICB_DPAD) row[ICB_DPAD] = tl;
     S.qt[0] = tl;
     if (over) m->scale_clamps += 1;
     F.level[F.tk(t, tok)] = (int8_t)s_level;

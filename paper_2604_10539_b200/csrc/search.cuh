@@ -896,16 +896,14 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
     ICB_MARK(2);
     const int R = S.misc[6];
     ICB_MARK(3);
-    // (3b) stream the rows through shared memory with TMA bulk copies.  Every
-    //      warp owns a private kSub-slot ring (two batches of 8 rows): lanes
-    //      0..7 issue the 528-byte cp.async.bulk copies of the warp's batch
-    //      after next while the warp scores the current batch from smem
-    //      against all heads (head-transposed butterfly, same pairing tree as
-    //      warp_sum_butterfly).  Batches go to warps round-robin; a warp's
-    //      running batch count (qp[warp], persistent across levels and calls)
-    //      fixes the slot set (count & 1) and the mbarrier phase (count >> 1);
-    //      missing rows of a partial batch complete their slot's phase with a
-    //      plain arrive.  A warp only ever waits on its own slots, in order.
+    // (3b) stream the rows through shared memory.  Every warp owns a private
+    //      kSub-slot ring (two batches of 8 rows): it issues the async copies
+    //      (cp.async, one 512-byte row per instruction) of its batch after
+    //      next while it scores the current batch from smem against all heads
+    //      (packed f32x2 lane partials, head-transposed butterfly with the
+    //      pairing tree of warp_sum_butterfly).  Batches go to warps
+    //      round-robin.  (A TMA cp.async.bulk + mbarrier ring was measured to
+    //      be no faster for 512-byte rows.)
     {
       constexpr int NW = NT / 32;
       constexpr int LPG = 32 / GP;              // lanes holding one head's sum
@@ -916,44 +914,47 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
       float* wring = RG.ring + (size_t)warp * kSub * ICB_ROWF;
       unsigned long long* wfull = RG.full + warp * kSub;
       const int nb = (R + 7) / 8;
-      // per-row metadata, prefetched two batches ahead by lanes 0..7: token,
-      // requesting-head mask and, per head, the row's output slot
+      // Row metadata pipeline, lanes 0..7 holding one row each:
+      //   stage A, three batches ahead: token and union index (row list);
+      //   stage B, two batches ahead: lifted tail, requesting-head mask and
+      //   the row's output slot per head (gathers that depend on stage A).
+      struct RowTok {
+        int tok, ix;
+      };
       struct RowMeta {
         int tok;
+        float tail;
         int mask;
         int pos[GP];
       };
-      auto load_tok = [&](int kb, RowMeta& m, int& ix) {
+      auto load_a = [&](int kb) {
+        RowTok a{0, -1};
         const int j = warp + kb * NW;
-        m.tok = 0;
-        m.mask = 0;
-        ix = 0;
         if (j < nb && lane < 8 && 8 * j + lane < R) {
-          const int r = 8 * j + lane;
-          m.tok = SS.rlist[2 * (size_t)r];
-          ix = SS.rlist[2 * (size_t)r + 1];
-          m.mask = SS.umask[ix];
-          const int rel = r - SS.upre[ix];
+          a.tok = SS.rlist[2 * (size_t)(8 * j + lane)];
+          a.ix = SS.rlist[2 * (size_t)(8 * j + lane) + 1];
+        }
+        return a;
+      };
+      auto load_b = [&](int kb, const RowTok& a) {
+        RowMeta m;
+        m.tok = a.tok;
+        m.tail = 0.f;
+        m.mask = 0;
 #pragma unroll
-          for (int g = 0; g < GP; ++g) m.pos[g] = g < G ? SS.uoff[(size_t)g * F.node_cap + ix] + rel : 0;
+        for (int g = 0; g < GP; ++g) m.pos[g] = 0;
+        if (a.ix >= 0) {
+          const int r = 8 * (warp + kb * NW) + lane;
+          m.tail = F.tail[F.tk(t, a.tok)];
+          m.mask = SS.umask[a.ix];
+          const int rel = r - SS.upre[a.ix];
+#pragma unroll
+          for (int g = 0; g < GP; ++g) m.pos[g] = g < G ? SS.uoff[(size_t)g * F.node_cap + a.ix] + rel : 0;
         }
+        return m;
       };
-#if ICB_STREAM_TMA
-      auto issue = [&](int kb, int tk) {
-        const int j = warp + kb * NW;
-        if (j < nb && lane < 8) {
-          const int slot = (int)(((qb + (unsigned)kb) & 1u) * 8) + lane;
-          if (8 * j + lane < R) {
-            mbar_expect_tx(wfull + slot, ICB_ROWF * 4);
-            bulk_g2s(wring + (size_t)slot * ICB_ROWF, F.row(t, tk), ICB_ROWF * 4, wfull + slot);
-          } else {
-            mbar_arrive(wfull + slot);
-          }
-        }
-      };
-#else
-      // LDGSTS variant: the whole warp copies each 528-byte row (16 B per
-      // lane + the tail by lane 0), one commit group per batch
+      // LDGSTS: the warp copies each 512-byte row with one instruction (16 B
+      // per lane, four full 128-B lines), one commit group per batch
       auto issue = [&](int kb, int tk) {
         const int j = warp + kb * NW;
         if (j < nb) {
@@ -962,21 +963,14 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const int tu = __shfl_sync(0xffffffffu, tk, u);
-            if (u < nr) {
-              const float* src = F.row(t, tu);
-              float* dst = wring + (size_t)(sb + u) * ICB_ROWF;
-              cp_async16(dst + lane * 4, src + lane * 4);
-              if (lane == 0) cp_async16(dst + ICB_DPAD, src + ICB_DPAD);
-            }
+            if (u < nr) cp_async16(wring + (size_t)(sb + u) * ICB_ROWF + lane * 4, F.row(t, tu) + lane * 4);
           }
         }
         cp_async_commit();
       };
-#endif
-      RowMeta m0, m1;
-      int ix0, ix1;
-      load_tok(0, m0, ix0);
-      load_tok(1, m1, ix1);
+      RowTok a2 = load_a(2);
+      RowMeta m0 = load_b(0, load_a(0));
+      RowMeta m1 = load_b(1, load_a(1));
       issue(0, m0.tok);
       issue(1, m1.tok);
       unsigned mn = 0xffffffffu, mx = 0u;
@@ -984,30 +978,19 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
       for (int j = warp; j < nb; j += NW, ++kb) {
         const int base = 8 * j;
         const int nrow = min(8, R - base);
-        RowMeta m2;
-        int ix2;
-        load_tok(kb + 2, m2, ix2);   // prefetched; used after this batch
-        (void)ix2;
-#if ICB_STREAM_TMA
-        const unsigned cnt = qb + (unsigned)kb;
-        const int sbase = (int)((cnt & 1u) * 8);
-        const unsigned par = (cnt >> 1) & 1u;
-#else
+        const RowTok a3 = load_a(kb + 3);       // stage A for the batch three ahead
+        const RowMeta m2 = load_b(kb + 2, a2);  // stage B for the batch two ahead
         const int sbase = (kb & 1) * 8;
         cp_async_wait<1>();   // this batch's group has landed (the next one may be in flight)
         __syncwarp();         // ...and every lane's part of it is visible to the warp
-#endif
         float keep[SLOTS];
         // branch-free over the 8 rows (rows >= nrow score stale smem and are
         // never stored) so the 8 independent reduction chains interleave
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-#if ICB_STREAM_TMA
-          mbar_wait(wfull + sbase + u, par);
-#endif
           const float* srow = wring + (size_t)(sbase + u) * ICB_ROWF;
           const float4 p = reinterpret_cast<const float4*>(srow)[lane];
-          const float tl = srow[ICB_DPAD];
+          const float tl = __shfl_sync(0xffffffffu, m0.tail, u);
           float v[GP];
           if constexpr (GP == 1) {
             v[0] = lane_sq4(p, qv[0]);
@@ -1026,7 +1009,7 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
         // every lane's smem reads of this batch have retired (the butterflies
         // consumed them): its slots take the batch after next
         __syncwarp();
-        issue(kb + 2, m2.tok);
+        issue(kb + 2, a2.tok);
 #pragma unroll
         for (int sl = 0; sl < SLOTS; ++sl) {
           const int u = sl * LPG + (lane % LPG);
@@ -1049,8 +1032,7 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
         }
         m0 = m1;
         m1 = m2;
-        (void)ix0;
-        (void)ix1;
+        a2 = a3;
       }
       // per-head d2 range of this level's candidates (feeds the selection bins)
 #pragma unroll

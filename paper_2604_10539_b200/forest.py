@@ -19,7 +19,7 @@ from . import _native as N
 from .errors import ConfigError, InputError
 
 DPAD = 128
-ROWF = 132   # device row stride in floats: 128 dims, the lifted tail, 3 zeros
+ROWF = 128   # device row stride in floats (512 B); the lifted tail lives in its own array
 
 
 def entropy_words(seed) -> list[int]:
@@ -285,7 +285,6 @@ class DeviceForest:
         if with_rows:
             rows = lift.reshape(cp.tok_cap, ROWF)
             out["lift"] = rows[:, :DPAD]
-            out["row_tail"] = rows[:, DPAD]
             out["tail"] = tail
         return out
 
