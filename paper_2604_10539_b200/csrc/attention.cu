@@ -53,6 +53,33 @@ struct HeadAcc {
   float4 acc;
 };
 
+template <int H, int OFF>
+__device__ __forceinline__ float head_sums_rest(const float (&w)[H], int lane) {
+  if constexpr (H == 1) {
+    float s = w[0];
+#pragma unroll
+    for (int o = OFF; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+  } else {
+    constexpr int H2 = H / 2;
+    float x[H2];
+    const bool up = lane & OFF;
+#pragma unroll
+    for (int i = 0; i < H2; ++i) {
+      float send = up ? w[i] : w[i + H2];
+      x[i] = (up ? w[i + H2] : w[i]) + __shfl_xor_sync(0xffffffffu, send, OFF);
+    }
+    return head_sums_rest<H2, OFF / 2>(x, lane);
+  }
+}
+
+// Sum of each head's lane partials transposed across heads: lane l ends with
+// head l / (32/G)'s total after G/2 + G/4 + ... + (5 - log2 G) shuffles.
+template <int G>
+__device__ __forceinline__ float head_sums(const float (&v)[G], int lane) {
+  return head_sums_rest<G, 16>(v, lane);
+}
+
 template <typename KT, int G>
 __device__ __forceinline__ void attend_row(HeadAcc (&h)[G], const float4 (&qv)[G], const KT* krow, const KT* vrow,
                                            int lane, int dim, int dim_v, float scale_log2) {
@@ -61,21 +88,33 @@ __device__ __forceinline__ void attend_row(HeadAcc (&h)[G], const float4 (&qv)[G
   float s[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) s[g] = qv[g].x * k.x + qv[g].y * k.y + qv[g].z * k.z + qv[g].w * k.w;
+  if constexpr (G == 1) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
+    for (int o = 16; o > 0; o >>= 1) s[0] += __shfl_xor_sync(0xffffffffu, s[0], o);
+  } else {
+    // transposed reduction (head g's sum lands in lanes g*32/G...), then broadcast
+    const float mine = head_sums<G>(s, lane);
 #pragma unroll
-    for (int g = 0; g < G; ++g) s[g] += __shfl_xor_sync(0xffffffffu, s[g], o);
+    for (int g = 0; g < G; ++g) s[g] = __shfl_sync(0xffffffffu, mine, g * (32 / G));
+  }
 #pragma unroll
   for (int g = 0; g < G; ++g) {
-    float x = s[g] * scale_log2;
-    float mn = fmaxf(h[g].m, x);
-    float a = exp2f(h[g].m - mn), p = exp2f(x - mn);
-    h[g].l = h[g].l * a + p;
-    h[g].acc.x = h[g].acc.x * a + p * v.x;
-    h[g].acc.y = h[g].acc.y * a + p * v.y;
-    h[g].acc.z = h[g].acc.z * a + p * v.z;
-    h[g].acc.w = h[g].acc.w * a + p * v.w;
-    h[g].m = mn;
+    const float x = s[g] * scale_log2;   // identical in every lane: the branch is warp-uniform
+    if (x > h[g].m) {                    // rescale only when the running max grows
+      const float a = exp2f(h[g].m - x);
+      h[g].l *= a;
+      h[g].acc.x *= a;
+      h[g].acc.y *= a;
+      h[g].acc.z *= a;
+      h[g].acc.w *= a;
+      h[g].m = x;
+    }
+    const float p = exp2f(x - h[g].m);
+    h[g].l += p;
+    h[g].acc.x += p * v.x;
+    h[g].acc.y += p * v.y;
+    h[g].acc.z += p * v.z;
+    h[g].acc.w += p * v.w;
   }
 }
 
