@@ -14,6 +14,9 @@ namespace icb {
 
 constexpr int kAttnThreads = 256;
 
+// kernels are instantiated for G in {1,2,4,8}; other GQA ratios run padded
+inline int padded_g(int G) { return G <= 2 ? G : G <= 4 ? 4 : 8; }
+
 template <typename KT>
 __device__ __forceinline__ float4 load4(const KT* p);
 template <>
@@ -130,13 +133,15 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(ForestView F, AttnAr
   __shared__ float4 s_acc[kAttnThreads / 32][G][32];
   __shared__ bool s_last;
   const int t = PAGED ? A.trees[b] : 0;
+  const int GA = A.G;   // actual heads; G is the instantiated (padded) count, extra heads see q = 0
   float4 qv[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
-    const float* q = A.q + ((size_t)b * G + g) * A.dim;
+    const float* q = A.q + ((size_t)b * GA + g) * A.dim;
     const int j = lane * 4;
-    qv[g] = make_float4(j < A.dim ? q[j] : 0.f, j + 1 < A.dim ? q[j + 1] : 0.f, j + 2 < A.dim ? q[j + 2] : 0.f,
-                        j + 3 < A.dim ? q[j + 3] : 0.f);
+    const bool on = g < GA;
+    qv[g] = make_float4(on && j < A.dim ? q[j] : 0.f, on && j + 1 < A.dim ? q[j + 1] : 0.f,
+                        on && j + 2 < A.dim ? q[j + 2] : 0.f, on && j + 3 < A.dim ? q[j + 3] : 0.f);
   }
   HeadAcc h[G];
 #pragma unroll
@@ -249,7 +254,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(ForestView F, AttnAr
   if (!s_last) return;
   __threadfence();
   const float* pb = A.part + (size_t)b * S * G * (2 + A.dim_v);
-  for (int x = threadIdx.x; x < G * A.dim_v; x += kAttnThreads) {
+  for (int x = threadIdx.x; x < GA * A.dim_v; x += kAttnThreads) {
     int g = x / A.dim_v, j = x % A.dim_v;
     float mx = -INFINITY;
     for (int s = 0; s < S; ++s) mx = fmaxf(mx, __ldcg(pb + ((size_t)s * G + g) * (2 + A.dim_v)));
@@ -261,14 +266,14 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(ForestView F, AttnAr
       l += __ldcg(pg + 1) * sc;
       acc += __ldcg(pg + 2 + j) * sc;
     }
-    A.out[((size_t)b * G + g) * A.dim_v + j] = acc / l;
+    A.out[((size_t)b * GA + g) * A.dim_v + j] = acc / l;
   }
   if (threadIdx.x == 0) A.counter[b] = 0;   // ready for the next launch
 }
 
 template <typename KT, bool PAGED>
 void launch_attn(int G, dim3 grid, cudaStream_t st, const ForestView& F, const AttnArgs& A) {
-  switch (G) {
+  switch (padded_g(G)) {
     case 1: attn_kernel<KT, 1, PAGED><<<grid, kAttnThreads, 0, st>>>(F, A); break;
     case 2: attn_kernel<KT, 2, PAGED><<<grid, kAttnThreads, 0, st>>>(F, A); break;
     case 4: attn_kernel<KT, 4, PAGED><<<grid, kAttnThreads, 0, st>>>(F, A); break;
@@ -300,13 +305,13 @@ static int ensure_attn_scratch(icb_forest* f, size_t part_floats, int n, float**
   return ICB_OK;
 }
 
-static bool valid_g(int G) { return G == 1 || G == 2 || G == 4 || G == 8; }
+static bool valid_g(int G) { return G >= 1 && G <= 8; }
 
 int icb_attention_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, const float* queries,
                        const int32_t* pages, int32_t pages_cap, const int32_t* npages, float* out,
                        int64_t* stats, int32_t scalar_bytes, int32_t splits, cudaStream_t st) {
   if (n <= 0) return ICB_OK;
-  if (!valid_g(G)) { icb_set_error(ICB_E_CONFIG, "attention supports G in {1,2,4,8}"); return ICB_E_CONFIG; }
+  if (!valid_g(G)) { icb_set_error(ICB_E_CONFIG, "attention supports 1 <= G <= 8"); return ICB_E_CONFIG; }
   const auto& c = f->cfg;
   if (splits <= 0) splits = std::max(1, std::min(8, (2 * 148 + n - 1) / n));
   AttnArgs A{};
@@ -314,7 +319,7 @@ int icb_attention_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t G
   A.pages = pages; A.pages_cap = pages_cap; A.npages = npages; A.out = out; A.stats = stats;
   A.scalar_bytes = scalar_bytes;
   A.scale_log2 = (float)(1.4426950408889634 / sqrt((double)c.dim));
-  int rc = ensure_attn_scratch(f, (size_t)n * splits * G * (2 + c.dim_v), n, &A.part, &A.counter);
+  int rc = ensure_attn_scratch(f, (size_t)n * splits * padded_g(G) * (2 + c.dim_v), n, &A.part, &A.counter);
   if (rc) return rc;
   dim3 grid(n, splits);
   if (c.kv_dtype == ICB_KV_BF16) launch_attn<__nv_bfloat16, true>(G, grid, st, f->view, A);
@@ -327,13 +332,13 @@ int icb_dense_attention_impl(int32_t n, int32_t G, int32_t dim, int32_t dim_v, i
                              const void* k, const void* v, int64_t ld, int32_t n_tokens, float* out,
                              int32_t splits, cudaStream_t st) {
   if (n <= 0) return ICB_OK;
-  if (!valid_g(G)) { icb_set_error(ICB_E_CONFIG, "attention supports G in {1,2,4,8}"); return ICB_E_CONFIG; }
+  if (!valid_g(G)) { icb_set_error(ICB_E_CONFIG, "attention supports 1 <= G <= 8"); return ICB_E_CONFIG; }
   if (splits <= 0) splits = std::max(1, std::min((n_tokens + 255) / 256, (4 * 148 + n - 1) / n));
   AttnArgs A{};
   A.n = n; A.G = G; A.dim = dim; A.dim_v = dim_v; A.splits = splits; A.q = q; A.k = k; A.v = v; A.ld = ld;
   A.n_tokens = n_tokens; A.out = out;
   A.scale_log2 = (float)(1.4426950408889634 / sqrt((double)dim));
-  int rc = ensure_attn_scratch(nullptr, (size_t)n * splits * G * (2 + dim_v), n, &A.part, &A.counter);
+  int rc = ensure_attn_scratch(nullptr, (size_t)n * splits * padded_g(G) * (2 + dim_v), n, &A.part, &A.counter);
   if (rc) return rc;
   ForestView F{};
   dim3 grid(n, splits);
