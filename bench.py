@@ -35,7 +35,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-E2E_STEPS = 16
+E2E_STEPS = 64
 METRIC = "decode tokens/s (TPOT) at 32k ctx, 256-token budget; DCI top-k query µs/head"
 C2 = dict(layers=32, kv_heads=8, query_heads_per_group=4, d=128, d_prime=128, page_size=16,
           token_budget=256, promotion_ratio=0.1, sink_pages=1, window_pages=2, skip_layers=2)
@@ -204,10 +204,7 @@ def run_ours(args, rank, world):
     gpu_launches = launches[0]
     info1 = [f.info(t) for t in range(eng.T)]
     f.check()
-    ms_t = torch.tensor([ms], dtype=torch.float64)
-    if world > 1:
-        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
+    ms_max = rank_max(ms, dev, world)
     q_ms = [ev_q0[j].elapsed_time(ev_q1[j]) for j in range(K)]
     a_ms = [ev_q1[j].elapsed_time(ev_a1[j]) for j in range(K)]
     # algorithmic bytes of the search kernel: 4(d+1) U + 4 E per tree-step
@@ -226,7 +223,7 @@ def run_ours(args, rank, world):
 
     # ---- e2e: the next steps through the public API with host (pinned) inputs/outputs
     f.query, f.attention = orig_query, orig_attn
-    e2e_val = run_e2e(eng, stream, n0, W + K, E2E_STEPS, dev)
+    e2e_val = run_e2e(eng, stream, n0, W + K, E2E_STEPS, dev, world)
 
     traffic = read_ncu_traffic()
     res = {
@@ -257,9 +254,20 @@ def run_ours(args, rank, world):
     return res
 
 
-def run_e2e(eng, stream, n0, start, K2, dev):
+def rank_max(x, dev, world):
+    """MAX of a per-rank scalar over ranks (NCCL all-reduce on the device)."""
+    import torch
+    if world == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_e2e(eng, stream, n0, start, K2, dev, world):
     """Same metric through Engine.decode_step with pinned host inputs (H2D)
-    and the step's outputs read back (D2H) inside the timed region."""
+    and the step's outputs read back (D2H) inside the timed region; whole-job
+    tokens over the slowest rank's wall time."""
     import torch
     qh = stream.queries[start:start + K2].cpu().pin_memory()
     kh = stream.keys[n0 + start:n0 + start + K2].cpu().pin_memory()
@@ -268,6 +276,8 @@ def run_e2e(eng, stream, n0, start, K2, dev):
     if eng.steps_done != start:
         return None
     torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
     t0 = time.perf_counter()
     for i in range(K2):
         tok = n0 + start + i
@@ -277,10 +287,10 @@ def run_e2e(eng, stream, n0, start, K2, dev):
         out, _ = eng.decode_step(tok, q, k, v, metrics=False)
         outh[i].copy_(out, non_blocking=True)
     torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
+    dt = rank_max(time.perf_counter() - t0, dev, world)
     h2d = (qh[0].numel() + kh[0].numel() + vh[0].numel()) * 4
     d2h = outh[0].numel() * 4
-    return {"value": K2 / dt, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+    return {"value": world * K2 / dt, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "steps": K2}
 
 
@@ -349,7 +359,7 @@ def run_reference(args):
     cores: one process per core, each owning one (layer, kv head) tree."""
     import multiprocessing as mp
     ncores = len(os.sched_getaffinity(0))
-    nproc = max(1, min(ncores, 8))
+    nproc = max(1, min(ncores, 16))
     ctx = mp.get_context("fork")
     with ctx.Pool(nproc) as pool:
         t0 = time.time()
@@ -383,7 +393,9 @@ def main():
         return
     if world > 1:
         import torch
-        torch.distributed.init_process_group("gloo")
+        dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+        torch.cuda.set_device(dev)
+        torch.distributed.init_process_group("nccl", device_id=dev)
     res = run_ours(args, rank, world)
     if rank == 0 and not args.no_cpu_baseline:
         cb = cpu_sample()

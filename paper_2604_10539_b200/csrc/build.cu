@@ -522,6 +522,36 @@ __global__ void build_page_totals_kernel(ForestView F, BuildArgs A, int max_node
   if (F.meta[t].next_page > F.page_cap) set_err(F.meta + t, ICB_ERR_CAP_PAGES);
 }
 
+// Level summary of a freshly built tree (TreeMeta.lvl_count / lvl_maxnode /
+// upper, read by the search's start level): one CTA per tree.
+__global__ void __launch_bounds__(256) build_summary_kernel(ForestView F, BuildArgs A) {
+  const int b = blockIdx.x, t = A.trees[b];
+  TreeMeta* m = F.meta + t;
+  __shared__ int cnt[ICB_LV_TRACK], mx[ICB_LV_TRACK], nup, ovf;
+  if (threadIdx.x < ICB_LV_TRACK) { cnt[threadIdx.x] = 0; mx[threadIdx.x] = 0; }
+  if (threadIdx.x == 0) { nup = 0; ovf = 0; }
+  __syncthreads();
+  int* up = F.upl(t);
+  for (int i = threadIdx.x; i < A.n_points; i += blockDim.x) {
+    const int tok = A.tokens[(size_t)b * A.n_points + i];
+    if (tok < 0 || tok >= F.tok_cap) continue;
+    const int lv = F.level[F.tk(t, tok)];
+    if (lv >= ICB_LV_TRACK) { ovf = 1; continue; }
+    atomicAdd(&cnt[lv], 1);
+    if (lv >= 2) {
+      const int pos = atomicAdd(&nup, 1);
+      if (pos < F.upper_cap) up[pos] = tok; else ovf = 1;
+    }
+  }
+  for (int x = threadIdx.x; x < min(m->n_nodes, F.node_cap); x += blockDim.x) {
+    const int lv = F.node_level[F.nd(t, x)];
+    if (lv < ICB_LV_TRACK) atomicMax(&mx[lv], F.node_size[F.nd(t, x)]);
+  }
+  __syncthreads();
+  if (threadIdx.x < ICB_LV_TRACK) { m->lvl_count[threadIdx.x] = cnt[threadIdx.x]; m->lvl_maxnode[threadIdx.x] = mx[threadIdx.x]; }
+  if (threadIdx.x == 0) { m->n_upper = min(nup, F.upper_cap); m->lv_ovf = ovf; }
+}
+
 }  // namespace icb
 
 // ---------------------------------------------------------------- host driver
@@ -643,6 +673,7 @@ int icb_build_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t n_poi
   }
   build_pages_kernel<<<dim3(max_nodes, n), 256, 0, st>>>(F, A, max_nodes, leaf_first, nullptr);
   build_page_totals_kernel<<<(n + 127) / 128, 128, 0, st>>>(F, A, max_nodes, leaf_first, leaf_pages);
+  build_summary_kernel<<<n, 256, 0, st>>>(F, A);
   ICB_CUDA(cudaGetLastError());
   return S.finish();
 }

@@ -119,6 +119,8 @@ int icb_forest_create(const icb_forest_config* cfg, icb_forest** out) {
   AL(F.page_tok, T * c.page_cap * c.page_size, 0xff);
   AL(F.dirs, T * F.dirs_cap * ICB_NPROJ * (c.dim + 1), 0);
   AL(F.prev_sel, T * (c.page_cap / 32 + 1), 0);
+  F.upper_cap = c.tok_cap / 4 + 64;   // ~r = 10% of points expected; overflow only disables the start shortcut
+  AL(F.upper, T * F.upper_cap, 0);
 #undef AL
   if (rc == ICB_OK) {
     char* pk = nullptr;

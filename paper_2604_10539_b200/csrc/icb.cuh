@@ -42,6 +42,7 @@
 #define ICB_MAX_SINK 8
 #define ICB_MAX_G 8
 #define ICB_ROOT_OWNER (-1)
+#define ICB_LV_TRACK 16      // levels with tracked point counts / max node sizes (search start level)
 
 // Sticky per-tree error bits (host maps them to the reference's exceptions).
 enum {
@@ -80,6 +81,14 @@ struct TreeMeta {
   unsigned long long query_count, distance_evals, scale_clamps;
   unsigned long long rows_read;      // lifted rows streamed by the search (union of heads)
   unsigned long long owner_rereads;  // rows re-read because a survivor heads its own child node
+  // Level summary for the search start (search.cuh start_level): points per
+  // exact top level, the largest node per level, and the list of points with
+  // top level >= 2 (unordered).  lv_ovf: a level >= ICB_LV_TRACK exists or the
+  // upper list overflowed -- the search then starts at the top node.
+  int lvl_count[ICB_LV_TRACK];
+  int lvl_maxnode[ICB_LV_TRACK];
+  int n_upper;
+  int lv_ovf;
 };
 
 struct ForestView {
@@ -110,6 +119,8 @@ struct ForestView {
   void* page_v;       // [T][page_cap][s][dim_v]
   double* dirs;       // [T][dirs_cap][8][dim+1]
   uint32_t* prev_sel; // [T][page_cap/32 + 1] residency: previous step's selection
+  int* upper;         // [T][upper_cap] points with top level >= 2
+  int upper_cap;
 
   __device__ __forceinline__ size_t tk(int t, int tok) const { return (size_t)t * tok_cap + tok; }
   __device__ __forceinline__ size_t nd(int t, int n) const { return (size_t)t * node_cap + n; }
@@ -121,6 +132,7 @@ struct ForestView {
     return own_list[(size_t)t * own_cap + own_base[tk(t, p)] + lv - 1];
   }
   __device__ __forceinline__ int* mem(int t) const { return members + (size_t)t * member_cap; }
+  __device__ __forceinline__ int* upl(int t) const { return upper + (size_t)t * upper_cap; }
   __device__ __forceinline__ int pwords() const { return page_cap / 32 + 1; }
 };
 
@@ -272,6 +284,20 @@ __device__ __forceinline__ void block_scan_multi(const int (&v)[V], int (&ex)[V]
 }
 
 __device__ __forceinline__ void set_err(TreeMeta* m, int bit) { atomicOr(&m->err, bit); }
+
+// Level-summary upkeep for inserts (one writer per tree).
+__device__ __forceinline__ void note_point_level(const ForestView& F, int t, int tok, int lv) {
+  TreeMeta* m = F.meta + t;
+  if (lv >= ICB_LV_TRACK) { m->lv_ovf = 1; return; }
+  m->lvl_count[lv] += 1;
+  if (lv >= 2) {
+    if (m->n_upper < F.upper_cap) F.upl(t)[m->n_upper++] = tok;
+    else m->lv_ovf = 1;
+  }
+}
+__device__ __forceinline__ void note_node_size(TreeMeta* m, int lv, int sz) {
+  if (lv < ICB_LV_TRACK && sz > m->lvl_maxnode[lv]) m->lvl_maxnode[lv] = sz;
+}
 
 // ---------------------------------------------------------------------------
 // mbarrier + TMA bulk copy (cp.async.bulk) helpers

@@ -53,6 +53,7 @@ __device__ int new_node(const ForestView& F, int t, int level, int parent, int o
   F.node_lastpage[x] = -1;
   F.node_dirs[x] = -1;
   F.mem(t)[off] = first_member;
+  note_node_size(m, level, 1);
   return id;
 }
 
@@ -73,6 +74,7 @@ __device__ void add_member(const ForestView& F, int t, int node, int tok) {
   }
   mem[off + sz] = tok;
   F.node_size[x] = sz + 1;
+  note_node_size(m, F.node_level[x], sz + 1);
   // the node's P-DCI ladders are a function of its member set: nothing to update
 }
 
@@ -160,6 +162,7 @@ __device__ int insert_one(SearchSmem& S, GroupSmem* GSA, const RingView& RG, con
     S.qt[0] = tl;
     if (over) m->scale_clamps += 1;
     F.level[F.tk(t, tok)] = (int8_t)s_level;
+    note_point_level(F, t, tok, s_level);
     F.own_base[F.tk(t, tok)] = m->own_top;
     if (m->own_top + s_level - 1 > F.own_cap) set_err(m, ICB_ERR_CAP_OWN);
     m->own_top += s_level - 1;

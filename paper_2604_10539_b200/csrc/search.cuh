@@ -787,11 +787,40 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
     q2[h][3] = pack_f2(qv[2 * h].w, qv[2 * h + 1].w);
   }
 
+  // (0) start level.  Every point of top level >= lv is a member of exactly
+  //     one node at level lv, so while C(lv) = #points of top >= lv is <= beam
+  //     (and no node is P-DCI-truncated) every candidate survives and the next
+  //     level's candidates are again all points of top >= lv - 1.  The search
+  //     therefore starts at the lowest such level with the candidate set {top
+  //     >= start} read from the tree's upper-point list: same survivors, same
+  //     pool (the skipped levels' candidates are a subset of the start
+  //     level's), same distance_evals (the skipped C(lv) are counted).
+  if (tid == 0) {
+    const TreeMeta& mt = F.meta[t];
+    int start = L;
+    if (!mt.lv_ovf && L < ICB_LV_TRACK) {
+      long long C = 0;
+      for (int lv = L; lv >= max(floor, 2); --lv) {
+        const int mxn = mt.lvl_maxnode[lv];
+        if (mxn > ICB_EXHAUSTIVE && (long long)mxn > P.visit_cap) break;
+        start = lv;
+        C += mt.lvl_count[lv];
+        if (C > P.beam) break;
+      }
+      unsigned long long Cs = 0, skipped = 0;
+      for (int lv = L; lv > start; --lv) { Cs += mt.lvl_count[lv]; skipped += Cs; }
+      if (skipped) atomicAdd(&F.meta[t].distance_evals, skipped * (unsigned long long)G);
+    }
+    S.misc[7] = start;
+  }
+  __syncthreads();
+  const int start = S.misc[7];
+
   long long tmark_ = clock64();
-  for (int lv = L; lv >= floor; --lv) {
+  for (int lv = start; lv >= floor; --lv) {
     ICB_MARK(0);
     // (1) union of the nodes requested by the heads' survivors
-    if (lv == L) {
+    if (lv == start) {
       if (tid == 0) { SS.ulist[0] = F.meta[t].top_node; SS.umask[0] = (int)allmask; S.U = 1; }
       __syncthreads();
     } else {
@@ -827,7 +856,40 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
     if (tid < GP) { GSA[tid].lo = 0xffffffffu; GSA[tid].hi = 0u; }
     __syncthreads();
     constexpr int NPT = 8;   // consecutive union nodes per thread per pass (loads in parallel)
-    for (int base = 0; base < U; base += NT * NPT) {
+    if (lv == start && start < L) {
+      // rows of the start level: the upper points of top >= start, as one
+      // virtual union entry 0 requested by every head
+      const int nu = F.meta[t].n_upper;
+      const int* up = F.upl(t);
+      for (int base = 0; base < nu; base += NT * NPT) {
+        int tk[NPT], v[1] = {0}, ex[1], tot[1];
+#pragma unroll
+        for (int u = 0; u < NPT; ++u) {
+          const int i = base + tid * NPT + u;
+          tk[u] = -1;
+          if (i < nu) {
+            const int tok = up[i];
+            if (start == 2 || F.level[F.tk(t, tok)] >= start) tk[u] = tok;
+          }
+          v[0] += tk[u] >= 0 ? 1 : 0;
+        }
+        block_scan_multi<NT, 1>(v, ex, tot, S.wsum2);
+        int run = S.scan_carry[GP] + ex[0];
+#pragma unroll
+        for (int u = 0; u < NPT; ++u)
+          if (tk[u] >= 0) {
+            SS.rlist[2 * (size_t)run] = tk[u];
+            SS.rlist[2 * (size_t)run + 1] = 0;
+            ++run;
+          }
+        __syncthreads();
+        if (tid == 0) S.scan_carry[GP] += tot[0];
+        __syncthreads();
+      }
+      if (tid < G) { S.scan_carry[tid] = S.scan_carry[GP]; SS.uoff[(size_t)tid * F.node_cap] = 0; }
+      if (tid == 0) SS.upre[0] = 0;
+    }
+    for (int base = 0; base < U && !(lv == start && start < L); base += NT * NPT) {
       const int i0 = base + tid * NPT;
       int sz[NPT], off[NPT];
       unsigned mk[NPT];
@@ -1075,9 +1137,9 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
       for (int g = 0; g < G; ++g) ev += S.M[g];
       atomicAdd(&F.meta[t].distance_evals, ev);
       atomicAdd(&F.meta[t].rows_read, (unsigned long long)S.misc[5]);
-      if (lv < L) atomicAdd(&F.meta[t].owner_rereads, (unsigned long long)U);
+      if (lv < start) atomicAdd(&F.meta[t].owner_rereads, (unsigned long long)U);
     }
-    if (lv < L)
+    if (lv < start)
       for (int i = tid; i < U; i += NT) SS.nmask[SS.ulist[i]] = 0u;
     __syncthreads();
     ICB_MARK(5);
@@ -1091,7 +1153,7 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
       unsigned long long* pg = SS.pool + (size_t)g * SS.ccap;
       unsigned* sg = SS.seen + (size_t)g * (F.tok_cap / 32 + 1);
       const int M = S.M[g];
-      if (lv == L && gtid == 0) { GS.plo = 0xffffffffu; GS.phi = 0u; }
+      if (lv == start && gtid == 0) { GS.plo = 0xffffffffu; GS.phi = 0u; }
       gsync(gbar, NTG);
       if (lv > floor) {
         unsigned long long thr = group_threshold<NTG>(GS, gtid, gbar, cg, M, P.beam, GS.lo, GS.hi);

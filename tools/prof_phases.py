@@ -27,7 +27,7 @@ lib.icb_search_profile(buf.ctypes.data_as(ctypes.c_void_p), 1)
 for i in range(4, 12):
     eng.decode_step(ctx + i, st.queries[i], st.keys[ctx + i], st.values[ctx + i], metrics=False)
 lib.icb_search_profile(buf.ctypes.data_as(ctypes.c_void_p), 1)
-names = ["union", "scans", "rowlist", "stream", "pdci+ctr", "select", "tail", "finalize"]
+names = ["loop", "union", "scan+rowlist", "-", "stream", "pdci+ctr", "select", "finalize"]
 tot = buf.sum()
 per_cta_us = buf / (8 * eng.T) / 1.9e3
 for n, v, u in zip(names, buf, per_cta_us):
