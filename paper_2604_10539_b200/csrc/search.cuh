@@ -111,6 +111,7 @@ struct SearchSmem {
   int scan_carry[ICB_MAX_G + 1];
   int wsum2[(ICB_MAX_G + 1) * (kSearchThreads / 32)];
   int misc[8];
+  int nopool;   // the final top-k is the floor level's top-k (no cross-level pool)
   unsigned long long* sortbuf;   // fallback sort buffer (aliases the idle row ring, >= kSortMax keys)
 };
 
@@ -798,6 +799,7 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
   if (tid == 0) {
     const TreeMeta& mt = F.meta[t];
     int start = L;
+    S.nopool = 0;
     if (!mt.lv_ovf && L < ICB_LV_TRACK) {
       long long C = 0;
       for (int lv = L; lv >= max(floor, 2); --lv) {
@@ -807,11 +809,25 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
         C += mt.lvl_count[lv];
         if (C > P.beam) break;
       }
+      // No pool needed when every pooled survivor that could rank in the final
+      // top-k is also a floor candidate: a survivor x of level lv is a member
+      // of its own node at lv - 1, which x itself requests, so x is evaluated
+      // there unless that node is P-DCI-truncated; if x then fails to survive,
+      // beam >= k better keys are pooled and x cannot rank.  Hence with
+      // beam >= k and no truncated node at any level, pool top-k = floor
+      // top-k.  (Targeted searches pool only the floor anyway.)
+      int np = P.beam >= P.k;
+      for (int lv = 1; lv <= L; ++lv) {
+        const int mxn = mt.lvl_maxnode[lv];
+        if (mxn > ICB_EXHAUSTIVE && (long long)mxn > P.visit_cap) np = 0;
+      }
+      S.nopool = np && P.k <= kBuf;
       unsigned long long Cs = 0, skipped = 0;
       for (int lv = L; lv > start; --lv) { Cs += mt.lvl_count[lv]; skipped += Cs; }
       if (skipped) atomicAdd(&F.meta[t].distance_evals, skipped * (unsigned long long)G);
     }
     S.misc[7] = start;
+    if (!collect_all) S.nopool = P.k <= kBuf;
   }
   __syncthreads();
   const int start = S.misc[7];
@@ -831,15 +847,31 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
       pre[0] = 0;
 #pragma unroll
       for (int g = 0; g < GP; ++g) pre[g + 1] = pre[g] + (g < G ? S.nsurv[g] : 0);
-      for (int fl = tid; fl < pre[GP]; fl += NT) {
-        int g = 0;
+      // 8 independent (survivor -> own base -> own node) chains per thread
+      constexpr int UU = 8;
+      const int* ownl = F.own_list + (size_t)t * F.own_cap;
+      for (int f0 = tid; f0 < pre[GP]; f0 += NT * UU) {
+        int gg[UU], x[UU];
 #pragma unroll
-        for (int h = 1; h < GP; ++h) g += fl >= pre[h] ? 1 : 0;
-        const int s = SS.surv[(size_t)g * SS.ccap + fl - pre[g]];
-        const int node = F.own(t, s, lv);
-        ICB_CHECK(node >= 0 && node < F.node_cap, "own(%d, %d) = %d", s, lv, node);
-        unsigned old = atomicOr(SS.nmask + node, 1u << g);
-        if (old == 0) SS.ulist[atomicAdd(&S.U, 1)] = node;
+        for (int u = 0; u < UU; ++u) {
+          const int fl = f0 + u * NT;
+          int g = 0;
+#pragma unroll
+          for (int h = 1; h < GP; ++h) g += fl >= pre[h] ? 1 : 0;
+          gg[u] = fl < pre[GP] ? g : -1;
+          x[u] = gg[u] >= 0 ? SS.surv[(size_t)g * SS.ccap + fl - pre[g]] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < UU; ++u) x[u] = gg[u] >= 0 ? F.own_base[F.tk(t, x[u])] : 0;
+#pragma unroll
+        for (int u = 0; u < UU; ++u) x[u] = gg[u] >= 0 ? ownl[x[u] + lv - 1] : 0;
+#pragma unroll
+        for (int u = 0; u < UU; ++u) {
+          if (gg[u] < 0) continue;
+          ICB_CHECK(x[u] >= 0 && x[u] < F.node_cap, "own(.., %d) = %d", lv, x[u]);
+          const unsigned old = atomicOr(SS.nmask + x[u], 1u << gg[u]);
+          if (old == 0) SS.ulist[atomicAdd(&S.U, 1)] = x[u];
+        }
       }
       __syncthreads();
       for (int i = tid; i < S.U; i += NT) SS.umask[i] = (int)SS.nmask[SS.ulist[i]];
@@ -856,6 +888,8 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
     if (tid < GP) { GSA[tid].lo = 0xffffffffu; GSA[tid].hi = 0u; }
     __syncthreads();
     constexpr int NPT = 8;   // consecutive union nodes per thread per pass (loads in parallel)
+    int* stage_up = reinterpret_cast<int*>(RG.ring);   // [NT * NPT] (the ring is idle outside the stream)
+    int* stage_off = stage_up + NT * NPT;
     if (lv == start && start < L) {
       // rows of the start level: the upper points of top >= start, as one
       // virtual union entry 0 requested by every head
@@ -929,22 +963,43 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
           run[g] += ((mk[u] >> g) & 1) ? s : 0;
         }
         SS.upre[i] = run[GP];
-        SS.umoff[i] = sz[u] > 0 ? off[u] : -1;   // member offset for the copy pass (-1: P-DCI node)
+        stage_up[i - base] = run[GP];     // row prefix / member offset of the pass's nodes (idle ring smem)
+        stage_off[i - base] = off[u];
         run[GP] += s;
       }
       __syncthreads();
-      // member copies, one warp per node (coalesced over the contiguous members)
-      const int cend = min(U, base + NT * NPT);
-      for (int i = base + warp; i < cend; i += NT / 32) {
-        const int mo = SS.umoff[i];
-        if (mo < 0) continue;
-        const int up = SS.upre[i];
-        const int s = (i + 1 < cend ? SS.upre[i + 1] : S.scan_carry[GP] + tot[GP]) - up;
-        for (int j = lane; j < s; j += 32) {
-          SS.rlist[2 * (size_t)(up + j)] = mem[mo + j];
-          SS.rlist[2 * (size_t)(up + j) + 1] = i;
+      // the pass's rows in parallel: row r belongs to the last node whose
+      // prefix is <= r (binary search over the staged prefixes; nodes without
+      // rows share their successor's prefix and are never chosen)
+      {
+        const int r0 = S.scan_carry[GP], r1 = r0 + tot[GP];
+        const int nn = min(U - base, NT * NPT);
+        for (int rb = r0 + tid; rb < r1; rb += NT * 8) {
+          int src[8], ix[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int r = rb + u * NT;
+            int lo = 0, hi = nn;   // first index with prefix > r, minus one
+            while (lo < hi) {
+              const int mid = (lo + hi) >> 1;
+              if (stage_up[mid] <= r) lo = mid + 1; else hi = mid;
+            }
+            ix[u] = lo - 1;
+            src[u] = r < r1 ? stage_off[ix[u]] + (r - stage_up[ix[u]]) : -1;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) src[u] = src[u] >= 0 ? mem[src[u]] : -1;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int r = rb + u * NT;
+            if (r < r1) {
+              SS.rlist[2 * (size_t)r] = src[u];
+              SS.rlist[2 * (size_t)r + 1] = base + ix[u];
+            }
+          }
         }
       }
+      __syncthreads();
       if (tid == 0)
 #pragma unroll
         for (int g = 0; g <= GP; ++g) S.scan_carry[g] += tot[g];
@@ -1155,14 +1210,22 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
       const int M = S.M[g];
       if (lv == start && gtid == 0) { GS.plo = 0xffffffffu; GS.phi = 0u; }
       gsync(gbar, NTG);
+      const bool nopool = S.nopool;
       if (lv > floor) {
         unsigned long long thr = group_threshold<NTG>(GS, gtid, gbar, cg, M, P.beam, GS.lo, GS.hi);
         const int2 r = group_emit<NTG>(GS, gtid, gbar, cg, M, thr, SS.surv + (size_t)g * SS.ccap, 0,
-                                       collect_all ? pg : nullptr, S.npool[g], sg, &GS.plo, &GS.phi);
+                                       collect_all && !nopool ? pg : nullptr, S.npool[g], sg, &GS.plo, &GS.phi);
         if (gtid == 0) {
           S.nsurv[g] = r.x;
           S.npool[g] += r.y;
         }
+      } else if (nopool) {
+        // the floor's top-k is the answer: straight into the group's buffer, sorted
+        unsigned long long thr = group_threshold<NTG>(GS, gtid, gbar, cg, M, P.k, GS.lo, GS.hi);
+        const int n = group_emit<NTG>(GS, gtid, gbar, cg, M, thr, nullptr, 0, GS.buf, 0, nullptr, nullptr,
+                                      nullptr).y;
+        group_sort<NTG>(GS, gtid, gbar, n);
+        if (gtid == 0) S.npool[g] = n;
       } else {
         unsigned long long thr = group_threshold<NTG>(GS, gtid, gbar, cg, M, P.k, GS.lo, GS.hi);
         const int2 r = group_emit<NTG>(GS, gtid, gbar, cg, M, thr, nullptr, 0, pg, S.npool[g], sg, &GS.plo,
@@ -1184,6 +1247,10 @@ __device__ int finalize_groups(SearchSmem& S, GroupSmem* GSA, const ForestView& 
   constexpr int NTG = NT / GP;
   const int tid = threadIdx.x, grp = tid / NTG, gtid = tid % NTG, gbar = 1 + grp;
   int n = 0;
+  if (S.nopool) {   // tree_search left the sorted floor top-k in GS.buf
+    __syncthreads();
+    return grp < G ? S.npool[grp] : 0;
+  }
   if (grp < G) {
     GroupSmem& GS = GSA[grp];
     unsigned long long* pg = SS.pool + (size_t)grp * SS.ccap;
