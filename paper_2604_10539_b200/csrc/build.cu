@@ -399,6 +399,7 @@ __global__ void build_nodes_kernel(ForestView F, BuildArgs A, const unsigned lon
   int T = top[(size_t)b * A.n_points + pos];
   if (lv < F.meta[t].levels && T > lv) {   // this member owns the node
     F.node_owner[F.nd(t, node)] = tok;
+    F.node_opos[F.nd(t, node)] = local;   // absolute here; made node-relative by build_summary_kernel
     F.own_list[(size_t)t * F.own_cap + own_base_pos[(size_t)b * A.n_points + pos] + lv - 1] = node;
   }
   // node size: count members
@@ -545,6 +546,8 @@ __global__ void __launch_bounds__(256) build_summary_kernel(ForestView F, BuildA
   }
   for (int x = threadIdx.x; x < min(m->n_nodes, F.node_cap); x += blockDim.x) {
     const int lv = F.node_level[F.nd(t, x)];
+    const size_t nx = F.nd(t, x);
+    F.node_opos[nx] = F.node_owner[nx] >= 0 ? F.node_opos[nx] - F.node_off[nx] : -1;
     if (lv < ICB_LV_TRACK) atomicMax(&mx[lv], F.node_size[F.nd(t, x)]);
   }
   __syncthreads();

@@ -113,6 +113,7 @@ int icb_forest_create(const icb_forest_config* cfg, icb_forest** out) {
   AL(F.node_capm, T * c.node_cap, 0);
   AL(F.node_lastpage, T * c.node_cap, 0xff);
   AL(F.node_dirs, T * c.node_cap, 0xff);
+  AL(F.node_opos, T * c.node_cap, 0xff);
   AL(F.members, T * c.member_cap, 0);
   AL(F.page_fill, T * c.page_cap, 0);
   AL(F.page_role, T * c.page_cap, 0);

@@ -111,6 +111,7 @@ struct ForestView {
   int* node_capm;     // member capacity of the node's block
   int* node_lastpage; // leaves: last page id (-1 none)
   int* node_dirs;     // P-DCI direction cache slot (-1 none)
+  int* node_opos;     // position of the owner within the node's members (-1: root node)
   int* members;       // [T][member_cap] token ids
   int* page_fill;     // [T][page_cap]
   int8_t* page_role;  // [T][page_cap] 0 none, 1 sink, 2 window, 3 indexed

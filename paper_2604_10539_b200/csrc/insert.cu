@@ -52,6 +52,7 @@ __device__ int new_node(const ForestView& F, int t, int level, int parent, int o
   F.node_capm[x] = cap;
   F.node_lastpage[x] = -1;
   F.node_dirs[x] = -1;
+  F.node_opos[x] = (owner >= 0 && owner == first_member) ? 0 : -1;
   F.mem(t)[off] = first_member;
   note_node_size(m, level, 1);
   return id;
@@ -193,6 +194,7 @@ __device__ int insert_one(SearchSmem& S, GroupSmem* GSA, const RingView& RG, con
       F.node_parent[x] = prev;
       set_own(F, t, tok, L, old_top);
       add_member(F, t, old_top, tok);
+      F.node_opos[x] = F.node_size[x] - 1;   // the new owner was appended
       m->levels = level;
       s_container = old_top;   // membership at level L
       s_chain_from = L - 1;

@@ -25,7 +25,7 @@ constexpr int kSortMax = 4096;   // largest k served by the in-smem final sort
 struct SearchScratch {
   unsigned long long* cand;   // [G][ccap]
   unsigned long long* pool;   // [G][ccap]
-  int* surv;                  // [G][ccap]
+  unsigned long long* surv;   // [G][ccap] survivor keys
   int* ulist;                 // [node_cap]
   int* umask;                 // [node_cap]
   int* uoff;                  // [G][node_cap]
@@ -54,7 +54,7 @@ __host__ __device__ inline SlotLayout slot_layout(int G, int tok_cap, int node_c
   size_t cc = (size_t)tok_cap;
   L.cand = o; o = al256(o + (size_t)G * cc * 8);
   L.pool = o; o = al256(o + (size_t)G * cc * 8);
-  L.surv = o; o = al256(o + (size_t)G * cc * 4);
+  L.surv = o; o = al256(o + (size_t)G * cc * 8);
   L.ulist = o; o = al256(o + (size_t)node_cap * 4);
   L.umask = o; o = al256(o + (size_t)node_cap * 4);
   L.uoff = o; o = al256(o + (size_t)G * node_cap * 4);
@@ -77,7 +77,7 @@ __device__ inline SearchScratch slot_scratch(char* base, const SlotLayout& L, in
   SearchScratch S;
   S.cand = (unsigned long long*)(base + L.cand);
   S.pool = (unsigned long long*)(base + L.pool);
-  S.surv = (int*)(base + L.surv);
+  S.surv = (unsigned long long*)(base + L.surv);
   S.ulist = (int*)(base + L.ulist);
   S.umask = (int*)(base + L.umask);
   S.uoff = (int*)(base + L.uoff);
@@ -112,6 +112,7 @@ struct SearchSmem {
   int wsum2[(ICB_MAX_G + 1) * (kSearchThreads / 32)];
   int misc[8];
   int nopool;   // the final top-k is the floor level's top-k (no cross-level pool)
+  int oskip;    // owners are not re-read: their keys are the survivors' (no P-DCI node can occur)
   unsigned long long* sortbuf;   // fallback sort buffer (aliases the idle row ring, >= kSortMax keys)
 };
 
@@ -332,14 +333,15 @@ __device__ __forceinline__ int group_scan(GroupSmem& GS, int gtid, int bar, int 
   return before;
 }
 
-// One pass over the list emitting every key <= thr: their ids to out_ids
+// One pass over the list emitting every key <= thr: the keys to out_ids
 // (from out_ids_base, no dedup) and/or the keys to out_keys (from
 // out_keys_base, skipping ids already marked in `seen` and marking new ones;
 // the emitted keys' d2 range is folded into plo/phi).  8 independent loads in
 // flight per thread.  Returns (ids written, keys written).
 template <int NTG>
 __device__ int2 group_emit(GroupSmem& GS, int gtid, int bar, const unsigned long long* keys, int M,
-                           unsigned long long thr, int* out_ids, int out_ids_base, unsigned long long* out_keys,
+                           unsigned long long thr, unsigned long long* out_ids, int out_ids_base,
+                           unsigned long long* out_keys,
                            int out_keys_base, unsigned* seen, unsigned* plo, unsigned* phi) {
   constexpr int U = 8;
   const int lane = gtid & 31;
@@ -363,7 +365,7 @@ __device__ int2 group_emit(GroupSmem& GS, int gtid, int bar, const unsigned long
         int base = 0;
         if (lane == 0 && bal) base = atomicAdd(&GS.misc[0], __popc(bal));
         base = __shfl_sync(0xffffffffu, base, 0);
-        if (sel) out_ids[out_ids_base + base + __popc(bal & ((1u << lane) - 1))] = key_id(k);
+        if (sel) out_ids[out_ids_base + base + __popc(bal & ((1u << lane) - 1))] = k;
       }
       if (out_keys) {
         bool take = sel;
@@ -800,6 +802,7 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
     const TreeMeta& mt = F.meta[t];
     int start = L;
     S.nopool = 0;
+    S.oskip = 0;
     if (!mt.lv_ovf && L < ICB_LV_TRACK) {
       long long C = 0;
       for (int lv = L; lv >= max(floor, 2); --lv) {
@@ -816,12 +819,13 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
       // beam >= k better keys are pooled and x cannot rank.  Hence with
       // beam >= k and no truncated node at any level, pool top-k = floor
       // top-k.  (Targeted searches pool only the floor anyway.)
-      int np = P.beam >= P.k;
+      int notrunc = 1;
       for (int lv = 1; lv <= L; ++lv) {
         const int mxn = mt.lvl_maxnode[lv];
-        if (mxn > ICB_EXHAUSTIVE && (long long)mxn > P.visit_cap) np = 0;
+        if (mxn > ICB_EXHAUSTIVE && (long long)mxn > P.visit_cap) notrunc = 0;
       }
-      S.nopool = np && P.k <= kBuf;
+      S.nopool = notrunc && P.beam >= P.k && P.k <= kBuf;
+      S.oskip = notrunc;
       unsigned long long Cs = 0, skipped = 0;
       for (int lv = L; lv > start; --lv) { Cs += mt.lvl_count[lv]; skipped += Cs; }
       if (skipped) atomicAdd(&F.meta[t].distance_evals, skipped * (unsigned long long)G);
@@ -831,6 +835,7 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
   }
   __syncthreads();
   const int start = S.misc[7];
+  const bool oskip = S.oskip;
 
   long long tmark_ = clock64();
   for (int lv = start; lv >= floor; --lv) {
@@ -841,6 +846,7 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
       __syncthreads();
     } else {
       if (tid == 0) S.U = 0;
+      if (tid < GP) { GSA[tid].lo = 0xffffffffu; GSA[tid].hi = 0u; }
       __syncthreads();
       // every (head, survivor) pair in parallel: independent own() lookups
       int pre[GP + 1];
@@ -850,7 +856,8 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
       // 8 independent (survivor -> own base -> own node) chains per thread
       constexpr int UU = 8;
       const int* ownl = F.own_list + (size_t)t * F.own_cap;
-      for (int f0 = tid; f0 < pre[GP]; f0 += NT * UU) {
+      for (int fb = 0; fb < pre[GP]; fb += NT * UU) {   // block-uniform trip count (ballots below)
+        const int f0 = fb + tid;
         int gg[UU], x[UU];
 #pragma unroll
         for (int u = 0; u < UU; ++u) {
@@ -859,7 +866,18 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
 #pragma unroll
           for (int h = 1; h < GP; ++h) g += fl >= pre[h] ? 1 : 0;
           gg[u] = fl < pre[GP] ? g : -1;
-          x[u] = gg[u] >= 0 ? SS.surv[(size_t)g * SS.ccap + fl - pre[g]] : 0;
+          x[u] = 0;
+          if (gg[u] >= 0) {
+            const unsigned long long sk = SS.surv[(size_t)g * SS.ccap + fl - pre[g]];
+            x[u] = key_id(sk);
+            if (oskip) {
+              // the survivor owns exactly the node it requests here: its key for
+              // head g opens g's candidate list (one entry per requested node)
+              SS.cand[(size_t)g * SS.ccap + fl - pre[g]] = sk;
+              atomicMin(&GSA[g].lo, (unsigned)(sk >> 32));
+              atomicMax(&GSA[g].hi, (unsigned)(sk >> 32));
+            }
+          }
         }
 #pragma unroll
         for (int u = 0; u < UU; ++u) x[u] = gg[u] >= 0 ? F.own_base[F.tk(t, x[u])] : 0;
@@ -867,10 +885,14 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
         for (int u = 0; u < UU; ++u) x[u] = gg[u] >= 0 ? ownl[x[u] + lv - 1] : 0;
 #pragma unroll
         for (int u = 0; u < UU; ++u) {
-          if (gg[u] < 0) continue;
-          ICB_CHECK(x[u] >= 0 && x[u] < F.node_cap, "own(.., %d) = %d", lv, x[u]);
-          const unsigned old = atomicOr(SS.nmask + x[u], 1u << gg[u]);
-          if (old == 0) SS.ulist[atomicAdd(&S.U, 1)] = x[u];
+          ICB_CHECK(gg[u] < 0 || (x[u] >= 0 && x[u] < F.node_cap), "own(.., %d) = %d", lv, x[u]);
+          const bool fresh = gg[u] >= 0 && atomicOr(SS.nmask + x[u], 1u << gg[u]) == 0u;
+          // one smem atomic per warp for the new nodes' list slots
+          const unsigned bal = __ballot_sync(0xffffffffu, fresh);
+          int at = 0;
+          if (lane == 0 && bal) at = atomicAdd(&S.U, __popc(bal));
+          at = __shfl_sync(0xffffffffu, at, 0);
+          if (fresh) SS.ulist[at + __popc(bal & ((1u << lane) - 1))] = x[u];
         }
       }
       __syncthreads();
@@ -883,13 +905,15 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
     //     union (normal nodes only)
     //     (all heads + the union in one multi-value block scan) and (3a) the
     //     flattened row list (token, union index) written by the node's thread
-    if (tid <= GP) S.scan_carry[tid] = 0;
+    const bool skip_owner = oskip && lv < start;   // rows exclude owners; survivors prefix each head's list
+    if (tid <= GP) S.scan_carry[tid] = (skip_owner && tid < G) ? S.nsurv[tid] : 0;
     if (tid == 0) S.nbig = 0;
-    if (tid < GP) { GSA[tid].lo = 0xffffffffu; GSA[tid].hi = 0u; }
+    if (lv == start && tid < GP) { GSA[tid].lo = 0xffffffffu; GSA[tid].hi = 0u; }
     __syncthreads();
     constexpr int NPT = 8;   // consecutive union nodes per thread per pass (loads in parallel)
     int* stage_up = reinterpret_cast<int*>(RG.ring);   // [NT * NPT] (the ring is idle outside the stream)
     int* stage_off = stage_up + NT * NPT;
+    int* stage_opos = stage_off + NT * NPT;
     if (lv == start && start < L) {
       // rows of the start level: the upper points of top >= start, as one
       // virtual union entry 0 requested by every head
@@ -925,15 +949,16 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
     }
     for (int base = 0; base < U && !(lv == start && start < L); base += NT * NPT) {
       const int i0 = base + tid * NPT;
-      int sz[NPT], off[NPT];
+      int sz[NPT], off[NPT], op[NPT];
       unsigned mk[NPT];
 #pragma unroll
       for (int u = 0; u < NPT; ++u) {
-        sz[u] = 0; off[u] = 0; mk[u] = 0u;
+        sz[u] = 0; off[u] = 0; mk[u] = 0u; op[u] = -1;
         if (i0 + u < U) {
           const size_t x = F.nd(t, SS.ulist[i0 + u]);
           sz[u] = F.node_size[x];
           off[u] = F.node_off[x];
+          if (skip_owner) op[u] = F.node_opos[x];
           mk[u] = (unsigned)SS.umask[i0 + u];
         }
       }
@@ -944,6 +969,10 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
       for (int u = 0; u < NPT; ++u) {
         const bool big = sz[u] > ICB_EXHAUSTIVE && (long long)sz[u] > P.visit_cap;
         if (big) { atomicAdd(&S.nbig, 1); sz[u] = -sz[u]; continue; }   // negative marks P-DCI nodes
+        if (skip_owner && i0 + u < U) {   // the owner's row is not streamed (rows = members - owner)
+          ICB_CHECK(op[u] >= 0 && op[u] < sz[u], "owner position %d size %d", op[u], sz[u]);
+          sz[u] -= 1;
+        }
 #pragma unroll
         for (int g = 0; g < GP; ++g) v[g] += ((mk[u] >> g) & 1) ? sz[u] : 0;
         v[GP] += sz[u];
@@ -965,6 +994,7 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
         SS.upre[i] = run[GP];
         stage_up[i - base] = run[GP];     // row prefix / member offset of the pass's nodes (idle ring smem)
         stage_off[i - base] = off[u];
+        stage_opos[i - base] = skip_owner ? op[u] : 0x7fffffff;
         run[GP] += s;
       }
       __syncthreads();
@@ -985,7 +1015,12 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
               if (stage_up[mid] <= r) lo = mid + 1; else hi = mid;
             }
             ix[u] = lo - 1;
-            src[u] = r < r1 ? stage_off[ix[u]] + (r - stage_up[ix[u]]) : -1;
+            if (r < r1) {
+              const int j = r - stage_up[ix[u]];   // member index with the owner skipped
+              src[u] = stage_off[ix[u]] + j + (j >= stage_opos[ix[u]] ? 1 : 0);
+            } else {
+              src[u] = -1;
+            }
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) src[u] = src[u] >= 0 ? mem[src[u]] : -1;
@@ -1038,11 +1073,14 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
       struct RowTok {
         int tok, ix;
       };
+      // raw gathered values only: every use is deferred to the batch's own
+      // iteration, two batches later, so the loads stay in flight meanwhile
       struct RowMeta {
         int tok;
         float tail;
         int mask;
-        int pos[GP];
+        int upre;
+        int uo[GP];
       };
       auto load_a = [&](int kb) {
         RowTok a{0, -1};
@@ -1058,16 +1096,17 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
         m.tok = a.tok;
         m.tail = 0.f;
         m.mask = 0;
+        m.upre = 0;
 #pragma unroll
-        for (int g = 0; g < GP; ++g) m.pos[g] = 0;
+        for (int g = 0; g < GP; ++g) m.uo[g] = 0;
         if (a.ix >= 0) {
-          const int r = 8 * (warp + kb * NW) + lane;
           m.tail = F.tail[F.tk(t, a.tok)];
           m.mask = SS.umask[a.ix];
-          const int rel = r - SS.upre[a.ix];
+          m.upre = SS.upre[a.ix];
 #pragma unroll
-          for (int g = 0; g < GP; ++g) m.pos[g] = g < G ? SS.uoff[(size_t)g * F.node_cap + a.ix] + rel : 0;
+          for (int g = 0; g < GP; ++g) m.uo[g] = g < G ? SS.uoff[(size_t)g * F.node_cap + a.ix] : 0;
         }
+        (void)kb;
         return m;
       };
       // LDGSTS: the warp copies each 512-byte row with one instruction (16 B
@@ -1133,12 +1172,14 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
           const int src = u < 8 ? u : 0;
           const int tok = __shfl_sync(0xffffffffu, m0.tok, src);
           const int msk = __shfl_sync(0xffffffffu, m0.mask, src);
+          const int upr = __shfl_sync(0xffffffffu, m0.upre, src);
           int pos = 0;
 #pragma unroll
           for (int g = 0; g < GP; ++g) {
-            const int pg = __shfl_sync(0xffffffffu, m0.pos[g], src);
+            const int pg = __shfl_sync(0xffffffffu, m0.uo[g], src);
             if (g == myh) pos = pg;
           }
+          pos += base + u - upr;   // row index within its node
           if (u < nrow && myh < G && ((msk >> myh) & 1)) {
             ICB_CHECK(pos >= 0 && pos < S.M[myh], "cand pos %d M %d", pos, S.M[myh]);
             SS.cand[(size_t)myh * SS.ccap + pos] = make_key(keep[sl], tok);
@@ -1192,7 +1233,7 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
       for (int g = 0; g < G; ++g) ev += S.M[g];
       atomicAdd(&F.meta[t].distance_evals, ev);
       atomicAdd(&F.meta[t].rows_read, (unsigned long long)S.misc[5]);
-      if (lv < start) atomicAdd(&F.meta[t].owner_rereads, (unsigned long long)U);
+      if (lv < start && !oskip) atomicAdd(&F.meta[t].owner_rereads, (unsigned long long)U);
     }
     if (lv < start)
       for (int i = tid; i < U; i += NT) SS.nmask[SS.ulist[i]] = 0u;
