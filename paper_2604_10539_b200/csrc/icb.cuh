@@ -156,6 +156,30 @@ __device__ __forceinline__ float lane_sq4(float4 p, float4 q) {
 __device__ __forceinline__ unsigned long long pack_f2(float lo, float hi) {
   return ((unsigned long long)__float_as_uint(hi) << 32) | __float_as_uint(lo);
 }
+__device__ __forceinline__ unsigned long long lane_sq4_x2_packed(float4 p, const unsigned long long (&q2)[4]) {
+  unsigned long long d[4], s;
+  const float pv[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const unsigned long long pp = pack_f2(pv[i], pv[i]);
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d[i]) : "l"(pp), "l"(q2[i]));
+  }
+  asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(s) : "l"(d[0]));
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(s) : "l"(d[1]), "l"(s));
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(s) : "l"(d[2]), "l"(s));
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(s) : "l"(d[3]), "l"(s));
+  return s;
+}
+__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsigned long long b) {
+  unsigned long long c;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(c) : "l"(a), "l"(b));
+  return c;
+}
+__device__ __forceinline__ unsigned long long shfl_xor_u64(unsigned long long v, int o) {
+  const unsigned lo = __shfl_xor_sync(0xffffffffu, (unsigned)v, o);
+  const unsigned hi = __shfl_xor_sync(0xffffffffu, (unsigned)(v >> 32), o);
+  return ((unsigned long long)hi << 32) | lo;
+}
 __device__ __forceinline__ float2 lane_sq4_x2(float4 p, const unsigned long long (&q2)[4]) {
   unsigned long long d[4], s;
   const float pv[4] = {p.x, p.y, p.z, p.w};

@@ -1061,7 +1061,7 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
       constexpr int LPG = 32 / GP;              // lanes holding one head's sum
       constexpr int SLOTS = (8 + LPG - 1) / LPG;
       const int myh = lane / LPG;
-      const float qt_my = S.qt[myh];
+      const float qt_my = S.qt[GP == 4 ? (lane & 3) : myh];
       const unsigned qb = RG.qp[warp];
       float* wring = RG.ring + (size_t)warp * kSub * ICB_ROWF;
       unsigned long long* wfull = RG.full + warp * kSub;
@@ -1139,68 +1139,136 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
         const int sbase = (kb & 1) * 8;
         cp_async_wait<1>();   // this batch's group has landed (the next one may be in flight)
         __syncwarp();         // ...and every lane's part of it is visible to the warp
-        float keep[SLOTS];
-        // branch-free over the 8 rows (rows >= nrow score stale smem and are
-        // never stored) so the 8 independent reduction chains interleave
+        if constexpr (GP == 4) {
+          // Fully transposed reduction of the batch's 8 rows x 4 heads: in
+          // slot jj lane l scores smem row jj ^ pi(l), pi(l) = lane bits 4..2,
+          // so at the row levels (xor 16, 8, 4) every lane keeps its low slots
+          // and sends its high ones with no selects, on packed head pairs
+          // (FADD2); the head levels (xor 2, 1) split the pairs.  Every sum is
+          // still the 16,8,4,2,1 pairing tree of warp_sum_butterfly, and lane l
+          // ends with (row pi(l), head l & 3).
+          const int pi = (lane >> 2) & 7;
+          unsigned long long v[8][2];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const float* srow = wring + (size_t)(sbase + u) * ICB_ROWF;
-          const float4 p = reinterpret_cast<const float4*>(srow)[lane];
-          const float tl = __shfl_sync(0xffffffffu, m0.tail, u);
-          float v[GP];
-          if constexpr (GP == 1) {
-            v[0] = lane_sq4(p, qv[0]);
-          } else {
-#pragma unroll
-            for (int h = 0; h < GP / 2; ++h) {
-              const float2 r2 = lane_sq4_x2(p, q2[h]);
-              v[2 * h] = r2.x;
-              v[2 * h + 1] = r2.y;
-            }
+          for (int jj = 0; jj < 8; ++jj) {
+            const float4 p = reinterpret_cast<const float4*>(wring + (size_t)(sbase + (jj ^ pi)) * ICB_ROWF)[lane];
+            v[jj][0] = lane_sq4_x2_packed(p, q2[0]);
+            v[jj][1] = lane_sq4_x2_packed(p, q2[1]);
           }
-          float f = reduce_heads<GP>(v, lane);
-          float d2 = d2_finish(f, tl, qt_my);
-          if ((u % LPG) == (lane % LPG)) keep[u / LPG] = d2;
-        }
-        // every lane's smem reads of this batch have retired (the butterflies
-        // consumed them): its slots take the batch after next
-        __syncwarp();
-        issue(kb + 2, a2.tok);
 #pragma unroll
-        for (int sl = 0; sl < SLOTS; ++sl) {
-          const int u = sl * LPG + (lane % LPG);
-          const int src = u < 8 ? u : 0;
-          const int tok = __shfl_sync(0xffffffffu, m0.tok, src);
-          const int msk = __shfl_sync(0xffffffffu, m0.mask, src);
-          const int upr = __shfl_sync(0xffffffffu, m0.upre, src);
+          for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) v[jj][h] = fadd2(v[jj][h], shfl_xor_u64(v[jj + 4][h], 16));
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) v[jj][h] = fadd2(v[jj][h], shfl_xor_u64(v[jj + 2][h], 8));
+#pragma unroll
+          for (int h = 0; h < 2; ++h) v[0][h] = fadd2(v[0][h], shfl_xor_u64(v[1][h], 4));
+          const bool b1 = lane & 2, b0 = lane & 1;
+          const unsigned long long w = fadd2(b1 ? v[0][1] : v[0][0], shfl_xor_u64(b1 ? v[0][0] : v[0][1], 2));
+          const float wl = __uint_as_float((unsigned)w), wh = __uint_as_float((unsigned)(w >> 32));
+          const float f = __fadd_rn(b0 ? wh : wl, __shfl_xor_sync(0xffffffffu, b0 ? wl : wh, 1));
+          const float d2 = d2_finish(f, __shfl_sync(0xffffffffu, m0.tail, pi), qt_my);
+          // every lane's smem reads of this batch have retired: its slots take
+          // the batch after next
+          __syncwarp();
+          issue(kb + 2, a2.tok);
+          const int h = lane & 3;
+          const int tok = __shfl_sync(0xffffffffu, m0.tok, pi);
+          const int msk = __shfl_sync(0xffffffffu, m0.mask, pi);
+          const int upr = __shfl_sync(0xffffffffu, m0.upre, pi);
           int pos = 0;
 #pragma unroll
-          for (int g = 0; g < GP; ++g) {
-            const int pg = __shfl_sync(0xffffffffu, m0.uo[g], src);
-            if (g == myh) pos = pg;
+          for (int g = 0; g < 4; ++g) {
+            const int pg = __shfl_sync(0xffffffffu, m0.uo[g], pi);
+            if (g == h) pos = pg;
           }
-          pos += base + u - upr;   // row index within its node
-          if (u < nrow && myh < G && ((msk >> myh) & 1)) {
-            ICB_CHECK(pos >= 0 && pos < S.M[myh], "cand pos %d M %d", pos, S.M[myh]);
-            SS.cand[(size_t)myh * SS.ccap + pos] = make_key(keep[sl], tok);
-            const unsigned hb = __float_as_uint(keep[sl]);
+          pos += base + pi - upr;
+          if (pi < nrow && h < G && ((msk >> h) & 1)) {
+            ICB_CHECK(pos >= 0 && pos < S.M[h], "cand pos %d M %d", pos, S.M[h]);
+            SS.cand[(size_t)h * SS.ccap + pos] = make_key(d2, tok);
+            const unsigned hb = __float_as_uint(d2);
             mn = min(mn, hb);
             mx = max(mx, hb);
           }
+        } else {
+          float keep[SLOTS];
+          // branch-free over the 8 rows (rows >= nrow score stale smem and are
+          // never stored) so the 8 independent reduction chains interleave
+  #pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float* srow = wring + (size_t)(sbase + u) * ICB_ROWF;
+            const float4 p = reinterpret_cast<const float4*>(srow)[lane];
+            const float tl = __shfl_sync(0xffffffffu, m0.tail, u);
+            float v[GP];
+            if constexpr (GP == 1) {
+              v[0] = lane_sq4(p, qv[0]);
+            } else {
+  #pragma unroll
+              for (int h = 0; h < GP / 2; ++h) {
+                const float2 r2 = lane_sq4_x2(p, q2[h]);
+                v[2 * h] = r2.x;
+                v[2 * h + 1] = r2.y;
+              }
+            }
+            float f = reduce_heads<GP>(v, lane);
+            float d2 = d2_finish(f, tl, qt_my);
+            if ((u % LPG) == (lane % LPG)) keep[u / LPG] = d2;
+          }
+          // every lane's smem reads of this batch have retired (the butterflies
+          // consumed them): its slots take the batch after next
+          __syncwarp();
+          issue(kb + 2, a2.tok);
+  #pragma unroll
+          for (int sl = 0; sl < SLOTS; ++sl) {
+            const int u = sl * LPG + (lane % LPG);
+            const int src = u < 8 ? u : 0;
+            const int tok = __shfl_sync(0xffffffffu, m0.tok, src);
+            const int msk = __shfl_sync(0xffffffffu, m0.mask, src);
+            const int upr = __shfl_sync(0xffffffffu, m0.upre, src);
+            int pos = 0;
+  #pragma unroll
+            for (int g = 0; g < GP; ++g) {
+              const int pg = __shfl_sync(0xffffffffu, m0.uo[g], src);
+              if (g == myh) pos = pg;
+            }
+            pos += base + u - upr;   // row index within its node
+            if (u < nrow && myh < G && ((msk >> myh) & 1)) {
+              ICB_CHECK(pos >= 0 && pos < S.M[myh], "cand pos %d M %d", pos, S.M[myh]);
+              SS.cand[(size_t)myh * SS.ccap + pos] = make_key(keep[sl], tok);
+              const unsigned hb = __float_as_uint(keep[sl]);
+              mn = min(mn, hb);
+              mx = max(mx, hb);
+            }
+          }
+
         }
         m0 = m1;
         m1 = m2;
         a2 = a3;
       }
       // per-head d2 range of this level's candidates (feeds the selection bins)
+      if constexpr (GP == 4) {   // head = lane & 3
 #pragma unroll
-      for (int o = 1; o < LPG; o <<= 1) {
-        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      }
-      if ((lane % LPG) == 0 && myh < G && mx >= mn) {
-        atomicMin(&GSA[myh].lo, mn);
-        atomicMax(&GSA[myh].hi, mx);
+        for (int o = 4; o < 32; o <<= 1) {
+          mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+          mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (lane < G && lane < 4 && mx >= mn) {
+          atomicMin(&GSA[lane].lo, mn);
+          atomicMax(&GSA[lane].hi, mx);
+        }
+      } else {
+#pragma unroll
+        for (int o = 1; o < LPG; o <<= 1) {
+          mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+          mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if ((lane % LPG) == 0 && myh < G && mx >= mn) {
+          atomicMin(&GSA[myh].lo, mn);
+          atomicMax(&GSA[myh].hi, mx);
+        }
       }
       __syncwarp();
       if (lane == 0) RG.qp[warp] = qb + (unsigned)kb;   // batches this warp consumed
