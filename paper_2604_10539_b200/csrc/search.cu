@@ -157,9 +157,11 @@ using namespace icb;
 extern "C" int icb_search_profile(unsigned long long* out, int reset) {
   ICB_CUDA(cudaDeviceSynchronize());
   ICB_CUDA(cudaMemcpyFromSymbol(out, g_search_prof, sizeof(unsigned long long) * kPhases));
+  ICB_CUDA(cudaMemcpyFromSymbol(out + kPhases, g_topb_stats, sizeof(unsigned long long) * 8));
   if (reset) {
     unsigned long long z[kPhases] = {};
     ICB_CUDA(cudaMemcpyToSymbol(g_search_prof, z, sizeof(z)));
+    ICB_CUDA(cudaMemcpyToSymbol(g_topb_stats, z, sizeof(unsigned long long) * kPhases));
   }
   return ICB_OK;
 }

@@ -456,26 +456,31 @@ __device__ unsigned long long group_radix_threshold(GroupSmem& GS, int gtid, int
   return ~0ull;
 }
 
-// bitonic sort of n <= kBuf keys in GS.buf (ascending), group-wide
+// bitonic sort of n keys in the smem buffer `buf` (capacity >= the next power
+// of two), ascending, group-wide
 template <int NTG>
-__device__ void group_sort(GroupSmem& GS, int gtid, int bar, int n) {
+__device__ void group_sort_buf(unsigned long long* buf, int gtid, int bar, int n) {
   int P = 1;
   while (P < n) P <<= 1;
-  for (int i = n + gtid; i < P; i += NTG) GS.buf[i] = ~0ull;
+  for (int i = n + gtid; i < P; i += NTG) buf[i] = ~0ull;
   gsync(bar, NTG);
   for (int k = 2; k <= P; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int i = gtid; i < P; i += NTG) {
         int ixj = i ^ j;
         if (ixj > i) {
-          unsigned long long a = GS.buf[i], b = GS.buf[ixj];
+          unsigned long long a = buf[i], b = buf[ixj];
           bool upw = (i & k) == 0;
-          if ((a > b) == upw) { GS.buf[i] = b; GS.buf[ixj] = a; }
+          if ((a > b) == upw) { buf[i] = b; buf[ixj] = a; }
         }
       }
       gsync(bar, NTG);
     }
   }
+}
+template <int NTG>
+__device__ void group_sort(GroupSmem& GS, int gtid, int bar, int n) {
+  group_sort_buf<NTG>(GS.buf, gtid, bar, n);
 }
 
 // Threshold of the B smallest of M unique keys (d2 bits of every key within
@@ -559,6 +564,138 @@ __device__ unsigned long long group_threshold(GroupSmem& GS, int gtid, int bar, 
     thr = group_radix_threshold<NTG>(GS, gtid, bar, keys, M, B);
   }
   return thr;
+}
+
+// Top-B of M unique keys (d2 bits within [lo, hi]) written UNORDERED to `out`
+// (global or smem) in two passes over the list instead of three: a
+// kTopBins-bin histogram over [lo, hi] in the head group's slice of the idle
+// row ring, then one pass that emits every key of a bin below the boundary
+// bin and gathers the boundary bin into smem; its sorted head completes the
+// B.  16 loads in flight per thread.  A crowded boundary bin falls back to the
+// radix threshold.  Returns min(M, B).
+// selection statistics (per translation unit; the query kernel's are
+// reported by icb_search_profile): selections, radix fallbacks, boundary sizes
+static __device__ unsigned long long g_topb_stats[8];
+
+template <int GP>
+struct TopB {
+  static constexpr int kBins = GP <= 4 ? 2048 : 1024;
+  static constexpr int kBufN = 512;
+  static constexpr size_t kBytes = (size_t)kBins * 4 + (size_t)kBufN * 8;   // per head group
+};
+
+template <int NTG, int GP>
+__device__ int group_topb(GroupSmem& GS, unsigned char* rg, int gtid, int bar, const unsigned long long* keys,
+                          int M, long long B, unsigned lo, unsigned hi, unsigned long long* out, bool prof) {
+  static_assert(TopB<GP>::kBytes * GP <= (size_t)kRing * ICB_ROWF * 4, "top-B scratch exceeds the row ring");
+  constexpr int U = 16;
+  constexpr int NB = TopB<GP>::kBins;
+  constexpr int NBB = 31 - __builtin_clz(NB);
+  const int lane = gtid & 31;
+  int* hist = reinterpret_cast<int*>(rg);
+  unsigned long long* bb = reinterpret_cast<unsigned long long*>(rg + (size_t)NB * 4);
+  const int Mpad = (M + U * NTG - 1) / (U * NTG) * (U * NTG);   // group-uniform trip counts
+  if (B >= M) {
+    for (int i0 = gtid; i0 < Mpad; i0 += U * NTG) {
+      unsigned long long kk[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) kk[u] = i0 + u * NTG < M ? keys[i0 + u * NTG] : 0ull;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (i0 + u * NTG < M) out[i0 + u * NTG] = kk[u];
+    }
+    gsync(bar, NTG);
+    return M;
+  }
+  long long tq0 = clock64();
+  const unsigned range = hi - lo;
+  const int nbits = range ? 32 - __clz(range) : 0;
+  const int shift = nbits > NBB ? nbits - NBB : 0;
+  for (int i = gtid; i < NB; i += NTG) hist[i] = 0;
+  gsync(bar, NTG);
+  for (int i0 = gtid; i0 < Mpad; i0 += U * NTG) {
+    unsigned hb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) hb[u] = i0 + u * NTG < M ? (unsigned)(keys[i0 + u * NTG] >> 32) : 0u;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i0 + u * NTG < M) {
+        ICB_CHECK(hb[u] >= lo && hb[u] <= hi, "hb %u outside [%u, %u]", hb[u], lo, hi);
+        atomicAdd(&hist[(hb[u] - lo) >> shift], 1);
+      }
+  }
+  long long tq1 = clock64();
+  gsync(bar, NTG);
+  // boundary bin: each thread owns NB / NTG consecutive bins
+  constexpr int PER = NB / NTG;
+  int local = 0;
+#pragma unroll 8
+  for (int u = 0; u < PER; ++u) local += hist[gtid * PER + u];
+  int tot;
+  const int excl = group_scan<NTG>(GS, gtid, bar, local, tot);
+  if (excl < B && excl + local >= B) {
+    int run = excl;
+    for (int u = 0; u < PER; ++u) {
+      const int c = hist[gtid * PER + u];
+      if (run + c >= B) { GS.misc[4] = gtid * PER + u; GS.misc[5] = run; GS.misc[6] = c; break; }
+      run += c;
+    }
+  }
+  if (gtid == 0) { GS.misc[0] = 0; GS.misc[7] = 0; }
+  gsync(bar, NTG);
+  const int bstar = GS.misc[4], below = GS.misc[5], nb = GS.misc[6];
+  if (prof && gtid == 0) { atomicAdd(&g_topb_stats[0], 1ull); atomicAdd(&g_topb_stats[2], (unsigned long long)nb); }
+  if (nb > TopB<GP>::kBufN) {
+    if (prof && gtid == 0) atomicAdd(&g_topb_stats[1], 1ull);
+    const unsigned long long thr = group_radix_threshold<NTG>(GS, gtid, bar, keys, M, B);
+    group_emit<NTG>(GS, gtid, bar, keys, M, thr, nullptr, 0, out, 0, nullptr, nullptr, nullptr);
+    return (int)B;
+  }
+  long long tq2 = clock64();
+  for (int i0 = gtid; i0 < Mpad; i0 += U * NTG) {
+    unsigned long long kk[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) kk[u] = i0 + u * NTG < M ? keys[i0 + u * NTG] : ~0ull;
+    // classify all U keys, then ONE warp scan + ONE atomic place this
+    // thread's low keys contiguously
+    unsigned lowm = 0u;
+    int nlow = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool valid = i0 + u * NTG < M;
+      const int bin = (int)(((unsigned)(kk[u] >> 32) - lo) >> shift);
+      const bool low = valid && bin < bstar;
+      lowm |= low ? (1u << u) : 0u;
+      nlow += low ? 1 : 0;
+      if (valid && bin == bstar) bb[atomicAdd(&GS.misc[7], 1)] = kk[u];
+    }
+    int incl = nlow;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int at = 0;
+    if (lane == 31 && incl) at = atomicAdd(&GS.misc[0], incl);
+    at = __shfl_sync(0xffffffffu, at, 31) + incl - nlow;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if ((lowm >> u) & 1u) out[at++] = kk[u];
+  }
+  gsync(bar, NTG);
+  long long tq3 = clock64();
+  group_sort_buf<NTG>(bb, gtid, bar, nb);
+  const int need = (int)(B - below);
+  for (int i = gtid; i < need; i += NTG) out[below + i] = bb[i];
+  gsync(bar, NTG);
+  if (prof && gtid == 0) {
+    long long tq4 = clock64();
+    atomicAdd(&g_topb_stats[3], (unsigned long long)(tq1 - tq0));
+    atomicAdd(&g_topb_stats[4], (unsigned long long)(tq2 - tq1));
+    atomicAdd(&g_topb_stats[5], (unsigned long long)(tq3 - tq2));
+    atomicAdd(&g_topb_stats[6], (unsigned long long)(tq4 - tq3));
+  }
+  return (int)B;
 }
 
 // ------------------------------------------------------------------ P-DCI
@@ -1320,7 +1457,12 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
       if (lv == start && gtid == 0) { GS.plo = 0xffffffffu; GS.phi = 0u; }
       gsync(gbar, NTG);
       const bool nopool = S.nopool;
-      if (lv > floor) {
+      unsigned char* rg = reinterpret_cast<unsigned char*>(RG.ring) + (size_t)grp * TopB<GP>::kBytes;
+      if (nopool && lv > floor) {
+        const int n = group_topb<NTG, GP>(GS, rg, gtid, gbar, cg, M, P.beam, GS.lo, GS.hi,
+                                                  SS.surv + (size_t)g * SS.ccap, P.prof != nullptr);
+        if (gtid == 0) S.nsurv[g] = n;
+      } else if (lv > floor) {
         unsigned long long thr = group_threshold<NTG>(GS, gtid, gbar, cg, M, P.beam, GS.lo, GS.hi);
         const int2 r = group_emit<NTG>(GS, gtid, gbar, cg, M, thr, SS.surv + (size_t)g * SS.ccap, 0,
                                        collect_all && !nopool ? pg : nullptr, S.npool[g], sg, &GS.plo, &GS.phi);
@@ -1330,9 +1472,7 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
         }
       } else if (nopool) {
         // the floor's top-k is the answer: straight into the group's buffer, sorted
-        unsigned long long thr = group_threshold<NTG>(GS, gtid, gbar, cg, M, P.k, GS.lo, GS.hi);
-        const int n = group_emit<NTG>(GS, gtid, gbar, cg, M, thr, nullptr, 0, GS.buf, 0, nullptr, nullptr,
-                                      nullptr).y;
+        const int n = group_topb<NTG, GP>(GS, rg, gtid, gbar, cg, M, P.k, GS.lo, GS.hi, GS.buf, P.prof != nullptr);
         group_sort<NTG>(GS, gtid, gbar, n);
         if (gtid == 0) S.npool[g] = n;
       } else {
