@@ -13,8 +13,8 @@ from .errors import (ConfigError, ConsistencyError, DegenerateQueryError, IceCac
                      PolicyError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libicecache_b200_debug.so" if os.environ.get("ICB_DEBUG_LIB") == "1"
-                        else "libicecache_b200.so")
+LIB_PATH = os.environ.get("ICB_LIB") or os.path.join(
+    _HERE, "libicecache_b200_debug.so" if os.environ.get("ICB_DEBUG_LIB") == "1" else "libicecache_b200.so")
 
 ICB_OK, ICB_E_INPUT, ICB_E_CONFIG, ICB_E_CONSISTENCY, ICB_E_CUDA, ICB_E_CAPACITY, ICB_E_POLICY, \
     ICB_E_DEGENERATE = range(8)

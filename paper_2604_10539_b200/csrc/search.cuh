@@ -896,7 +896,9 @@ __device__ __forceinline__ float reduce_heads(float (&v)[G], int lane) {
 }
 
 // GP: padded head count (power of two >= P.G) fixing register arrays.
-template <int NT, int GP>
+// XP: the fully transposed G=4 stream reduction (register heavy; the insert
+// kernel's small parent searches use the generic path).
+template <int NT, int GP, bool XP = true>
 __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, const ForestView& F,
                             const SearchScratch& SS, int t,
                             const SearchParams& P, double* dirs_tmp) {
@@ -1198,7 +1200,7 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
       constexpr int LPG = 32 / GP;              // lanes holding one head's sum
       constexpr int SLOTS = (8 + LPG - 1) / LPG;
       const int myh = lane / LPG;
-      const float qt_my = S.qt[GP == 4 ? (lane & 3) : myh];
+      const float qt_my = S.qt[(GP == 4 && XP) ? (lane & 3) : myh];
       const unsigned qb = RG.qp[warp];
       float* wring = RG.ring + (size_t)warp * kSub * ICB_ROWF;
       unsigned long long* wfull = RG.full + warp * kSub;
@@ -1276,7 +1278,7 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
         const int sbase = (kb & 1) * 8;
         cp_async_wait<1>();   // this batch's group has landed (the next one may be in flight)
         __syncwarp();         // ...and every lane's part of it is visible to the warp
-        if constexpr (GP == 4) {
+        if constexpr (GP == 4 && XP) {
           // Fully transposed reduction of the batch's 8 rows x 4 heads: in
           // slot jj lane l scores smem row jj ^ pi(l), pi(l) = lane bits 4..2,
           // so at the row levels (xor 16, 8, 4) every lane keeps its low slots
@@ -1386,7 +1388,7 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
         a2 = a3;
       }
       // per-head d2 range of this level's candidates (feeds the selection bins)
-      if constexpr (GP == 4) {   // head = lane & 3
+      if constexpr (GP == 4 && XP) {   // head = lane & 3
 #pragma unroll
         for (int o = 4; o < 32; o <<= 1) {
           mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));

@@ -28,7 +28,7 @@ from .forest import DeviceForest, ForestCaps, dense_attention
 @dataclass
 class EngineConfig:
     """Field names and validation follow engine.py:37-92 verbatim; the last
-    three fields are device options."""
+    four fields are device options."""
 
     layers: int = 4
     kv_heads: int = 2
@@ -52,6 +52,7 @@ class EngineConfig:
     kv_dtype: str = "fp32"        # page K/V storage: "fp32" | "bf16"
     max_tokens: int | None = None  # token capacity (prefill + decode); default prefill + 1024
     layer_serial: bool = False
+    overlap_dense: bool = True     # skip layers' dense attention on a side stream, concurrent with the search
 
     def __post_init__(self) -> None:
         if min(self.layers, self.kv_heads, self.query_heads_per_group, self.d, self.d_prime) < 1:
@@ -123,6 +124,7 @@ class Engine:
         self._win_fills: list[int] = []
         self.last_pages = None
         self.last_npages = None
+        self._side = None
 
     # -- prefill ---------------------------------------------------------------
     def prefill(self, keys, values, n_prefill: int) -> "Engine":
@@ -260,11 +262,32 @@ class Engine:
         if out is None:
             out = torch.empty((L, H * G, cfg.d_prime), dtype=torch.float32, device=dev)
         rotate = self.rotation_due()
-        self._dense_part(q, kk, vv, token, out)
+        overlap = cfg.overlap_dense and not self.fallback and self.n_dense > 0 and dev.type == "cuda"
+        if not overlap:
+            self._dense_part(q, kk, vv, token, out)
+            dense_hook = None
+        else:
+            # The skip layers' dense attention depends only on this step's
+            # inputs: it runs on a side stream, issued right after the search
+            # kernel so its CTAs fill the SMs the search leaves idle (the
+            # search runs one CTA per tree, two per SM at most).
+            main = torch.cuda.current_stream(dev)
+            if self._side is None:
+                self._side = torch.cuda.Stream(device=dev)
+            ready, done = torch.cuda.Event(), torch.cuda.Event()
+            ready.record(main)
+
+            def dense_hook():
+                self._side.wait_event(ready)
+                with torch.cuda.stream(self._side):
+                    self._dense_part(q, kk, vv, token, out)
+                done.record(self._side)
         if not self.fallback:
             if metrics:
                 self.stats.zero_()
-            self._indexed_part(q, kk, vv, token, rotate, out)
+            self._indexed_part(q, kk, vv, token, rotate, out, dense_hook)
+            if overlap:
+                main.wait_event(done)
             if rotate:
                 start, fill = self._win_start[0], self._win_fills[0]
                 self.indexed_tokens.extend(range(start, start + fill))
@@ -295,7 +318,7 @@ class Engine:
         res = dense_attention(qd.contiguous(), self.dense_k, self.dense_v, token + 1)
         out[:nd] = res[:, :, : cfg.d_prime].reshape(nd, H * G, cfg.d_prime)
 
-    def _indexed_part(self, q, kk, vv, token, rotate, out):
+    def _indexed_part(self, q, kk, vv, token, rotate, out, after_query=None):
         cfg, f = self.cfg, self.forest
         s0, H, G = cfg.skip_layers, cfg.kv_heads, cfg.query_heads_per_group
         T = self.T
@@ -311,6 +334,9 @@ class Engine:
             f.append_window(trees, token, ki[a:b], vi[a:b])
             f.query(trees, qi[a:b], k, self.beam, self.visit_cap, k_out=k, pages_cap=self.pages_cap,
                     out=(self.ids[a:b], self.counts[a:b], self.pages[a:b], self.npages[a:b]))
+            if after_query is not None:
+                after_query()
+                after_query = None
             o = f.attention(trees, qi[a:b], self.pages[a:b], self.npages[a:b], stats=self.stats[a:b],
                             scalar_bytes=cfg.scalar_bytes)
             out[s0 + a // H: s0 + b // H] = o.reshape((b - a) // H, H * G, cfg.d_prime)

@@ -1,0 +1,40 @@
+"""Time the window-rotation insert kernel (16 inserts per tree, every 16
+decode steps) at C2 with CUDA events around Forest.rotate_window."""
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2604_10539_b200.engine import Engine, EngineConfig  # noqa: E402
+from paper_2604_10539_b200.workload import clustered_stream  # noqa: E402
+
+ctx = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
+C2 = dict(layers=32, kv_heads=8, query_heads_per_group=4, d=128, d_prime=128, page_size=16,
+          token_budget=256, promotion_ratio=0.1, sink_pages=1, window_pages=2, skip_layers=2)
+steps = 96
+st = clustered_stream(ctx, steps, 32, 8, 4, 128, 128, device="cuda")
+eng = Engine(EngineConfig(**C2, kv_dtype="bf16", max_tokens=ctx + steps + 1)).prefill(st.keys, st.values, ctx)
+f = eng.forest
+orig = f.rotate_window
+times = []
+
+
+def timed(*a, **kw):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    r = orig(*a, **kw)
+    e1.record()
+    times.append((e0, e1))
+    return r
+
+
+f.rotate_window = timed
+for i in range(steps):
+    eng.decode_step(ctx + i, st.queries[i], st.keys[ctx + i], st.values[ctx + i], metrics=False)
+torch.cuda.synchronize()
+ms = [a.elapsed_time(b) for a, b in times]
+print("rotations", len(ms), "ms each", [round(x, 3) for x in ms])
+print("mean rotation ms %.3f  -> %.1f us per decode step amortized" % (sum(ms[1:]) / max(1, len(ms) - 1),
+                                                                    1e3 * sum(ms[1:]) / max(1, len(ms) - 1) / 16))
