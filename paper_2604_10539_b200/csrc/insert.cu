@@ -16,6 +16,7 @@
 // stashed in the token's (not yet used) lifted row so the insert lifts the
 // exact input key even when pages store bf16.
 #include "search.cuh"
+#include "warp_search.cuh"
 #include "internal.h"
 
 namespace icb {
@@ -106,14 +107,22 @@ __device__ void write_slot(const ForestView& F, int t, int page, int slot, const
   }
 }
 
-// One insert; all threads of the block participate.  key: fp32 raw key
-// (global); returns the level (valid in thread 0).
+// Inserts run in three stages:
+//   prepare   duplicate check, level draw (the tree's level stream, in
+//             insertion order), lift (dci.py:225-240) into the token's row and
+//             into query slot `qs` of S; returns the level (-1: rejected);
+//   place     the node that receives the point at its level (top node /
+//             _grow_top / own(parent, level) from the parent search);
+//   finish    membership, own-node chain below the level, page placement
+//             (dci.py:368-381) and the K/V slot write.
+// The level summary (start level, upper list) learns of a point only when it
+// is placed, so a point prepared ahead of a pending batched search stays
+// invisible to that search.
 template <int NT>
-__device__ int insert_one(SearchSmem& S, GroupSmem* GSA, const RingView& RG, const ForestView& F, const SearchScratch& SS, int t, int tok,
-                          const float* key, const float* val, long long src_slot, int given_level,
-                          double* dirs_tmp) {
+__device__ int insert_prepare(SearchSmem& S, const ForestView& F, int t, int tok, const float* key, int given_level,
+                              int qs) {
   TreeMeta* m = F.meta + t;
-  __shared__ int s_level, s_bad, s_leaf, s_container, s_chain_from;
+  __shared__ int s_level, s_bad;
   __shared__ double s_norm;
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -132,7 +141,6 @@ __device__ int insert_one(SearchSmem& S, GroupSmem* GSA, const RingView& RG, con
     if (lv > 62) lv = 62;
     s_level = lv;
   }
-  // lift (dci.py:225-240): norm in pairwise order; clamp above c
   for (int u = tid; u < F.dim; u += NT) {
     double x = (double)key[u];
     S.q64[u] = __dmul_rn(x, x);
@@ -151,81 +159,72 @@ __device__ int insert_one(SearchSmem& S, GroupSmem* GSA, const RingView& RG, con
   for (int u = tid; u < ICB_DPAD; u += NT) {
     float v = u < F.dim ? __double2float_rn(__ddiv_rn((double)kv, safe)) : 0.0f;
     row[u] = v;
-    S.q[0][u] = v;
+    S.q[qs][u] = v;
   }
   if (tid > 0 && tid < ICB_ROWF - ICB_DPAD) row[ICB_DPAD + tid] = 0.0f;
+  const int level = s_level;
   if (tid == 0) {
     double ratio = __ddiv_rn(norm, safe);
     double rad = __dsub_rn(1.0, __dmul_rn(ratio, ratio));
     float tl = __double2float_rn(sqrt(rad > 0.0 ? rad : 0.0));
     F.tail[F.tk(t, tok)] = tl;
     if (ICB_ROWF > ICB_DPAD) row[ICB_DPAD] = tl;
-    S.qt[0] = tl;
+    S.qt[qs] = tl;
     if (over) m->scale_clamps += 1;
-    F.level[F.tk(t, tok)] = (int8_t)s_level;
-    note_point_level(F, t, tok, s_level);
+    F.level[F.tk(t, tok)] = (int8_t)level;
     F.own_base[F.tk(t, tok)] = m->own_top;
-    if (m->own_top + s_level - 1 > F.own_cap) set_err(m, ICB_ERR_CAP_OWN);
-    m->own_top += s_level - 1;
+    if (m->own_top + level - 1 > F.own_cap) set_err(m, ICB_ERR_CAP_OWN);
+    m->own_top += level - 1;
   }
   __syncthreads();
-  const int level = s_level;
-  const int L = m->levels;
-  if (L == 0) {
-    if (tid == 0) {
-      int top = new_node(F, t, level, -1, ICB_ROOT_OWNER, tok);
-      m->top_node = top;
-      m->levels = level;
-      s_container = top;
-      s_chain_from = level - 1;
-    }
-  } else if (level > L) {
-    if (tid == 0) {
-      int old_top = m->top_node;
-      int top = new_node(F, t, level, -1, ICB_ROOT_OWNER, tok);
-      m->top_node = top;
-      int prev = top;
-      for (int lv = level - 1; lv > L; --lv) {
-        prev = new_node(F, t, lv, prev, tok, tok);
-        set_own(F, t, tok, lv, prev);
-      }
-      size_t x = F.nd(t, old_top);
-      F.node_owner[x] = tok;
-      F.node_parent[x] = prev;
-      set_own(F, t, tok, L, old_top);
-      add_member(F, t, old_top, tok);
-      F.node_opos[x] = F.node_size[x] - 1;   // the new owner was appended
-      m->levels = level;
-      s_container = old_top;   // membership at level L
-      s_chain_from = L - 1;
-    }
-  } else {
-    if (level == L) {
-      if (tid == 0) { s_container = m->top_node; s_chain_from = level - 1; }
-    } else {
-      SearchParams P;
-      P.G = 1; P.k = 1; P.beam = 8; P.visit_cap = 64; P.target = level + 1; P.prof = nullptr;
-      tree_search<NT, 1>(S, GSA, RG, F, SS, t, P, dirs_tmp);
-      int n = finalize_groups<NT, 1>(S, GSA, F, SS, 1, 1);
-      if (tid == 0) {
-        int parent = n > 0 ? key_id(GSA[0].buf[0]) : -1;
-        s_container = parent >= 0 ? F.own(t, parent, level) : m->top_node;
-        s_chain_from = level - 1;
-      }
-    }
+  return level;
+}
+
+// Block-wide parent search of query slot qs (the P-DCI-capable path; used
+// only when a warp search meets a node the reference visits with P-DCI).
+template <int NT>
+__device__ __forceinline__ int block_parent_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG,
+                                                const ForestView& F, const SearchScratch& SS, int t, int qs,
+                                                int target, double* dirs_tmp) {
+  __shared__ int s_parent;
+  __shared__ float s_swap_t;
+  const int tid = threadIdx.x;
+  if (qs != 0) {   // tree_search reads slot 0: swap the slots
+    for (int u = tid; u < ICB_DPAD; u += NT) { float a = S.q[0][u]; S.q[0][u] = S.q[qs][u]; S.q[qs][u] = a; }
+    if (tid == 0) { s_swap_t = S.qt[0]; S.qt[0] = S.qt[qs]; S.qt[qs] = s_swap_t; }
     __syncthreads();
-    if (tid == 0) add_member(F, t, s_container, tok);
   }
+  SearchParams P;
+  P.G = 1; P.k = 1; P.beam = 8; P.visit_cap = 64; P.target = target; P.prof = nullptr;
+  tree_search<NT, 1>(S, GSA, RG, F, SS, t, P, dirs_tmp);
+  const int n = finalize_groups<NT, 1>(S, GSA, F, SS, 1, 1);
+  if (tid == 0) s_parent = n > 0 ? key_id(GSA[0].buf[0]) : -1;
   __syncthreads();
+  if (qs != 0) {
+    for (int u = tid; u < ICB_DPAD; u += NT) { float a = S.q[0][u]; S.q[0][u] = S.q[qs][u]; S.q[qs][u] = a; }
+    if (tid == 0) { s_swap_t = S.qt[0]; S.qt[0] = S.qt[qs]; S.qt[qs] = s_swap_t; }
+    __syncthreads();
+  }
+  return s_parent;
+}
+
+template <int NT>
+__device__ void insert_finish(SearchSmem& S, const ForestView& F, int t, int tok, int level, int container,
+                              int chain_from, bool add_to_container, const float* key, const float* val,
+                              long long src_slot) {
+  TreeMeta* m = F.meta + t;
+  __shared__ int s_leaf;
+  const int tid = threadIdx.x;
   if (tid == 0) {
-    int parent_node = s_container;   // node holding tok at chain_from + 1
-    for (int lv = s_chain_from; lv >= 1; --lv) {
+    note_point_level(F, t, tok, level);
+    if (add_to_container) add_member(F, t, container, tok);
+    int parent_node = container;   // node holding tok at chain_from + 1
+    for (int lv = chain_from; lv >= 1; --lv) {
       int nn = new_node(F, t, lv, parent_node, tok, tok);
       set_own(F, t, tok, lv, nn);
       parent_node = nn;
     }
-    int leaf = level >= 2 ? F.own(t, tok, 1) : s_container;
-    // page placement (dci.py:368-381)
+    int leaf = level >= 2 ? F.own(t, tok, 1) : container;
     size_t lx = F.nd(t, leaf);
     int page = F.node_lastpage[lx];
     if (page < 0 || F.page_fill[F.pg(t, page)] >= F.s) {
@@ -251,7 +250,135 @@ __device__ int insert_one(SearchSmem& S, GroupSmem* GSA, const RingView& RG, con
   __syncthreads();
   if (s_leaf >= 0 && tid < 32) write_slot(F, t, s_leaf, S.misc[4], key, val, src_slot);
   __syncthreads();
-  return level;
+}
+
+struct InsertPoint {
+  int tok;
+  const float* key;
+  const float* val;
+  long long src_slot;
+  int given_level;
+};
+
+// Structure + finish of a prepared point; `parent` is its parent search's
+// result when level < the tree height (searched by insert_points).
+template <int NT>
+__device__ void insert_place(SearchSmem& S, const ForestView& F, int t, const InsertPoint& pt, int level,
+                             int parent) {
+  TreeMeta* m = F.meta + t;
+  __shared__ int s_container, s_chain_from, s_add;
+  const int tid = threadIdx.x;
+  const int tok = pt.tok;
+  const int L = m->levels;
+  if (L == 0) {
+    if (tid == 0) {
+      int top = new_node(F, t, level, -1, ICB_ROOT_OWNER, tok);
+      m->top_node = top;
+      m->levels = level;
+      s_container = top;
+      s_chain_from = level - 1;
+      s_add = 0;
+    }
+  } else if (level > L) {
+    if (tid == 0) {
+      int old_top = m->top_node;
+      int top = new_node(F, t, level, -1, ICB_ROOT_OWNER, tok);
+      m->top_node = top;
+      int prev = top;
+      for (int lv = level - 1; lv > L; --lv) {
+        prev = new_node(F, t, lv, prev, tok, tok);
+        set_own(F, t, tok, lv, prev);
+      }
+      size_t x = F.nd(t, old_top);
+      F.node_owner[x] = tok;
+      F.node_parent[x] = prev;
+      set_own(F, t, tok, L, old_top);
+      add_member(F, t, old_top, tok);
+      F.node_opos[x] = F.node_size[x] - 1;   // the new owner was appended
+      m->levels = level;
+      s_container = old_top;   // membership at level L
+      s_chain_from = L - 1;
+      s_add = 0;
+    }
+  } else if (level == L) {
+    if (tid == 0) { s_container = m->top_node; s_chain_from = level - 1; s_add = 1; }
+  } else {
+    if (tid == 0) {
+      s_container = parent >= 0 ? F.own(t, parent, level) : m->top_node;
+      s_chain_from = level - 1;
+      s_add = 1;
+    }
+  }
+  __syncthreads();
+  insert_finish<NT>(S, F, t, tok, level, s_container, s_chain_from, s_add != 0, pt.key, pt.val, pt.src_slot);
+}
+
+// Inserts of one tree in order.  Consecutive level-1 points (tree height >=
+// 2) form runs of up to 8 whose parent searches run at once, one warp each:
+// a level-1 point's search reads only levels >= 2, which placing level-1
+// points never changes, so each parent equals the sequential one.  The point
+// that ends a run (level >= 2) has its search (levels >= level + 1 >= 3) on
+// the next warp, concurrently.  The run's points are then finished in
+// insertion order (membership, pages), then the ending point is placed --
+// exactly the sequential result.
+template <int NT, typename PointFn>
+__device__ void insert_points(SearchSmem& S, GroupSmem* GSA, const RingView& RG, const ForestView& F,
+                              const SearchScratch& SS, int t, double* dirs_tmp, int n, PointFn point,
+                              int32_t* out_levels) {
+  constexpr int NW = NT / 32;
+  static_assert(NW <= ICB_MAX_G, "one query slot per warp");
+  TreeMeta* m = F.meta + t;
+  WarpSearchBuf* WB = reinterpret_cast<WarpSearchBuf*>(RG.ring);   // the ring is idle during inserts
+  __shared__ int s_par[NW], s_ok[NW];
+  __shared__ unsigned long long s_ev[NW];
+  __shared__ InsertPoint s_pt[NW + 1];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int e = 0; e < n;) {
+    int nr = 0, single = -1;
+    while (e < n && nr < NW) {
+      const InsertPoint pt = point(e);
+      const int got = insert_prepare<NT>(S, F, t, pt.tok, pt.key, pt.given_level, nr);
+      if (tid == 0 && out_levels) out_levels[e] = got;
+      ++e;
+      if (got < 0) continue;
+      if (tid == 0) s_pt[nr] = pt;
+      if (got == 1 && m->levels >= 2) { ++nr; continue; }
+      single = got;
+      break;
+    }
+    __syncthreads();
+    const int L = m->levels;
+    const bool single_search = single > 0 && single < L;
+    const int nsearch = nr + (single_search ? 1 : 0);
+    if (warp < nsearch) {
+      int par = -1;
+      unsigned long long ev = 0;
+      const int target = warp < nr ? 2 : single + 1;
+      const bool ok = warp_parent_search(F, t, S.q[warp], S.qt[warp], target, WB[warp], &par, &ev);
+      if (lane == 0) { s_par[warp] = par; s_ok[warp] = ok; s_ev[warp] = ev; }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long ev = 0, qc = 0;
+      for (int w = 0; w < nsearch; ++w)
+        if (s_ok[w]) { ev += s_ev[w]; ++qc; }
+      if (qc) { atomicAdd(&m->query_count, qc); atomicAdd(&m->distance_evals, ev); }
+    }
+    for (int w = 0; w < nsearch; ++w) {
+      if (!s_ok[w]) {   // block-uniform; rare (a node the reference visits with P-DCI)
+        const int par = block_parent_search<NT>(S, GSA, RG, F, SS, t, w, w < nr ? 2 : single + 1, dirs_tmp);
+        if (tid == 0) s_par[w] = par;
+        __syncthreads();
+      }
+    }
+    for (int w = 0; w < nr; ++w) {
+      const int par = s_par[w];
+      const int container = par >= 0 ? F.own(t, par, 1) : m->top_node;
+      const InsertPoint pt = s_pt[w];
+      insert_finish<NT>(S, F, t, pt.tok, 1, container, 0, true, pt.key, pt.val, pt.src_slot);
+    }
+    if (single > 0) insert_place<NT>(S, F, t, s_pt[nr], single, single_search ? s_par[nr] : -1);
+  }
 }
 
 template <int NT>
@@ -282,11 +409,17 @@ __global__ void __launch_bounds__(NT, 512 / NT) insert_kernel(ForestView F, Inse
     __syncthreads();
     const int old = s_old;
     if (old < 0) return;
-    for (int e = 0; e < s_fill; ++e) {
-      int tok = F.page_tok[F.pg(t, old) * F.s + e];
-      const float* raw = F.lift + F.tk(t, tok) * ICB_ROWF;   // stashed raw key
-      insert_one<NT>(S, GSA, RG, F, SS, t, tok, raw, nullptr, (long long)(F.pg(t, old) * F.s + e), 0, dirs_tmp);
-    }
+    // the oldest window page's entries in slot order; raw keys were stashed in
+    // the tokens' lifted rows, K/V are copied from the page slot
+    insert_points<NT>(S, GSA, RG, F, SS, t, dirs_tmp, s_fill, [&](int e) {
+      InsertPoint p;
+      p.tok = F.page_tok[F.pg(t, old) * F.s + e];
+      p.key = F.lift + F.tk(t, p.tok) * ICB_ROWF;
+      p.val = nullptr;
+      p.src_slot = (long long)(F.pg(t, old) * F.s + e);
+      p.given_level = 0;
+      return p;
+    }, (int32_t*)nullptr);
     if (threadIdx.x == 0) {
       // release (pagestore.py:157-162) then a fresh window page
       F.page_role[F.pg(t, old)] = 0;
@@ -302,14 +435,16 @@ __global__ void __launch_bounds__(NT, 512 / NT) insert_kernel(ForestView F, Inse
     }
     return;
   }
-  for (int e = 0; e < A.m; ++e) {
-    size_t x = (size_t)b * A.m + e;
-    int tok = A.tokens[x];
-    int lv = A.levels ? A.levels[x] : 0;
-    int got = insert_one<NT>(S, GSA, RG, F, SS, t, tok, A.keys + x * F.dim, A.values ? A.values + x * F.dim_v : nullptr,
-                             -1, lv, dirs_tmp);
-    if (threadIdx.x == 0 && A.out_levels) A.out_levels[x] = got;
-  }
+  insert_points<NT>(S, GSA, RG, F, SS, t, dirs_tmp, A.m, [&](int e) {
+    const size_t x = (size_t)b * A.m + e;
+    InsertPoint p;
+    p.tok = A.tokens[x];
+    p.key = A.keys + x * F.dim;
+    p.val = A.values ? A.values + x * F.dim_v : nullptr;
+    p.src_slot = -1;
+    p.given_level = A.levels ? A.levels[x] : 0;
+    return p;
+  }, A.out_levels ? A.out_levels + (size_t)b * A.m : (int32_t*)nullptr);
 }
 
 // Append one decode token to the first non-full window page of each tree.

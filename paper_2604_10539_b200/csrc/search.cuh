@@ -95,7 +95,7 @@ __device__ inline SearchScratch slot_scratch(char* base, const SlotLayout& L, in
   return S;
 }
 
-struct SearchSmem {
+struct __align__(16) SearchSmem {   // q rows are read as float4
   float q[ICB_MAX_G][ICB_DPAD];
   float qt[ICB_MAX_G];
   double q64[ICB_DPAD + 1];
