@@ -33,7 +33,10 @@ struct InsertArgs {
   int from_window;         // 1: rotate the oldest window page
   int scalar_bytes;
   int64_t* stats;          // [n][2] offload bytes, transactions (may be null)
+  unsigned long long* prof;   // optional phase cycles (ICB_PROF): prepare, search, fallback, finish, segments
 };
+
+__device__ unsigned long long g_insert_prof[8];
 
 __device__ int new_node(const ForestView& F, int t, int level, int parent, int owner, int first_member) {
   TreeMeta* m = F.meta + t;
@@ -84,26 +87,55 @@ __device__ __forceinline__ void set_own(const ForestView& F, int t, int tok, int
   F.own_list[(size_t)t * F.own_cap + F.own_base[F.tk(t, tok)] + lv - 1] = node;
 }
 
-// Copy one entry into a page slot.  K/V come either from fp32 arrays or from
-// another page slot of the same forest (window rotation).
+// Copy one entry into a page slot (one warp; lane l owns dims 4l..4l+3).
+// K/V come either from fp32 arrays or from another page slot of the same
+// forest (window rotation).  Every source element is loaded before any store
+// so the copy costs one memory round trip.
 __device__ void write_slot(const ForestView& F, int t, int page, int slot, const float* kf, const float* vf,
                            long long src_slot) {
   const int lane = threadIdx.x & 31;
-  size_t dst = F.pg(t, page) * F.s + slot;
+  const int j0 = lane * 4;
+  const size_t dst = F.pg(t, page) * F.s + slot;
   if (F.kv_bf16) {
     __nv_bfloat16* K = (__nv_bfloat16*)F.page_k;
     __nv_bfloat16* V = (__nv_bfloat16*)F.page_v;
-    for (int j = lane; j < F.dim; j += 32)
-      K[dst * F.dkp + j] = src_slot >= 0 ? K[(size_t)src_slot * F.dkp + j] : __float2bfloat16_rn(kf[j]);
-    for (int j = lane; j < F.dim_v; j += 32)
-      V[dst * F.dvp + j] = src_slot >= 0 ? V[(size_t)src_slot * F.dvp + j]
-                                           : __float2bfloat16_rn(vf ? vf[j] : 0.f);
+    uint2 kw = make_uint2(0u, 0u), vw = make_uint2(0u, 0u);
+    if (src_slot >= 0) {
+      if (j0 < F.dkp) kw = *reinterpret_cast<const uint2*>(K + (size_t)src_slot * F.dkp + j0);
+      if (j0 < F.dvp) vw = *reinterpret_cast<const uint2*>(V + (size_t)src_slot * F.dvp + j0);
+    } else {
+      float k[4], v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        k[u] = j0 + u < F.dim ? kf[j0 + u] : 0.f;
+        v[u] = (vf && j0 + u < F.dim_v) ? vf[j0 + u] : 0.f;
+      }
+      __nv_bfloat162 k01 = __floats2bfloat162_rn(k[0], k[1]), k23 = __floats2bfloat162_rn(k[2], k[3]);
+      __nv_bfloat162 v01 = __floats2bfloat162_rn(v[0], v[1]), v23 = __floats2bfloat162_rn(v[2], v[3]);
+      kw = make_uint2(*reinterpret_cast<unsigned*>(&k01), *reinterpret_cast<unsigned*>(&k23));
+      vw = make_uint2(*reinterpret_cast<unsigned*>(&v01), *reinterpret_cast<unsigned*>(&v23));
+    }
+    if (j0 < F.dkp) *reinterpret_cast<uint2*>(K + dst * F.dkp + j0) = kw;
+    if (j0 < F.dvp) *reinterpret_cast<uint2*>(V + dst * F.dvp + j0) = vw;
   } else {
     float* K = (float*)F.page_k;
     float* V = (float*)F.page_v;
-    for (int j = lane; j < F.dim; j += 32) K[dst * F.dkp + j] = src_slot >= 0 ? K[(size_t)src_slot * F.dkp + j] : kf[j];
-    for (int j = lane; j < F.dim_v; j += 32)
-      V[dst * F.dvp + j] = src_slot >= 0 ? V[(size_t)src_slot * F.dvp + j] : (vf ? vf[j] : 0.f);
+    float4 kw = make_float4(0.f, 0.f, 0.f, 0.f), vw = kw;
+    if (src_slot >= 0) {
+      if (j0 < F.dkp) kw = *reinterpret_cast<const float4*>(K + (size_t)src_slot * F.dkp + j0);
+      if (j0 < F.dvp) vw = *reinterpret_cast<const float4*>(V + (size_t)src_slot * F.dvp + j0);
+    } else {
+      float k[4], v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        k[u] = j0 + u < F.dim ? kf[j0 + u] : 0.f;
+        v[u] = (vf && j0 + u < F.dim_v) ? vf[j0 + u] : 0.f;
+      }
+      kw = make_float4(k[0], k[1], k[2], k[3]);
+      vw = make_float4(v[0], v[1], v[2], v[3]);
+    }
+    if (j0 < F.dkp) *reinterpret_cast<float4*>(K + dst * F.dkp + j0) = kw;
+    if (j0 < F.dvp) *reinterpret_cast<float4*>(V + dst * F.dvp + j0) = vw;
   }
 }
 
@@ -208,6 +240,43 @@ __device__ __forceinline__ int block_parent_search(SearchSmem& S, GroupSmem* GSA
   return s_parent;
 }
 
+// Membership, own chain and page placement of one point (ONE thread);
+// returns the page (-1 on capacity error) and its slot in *slot.
+__device__ int finish_book(const ForestView& F, int t, int tok, int level, int container, int chain_from,
+                           bool add_to_container, int* slot_out) {
+  TreeMeta* m = F.meta + t;
+  note_point_level(F, t, tok, level);
+  if (add_to_container) add_member(F, t, container, tok);
+  int parent_node = container;   // node holding tok at chain_from + 1
+  for (int lv = chain_from; lv >= 1; --lv) {
+    int nn = new_node(F, t, lv, parent_node, tok, tok);
+    set_own(F, t, tok, lv, nn);
+    parent_node = nn;
+  }
+  int leaf = level >= 2 ? F.own(t, tok, 1) : container;
+  size_t lx = F.nd(t, leaf);
+  int page = F.node_lastpage[lx];
+  if (page < 0 || F.page_fill[F.pg(t, page)] >= F.s) {
+    page = m->next_page;
+    if (page >= F.page_cap) { set_err(m, ICB_ERR_CAP_PAGES); page = -1; }
+    else {
+      m->next_page = page + 1;
+      F.page_fill[F.pg(t, page)] = 0;
+      F.page_role[F.pg(t, page)] = ICB_ROLE_INDEXED;
+      F.node_lastpage[lx] = page;
+    }
+  }
+  if (page >= 0) {
+    int slot = F.page_fill[F.pg(t, page)];
+    F.page_tok[F.pg(t, page) * F.s + slot] = tok;
+    F.page_fill[F.pg(t, page)] = slot + 1;
+    F.tok2page[F.tk(t, tok)] = page;
+    *slot_out = slot;
+  }
+  m->n_points += 1;
+  return page;
+}
+
 template <int NT>
 __device__ void insert_finish(SearchSmem& S, const ForestView& F, int t, int tok, int level, int container,
                               int chain_from, bool add_to_container, const float* key, const float* val,
@@ -216,40 +285,14 @@ __device__ void insert_finish(SearchSmem& S, const ForestView& F, int t, int tok
   __shared__ int s_leaf;
   const int tid = threadIdx.x;
   if (tid == 0) {
-    note_point_level(F, t, tok, level);
-    if (add_to_container) add_member(F, t, container, tok);
-    int parent_node = container;   // node holding tok at chain_from + 1
-    for (int lv = chain_from; lv >= 1; --lv) {
-      int nn = new_node(F, t, lv, parent_node, tok, tok);
-      set_own(F, t, tok, lv, nn);
-      parent_node = nn;
-    }
-    int leaf = level >= 2 ? F.own(t, tok, 1) : container;
-    size_t lx = F.nd(t, leaf);
-    int page = F.node_lastpage[lx];
-    if (page < 0 || F.page_fill[F.pg(t, page)] >= F.s) {
-      page = m->next_page;
-      if (page >= F.page_cap) { set_err(m, ICB_ERR_CAP_PAGES); page = -1; }
-      else {
-        m->next_page = page + 1;
-        F.page_fill[F.pg(t, page)] = 0;
-        F.page_role[F.pg(t, page)] = ICB_ROLE_INDEXED;
-        F.node_lastpage[lx] = page;
-      }
-    }
-    s_leaf = page;
-    if (page >= 0) {
-      int slot = F.page_fill[F.pg(t, page)];
-      F.page_tok[F.pg(t, page) * F.s + slot] = tok;
-      F.page_fill[F.pg(t, page)] = slot + 1;
-      F.tok2page[F.tk(t, tok)] = page;
-      S.misc[4] = slot;
-    }
-    m->n_points += 1;
+    int slot = 0;
+    s_leaf = finish_book(F, t, tok, level, container, chain_from, add_to_container, &slot);
+    S.misc[4] = slot;
   }
   __syncthreads();
   if (s_leaf >= 0 && tid < 32) write_slot(F, t, s_leaf, S.misc[4], key, val, src_slot);
   __syncthreads();
+  (void)m;
 }
 
 struct InsertPoint {
@@ -324,15 +367,23 @@ __device__ void insert_place(SearchSmem& S, const ForestView& F, int t, const In
 template <int NT, typename PointFn>
 __device__ void insert_points(SearchSmem& S, GroupSmem* GSA, const RingView& RG, const ForestView& F,
                               const SearchScratch& SS, int t, double* dirs_tmp, int n, PointFn point,
-                              int32_t* out_levels) {
+                              int32_t* out_levels, unsigned long long* prof) {
   constexpr int NW = NT / 32;
   static_assert(NW <= ICB_MAX_G, "one query slot per warp");
   TreeMeta* m = F.meta + t;
   WarpSearchBuf* WB = reinterpret_cast<WarpSearchBuf*>(RG.ring);   // the ring is idle during inserts
-  __shared__ int s_par[NW], s_ok[NW];
+  __shared__ int s_par[NW], s_ok[NW], s_wpage[NW], s_wslot[NW];
   __shared__ unsigned long long s_ev[NW];
   __shared__ InsertPoint s_pt[NW + 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  long long tp = clock64();
+  auto mark = [&](int k) {
+    if (prof && tid == 0) {
+      const long long now = clock64();
+      atomicAdd(prof + k, (unsigned long long)(now - tp));
+      tp = now;
+    }
+  };
   for (int e = 0; e < n;) {
     int nr = 0, single = -1;
     while (e < n && nr < NW) {
@@ -347,6 +398,8 @@ __device__ void insert_points(SearchSmem& S, GroupSmem* GSA, const RingView& RG,
       break;
     }
     __syncthreads();
+    mark(0);
+    if (prof && tid == 0) atomicAdd(prof + 4, 1ull);
     const int L = m->levels;
     const bool single_search = single > 0 && single < L;
     const int nsearch = nr + (single_search ? 1 : 0);
@@ -358,6 +411,7 @@ __device__ void insert_points(SearchSmem& S, GroupSmem* GSA, const RingView& RG,
       if (lane == 0) { s_par[warp] = par; s_ok[warp] = ok; s_ev[warp] = ev; }
     }
     __syncthreads();
+    mark(1);
     if (tid == 0) {
       unsigned long long ev = 0, qc = 0;
       for (int w = 0; w < nsearch; ++w)
@@ -371,13 +425,23 @@ __device__ void insert_points(SearchSmem& S, GroupSmem* GSA, const RingView& RG,
         __syncthreads();
       }
     }
-    for (int w = 0; w < nr; ++w) {
-      const int par = s_par[w];
-      const int container = par >= 0 ? F.own(t, par, 1) : m->top_node;
-      const InsertPoint pt = s_pt[w];
-      insert_finish<NT>(S, F, t, pt.tok, 1, container, 0, true, pt.key, pt.val, pt.src_slot);
-    }
+    mark(2);
+    // the run's bookkeeping in insertion order (one thread, no barriers),
+    // then its K/V slot writes in parallel (one warp per point)
+    if (tid == 0)
+      for (int w = 0; w < nr; ++w) {
+        const int par = s_par[w];
+        const int container = par >= 0 ? F.own(t, par, 1) : m->top_node;
+        int slot = 0;
+        s_wpage[w] = finish_book(F, t, s_pt[w].tok, 1, container, 0, true, &slot);
+        s_wslot[w] = slot;
+      }
+    __syncthreads();
+    if (warp < nr && s_wpage[warp] >= 0)
+      write_slot(F, t, s_wpage[warp], s_wslot[warp], s_pt[warp].key, s_pt[warp].val, s_pt[warp].src_slot);
+    __syncthreads();
     if (single > 0) insert_place<NT>(S, F, t, s_pt[nr], single, single_search ? s_par[nr] : -1);
+    mark(3);
   }
 }
 
@@ -419,7 +483,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) insert_kernel(ForestView F, Inse
       p.src_slot = (long long)(F.pg(t, old) * F.s + e);
       p.given_level = 0;
       return p;
-    }, (int32_t*)nullptr);
+    }, (int32_t*)nullptr, A.prof);
     if (threadIdx.x == 0) {
       // release (pagestore.py:157-162) then a fresh window page
       F.page_role[F.pg(t, old)] = 0;
@@ -444,7 +508,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) insert_kernel(ForestView F, Inse
     p.src_slot = -1;
     p.given_level = A.levels ? A.levels[x] : 0;
     return p;
-  }, A.out_levels ? A.out_levels + (size_t)b * A.m : (int32_t*)nullptr);
+  }, A.out_levels ? A.out_levels + (size_t)b * A.m : (int32_t*)nullptr, A.prof);
 }
 
 // Append one decode token to the first non-full window page of each tree.
@@ -546,6 +610,8 @@ int icb_insert_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t m, c
   A.trees = trees; A.n = n; A.m = m; A.tokens = tokens; A.keys = keys; A.values = values;
   A.levels = levels; A.out_levels = out_levels; A.from_window = from_window;
   A.scalar_bytes = scalar_bytes; A.stats = stats;
+  A.prof = nullptr;
+  if (getenv("ICB_PROF")) ICB_CUDA(cudaGetSymbolAddress((void**)&A.prof, g_insert_prof));
   ICB_CUDA(cudaFuncSetAttribute(insert_kernel<kSearchThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)search_dsm_bytes(1)));
   insert_kernel<kSearchThreads><<<n, kSearchThreads, search_dsm_bytes(1), st>>>(f->view, A, scratch, L);
@@ -567,5 +633,17 @@ int icb_resident_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t ro
   if (n <= 0) return ICB_OK;
   resident_pages_kernel<<<n, 256, 0, st>>>(f->view, trees, n, role, count, n_tokens, tokens, keys, values);
   ICB_CUDA(cudaGetLastError());
+  return ICB_OK;
+}
+
+// Insert phase cycle counters (enabled by ICB_PROF=1): prepare, warp
+// searches, block fallbacks, finish/place, segments.
+extern "C" int icb_insert_profile(unsigned long long* out, int reset) {
+  ICB_CUDA(cudaDeviceSynchronize());
+  ICB_CUDA(cudaMemcpyFromSymbol(out, g_insert_prof, sizeof(unsigned long long) * 8));
+  if (reset) {
+    unsigned long long z[8] = {};
+    ICB_CUDA(cudaMemcpyToSymbol(g_insert_prof, z, sizeof(z)));
+  }
   return ICB_OK;
 }

@@ -81,29 +81,39 @@ __device__ bool warp_parent_search(const ForestView& F, int t, const float* q, f
     }
     __syncwarp();
     ev += (unsigned long long)M;
-    // distances, 8 rows per batch: in slot jj lane l scores row jj ^ pi(l)
-    for (int b0 = 0; b0 < M; b0 += 8) {
-      // the tail of this lane's output row is loaded with the rows (one round trip)
-      const int cm = b0 + pi;
-      const int idm = W.ids[cm < M ? cm : b0];
-      const float tl = F.tail[F.tk(t, idm)];
-      float4 p[8];
+    // distances, two 8-row batches per round trip: in slot jj of a batch lane
+    // l scores row jj ^ pi(l); each lane's output-row tail is loaded with the rows
+    for (int b0 = 0; b0 < M; b0 += 16) {
+      int idm[2];
+      float tl[2];
+      float4 p[2][8];
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {
-        const int c = b0 + (jj ^ pi);
-        p[jj] = reinterpret_cast<const float4*>(F.row(t, W.ids[c < M ? c : b0]))[lane];
+      for (int h = 0; h < 2; ++h) {
+        const int bb = b0 + 8 * h;
+        const int cm = bb + pi;
+        idm[h] = W.ids[cm < M ? cm : b0];
+        tl[h] = F.tail[F.tk(t, idm[h])];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const int c = bb + (jj ^ pi);
+          p[h][jj] = reinterpret_cast<const float4*>(F.row(t, W.ids[c < M ? c : b0]))[lane];
+        }
       }
-      float v[8];
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) v[jj] = lane_sq4(p[jj], qv);
+      for (int h = 0; h < 2; ++h) {
+        float v[8];
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) v[jj] = __fadd_rn(v[jj], __shfl_xor_sync(0xffffffffu, v[jj + 4], 16));
+        for (int jj = 0; jj < 8; ++jj) v[jj] = lane_sq4(p[h][jj], qv);
 #pragma unroll
-      for (int jj = 0; jj < 2; ++jj) v[jj] = __fadd_rn(v[jj], __shfl_xor_sync(0xffffffffu, v[jj + 2], 8));
-      float f = __fadd_rn(v[0], __shfl_xor_sync(0xffffffffu, v[1], 4));
-      f = __fadd_rn(f, __shfl_xor_sync(0xffffffffu, f, 2));
-      f = __fadd_rn(f, __shfl_xor_sync(0xffffffffu, f, 1));
-      if ((lane & 3) == 0 && cm < M) W.keys[cm] = make_key(d2_finish(f, tl, qt), idm);
+        for (int jj = 0; jj < 4; ++jj) v[jj] = __fadd_rn(v[jj], __shfl_xor_sync(0xffffffffu, v[jj + 4], 16));
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) v[jj] = __fadd_rn(v[jj], __shfl_xor_sync(0xffffffffu, v[jj + 2], 8));
+        float f = __fadd_rn(v[0], __shfl_xor_sync(0xffffffffu, v[1], 4));
+        f = __fadd_rn(f, __shfl_xor_sync(0xffffffffu, f, 2));
+        f = __fadd_rn(f, __shfl_xor_sync(0xffffffffu, f, 1));
+        const int cm = b0 + 8 * h + pi;
+        if ((lane & 3) == 0 && cm < M) W.keys[cm] = make_key(d2_finish(f, tl[h], qt), idm[h]);
+      }
     }
     __syncwarp();
     // top-B by B rounds of warp argmin over the unique keys

@@ -38,3 +38,15 @@ ms = [a.elapsed_time(b) for a, b in times]
 print("rotations", len(ms), "ms each", [round(x, 3) for x in ms])
 print("mean rotation ms %.3f  -> %.1f us per decode step amortized" % (sum(ms[1:]) / max(1, len(ms) - 1),
                                                                     1e3 * sum(ms[1:]) / max(1, len(ms) - 1) / 16))
+
+if os.environ.get("ICB_PROF"):
+    import ctypes
+    import numpy as np
+    from paper_2604_10539_b200 import _native as N
+    lib = N.lib()
+    lib.icb_insert_profile.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    buf = np.zeros(8, dtype=np.uint64)
+    lib.icb_insert_profile(buf.ctypes.data_as(ctypes.c_void_p), 0)
+    nrot = len(ms) * eng.T
+    print("per tree-rotation us: prepare %.1f search %.1f fallback %.1f finish %.1f | segments %.2f" % (
+        *(buf[i] / nrot / 1.9e3 for i in range(4)), buf[4] / nrot))
