@@ -83,11 +83,32 @@ __device__ __forceinline__ float head_sums(const float (&v)[G], int lane) {
   return head_sums_rest<G, 16>(v, lane);
 }
 
+// Raw row chunks: 4 dims per lane, loaded for a whole chunk of rows before
+// any of them is used (one memory round trip per chunk).
+template <typename KT>
+struct Raw4;
+template <>
+struct Raw4<float> {
+  using T = float4;
+  static __device__ __forceinline__ T load(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+  static __device__ __forceinline__ float4 cvt(T r) { return r; }
+  static __device__ __forceinline__ T zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+};
+template <>
+struct Raw4<__nv_bfloat16> {
+  using T = uint2;
+  static __device__ __forceinline__ T load(const __nv_bfloat16* p) { return __ldg(reinterpret_cast<const uint2*>(p)); }
+  static __device__ __forceinline__ float4 cvt(T u) {
+    float2 a = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.x));
+    float2 b = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.y));
+    return make_float4(a.x, a.y, b.x, b.y);
+  }
+  static __device__ __forceinline__ T zero() { return make_uint2(0u, 0u); }
+};
+
 template <typename KT, int G>
-__device__ __forceinline__ void attend_row(HeadAcc (&h)[G], const float4 (&qv)[G], const KT* krow, const KT* vrow,
-                                           int lane, int dim, int dim_v, float scale_log2) {
-  float4 k = lane * 4 < dim ? load4<KT>(krow + lane * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
-  float4 v = lane * 4 < dim_v ? load4<KT>(vrow + lane * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+__device__ __forceinline__ void attend_vals(HeadAcc (&h)[G], const float4 (&qv)[G], float4 k, float4 v, int lane,
+                                            float scale_log2) {
   float s[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) s[g] = qv[g].x * k.x + qv[g].y * k.y + qv[g].z * k.z + qv[g].w * k.w;
@@ -121,10 +142,126 @@ __device__ __forceinline__ void attend_row(HeadAcc (&h)[G], const float4 (&qv)[G
   }
 }
 
+template <typename KT, int G>
+__device__ __forceinline__ void attend_row(HeadAcc (&h)[G], const float4 (&qv)[G], const KT* krow, const KT* vrow,
+                                           int lane, int dim, int dim_v, float scale_log2) {
+  float4 k = lane * 4 < dim ? load4<KT>(krow + lane * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 v = lane * 4 < dim_v ? load4<KT>(vrow + lane * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  attend_vals<KT, G>(h, qv, k, v, lane, scale_log2);
+}
+
+// A chunk of CH rows starting at row index `r0` of a [rows][ld] K/V pair:
+// all loads first, then the rows' online-softmax updates in order.
+template <typename KT, int G, int CH>
+__device__ __forceinline__ void attend_chunk(HeadAcc (&h)[G], const float4 (&qv)[G], const KT* K, const KT* V,
+                                             size_t r0, int nrow, int ldk, int ldv, int lane, int dim, int dim_v,
+                                             float scale_log2) {
+  using R = Raw4<KT>;
+  typename R::T kr[CH], vr[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    kr[c] = (c < nrow && lane * 4 < dim) ? R::load(K + (r0 + c) * ldk + lane * 4) : R::zero();
+    vr[c] = (c < nrow && lane * 4 < dim_v) ? R::load(V + (r0 + c) * ldv + lane * 4) : R::zero();
+  }
+#pragma unroll
+  for (int c = 0; c < CH; ++c)
+    if (c < nrow) attend_vals<KT, G>(h, qv, R::cvt(kr[c]), R::cvt(vr[c]), lane, scale_log2);
+}
+
+// G = 4: a chunk of 8 rows at once.  Scores: lane l computes, in slot jj,
+// the partial dots of row jj ^ pi(l) (pi = lane bits 4..2) against the two
+// head pairs (f32x2), and a transposed reduction (select-free at the row
+// levels xor 16/8/4, splitting the pairs at xor 2/1) leaves lane l with the
+// score of (row pi(l), head l & 3).  Softmax: one chunk max per head (xor
+// 4/8/16), one exp2 per lane, the heads' rescale factors broadcast from lanes
+// 0..3; P.V: each lane accumulates its 4 dims of every head from the 32
+// broadcast probabilities.  Every lane keeps m and l of its own head.
+struct G4State {
+  float m, l;          // of head (lane & 3)
+  float4 acc[4];       // dims 4l..4l+3 of every head
+};
+
+template <typename KT>
+__device__ __forceinline__ void attend_chunk8_g4(G4State& st, const unsigned long long (&q2)[2][4], const KT* K,
+                                                 const KT* V, size_t r0, int nrow, int ldk, int ldv, int lane,
+                                                 int dim, int dim_v, float scale_log2) {
+  using R = Raw4<KT>;
+  const int pi = (lane >> 2) & 7;
+  typename R::T kr[8], vr[8];
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) {
+    const int rk = jj ^ pi;
+    kr[jj] = (rk < nrow && lane * 4 < dim) ? R::load(K + (r0 + rk) * ldk + lane * 4) : R::zero();
+    vr[jj] = (jj < nrow && lane * 4 < dim_v) ? R::load(V + (r0 + jj) * ldv + lane * 4) : R::zero();
+  }
+  unsigned long long v2[8][2];
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) {
+    const float4 k = R::cvt(kr[jj]);
+#pragma unroll
+    for (int hp = 0; hp < 2; ++hp) {
+      unsigned long long a;
+      const unsigned long long kx = pack_f2(k.x, k.x), ky = pack_f2(k.y, k.y);
+      const unsigned long long kz = pack_f2(k.z, k.z), kw = pack_f2(k.w, k.w);
+      asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(a) : "l"(kx), "l"(q2[hp][0]));
+      asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a) : "l"(ky), "l"(q2[hp][1]));
+      asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a) : "l"(kz), "l"(q2[hp][2]));
+      asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a) : "l"(kw), "l"(q2[hp][3]));
+      v2[jj][hp] = a;
+    }
+  }
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+    for (int hp = 0; hp < 2; ++hp) v2[jj][hp] = fadd2(v2[jj][hp], shfl_xor_u64(v2[jj + 4][hp], 16));
+#pragma unroll
+  for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+    for (int hp = 0; hp < 2; ++hp) v2[jj][hp] = fadd2(v2[jj][hp], shfl_xor_u64(v2[jj + 2][hp], 8));
+#pragma unroll
+  for (int hp = 0; hp < 2; ++hp) v2[0][hp] = fadd2(v2[0][hp], shfl_xor_u64(v2[1][hp], 4));
+  const bool b1 = lane & 2, b0 = lane & 1;
+  const unsigned long long w = fadd2(b1 ? v2[0][1] : v2[0][0], shfl_xor_u64(b1 ? v2[0][0] : v2[0][1], 2));
+  const float wl = __uint_as_float((unsigned)w), wh = __uint_as_float((unsigned)(w >> 32));
+  const float dot = (b0 ? wh : wl) + __shfl_xor_sync(0xffffffffu, b0 ? wl : wh, 1);
+  const float x = pi < nrow ? dot * scale_log2 : -INFINITY;
+  // chunk max of this lane's head (lanes sharing lane & 3)
+  float cm = x;
+  cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 4));
+  cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 8));
+  cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 16));
+  const float mn = fmaxf(st.m, cm);
+  const float alpha = exp2f(st.m - mn);   // 0 on the first chunk (m = -inf)
+  const float p = exp2f(x - mn);          // 0 for masked rows
+  float ps = p;
+  ps += __shfl_xor_sync(0xffffffffu, ps, 4);
+  ps += __shfl_xor_sync(0xffffffffu, ps, 8);
+  ps += __shfl_xor_sync(0xffffffffu, ps, 16);
+  st.l = st.l * alpha + ps;
+  st.m = mn;
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const float a = __shfl_sync(0xffffffffu, alpha, h);
+    st.acc[h].x *= a; st.acc[h].y *= a; st.acc[h].z *= a; st.acc[h].w *= a;
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const float4 v = R::cvt(vr[r]);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const float pr = __shfl_sync(0xffffffffu, p, 4 * r + h);
+      st.acc[h].x = fmaf(pr, v.x, st.acc[h].x);
+      st.acc[h].y = fmaf(pr, v.y, st.acc[h].y);
+      st.acc[h].z = fmaf(pr, v.z, st.acc[h].z);
+      st.acc[h].w = fmaf(pr, v.w, st.acc[h].w);
+    }
+  }
+}
+
 // Block = (tree b, split sp).  PAGED: rows come from the tree's sink, window
 // and selected pages; DENSE: rows [0, n_tokens) of k/v[b].
 template <typename KT, int G, bool PAGED>
-__global__ void __launch_bounds__(kAttnThreads) attn_kernel(ForestView F, AttnArgs A) {
+__global__ void __launch_bounds__(kAttnThreads, 2) attn_kernel(ForestView F, AttnArgs A) {
   const int b = blockIdx.x, sp = blockIdx.y, S = A.splits;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = kAttnThreads / 32;
   __shared__ int s_pages[1024];
@@ -146,6 +283,20 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(ForestView F, AttnAr
   HeadAcc h[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) { h[g].m = -INFINITY; h[g].l = 0.f; h[g].acc = make_float4(0.f, 0.f, 0.f, 0.f); }
+  G4State g4;   // G == 4 path (merged into h[] before the warp combine)
+  unsigned long long q2[2][4];
+  if constexpr (G == 4) {
+    g4.m = -INFINITY; g4.l = 0.f;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) g4.acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int hp = 0; hp < 2; ++hp) {
+      q2[hp][0] = pack_f2(qv[2 * hp].x, qv[2 * hp + 1].x);
+      q2[hp][1] = pack_f2(qv[2 * hp].y, qv[2 * hp + 1].y);
+      q2[hp][2] = pack_f2(qv[2 * hp].z, qv[2 * hp + 1].z);
+      q2[hp][3] = pack_f2(qv[2 * hp].w, qv[2 * hp + 1].w);
+    }
+  }
 
   if (PAGED) {
     // page list: sink, window, selected (entry order of engine.py:457-461)
@@ -166,13 +317,21 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(ForestView F, AttnAr
     __syncthreads();
     const KT* K = (const KT*)F.page_k;
     const KT* V = (const KT*)F.page_v;
+    // rows per chunk, loaded together (register budget: 2 CTAs / SM)
+    constexpr int CH = (sizeof(KT) == 2 ? 16 : 8) / (G >= 4 ? 2 : 1) / (G >= 8 ? 2 : 1);
     for (int i = warp; i < s_np; i += NW) {
       const int p = s_pages[i];
       const int fill = F.page_fill[F.pg(t, p)];
       const size_t base = F.pg(t, p) * F.s;
-      for (int r = 0; r < fill; ++r)
-        attend_row<KT, G>(h, qv, K + (base + r) * F.dkp, V + (base + r) * F.dvp, lane, A.dim, A.dim_v,
-                          A.scale_log2);
+      if constexpr (G == 4) {
+        for (int r0 = 0; r0 < fill; r0 += 8)
+          attend_chunk8_g4<KT>(g4, q2, K, V, base + r0, min(8, fill - r0), F.dkp, F.dvp, lane, A.dim, A.dim_v,
+                               A.scale_log2);
+      } else {
+        for (int r0 = 0; r0 < fill; r0 += CH)
+          attend_chunk<KT, G, CH>(h, qv, K, V, base + r0, min(CH, fill - r0), F.dkp, F.dvp, lane, A.dim, A.dim_v,
+                                  A.scale_log2);
+      }
     }
     // residency accounting (pagestore.py:169-215) by split 0
     if (sp == 0 && A.stats) {
@@ -210,13 +369,22 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(ForestView F, AttnAr
     const KT* K = (const KT*)A.k + (size_t)b * A.ld * A.dim;
     const KT* V = (const KT*)A.v + (size_t)b * A.ld * A.dim_v;
     const int r0 = (int)((long long)A.n_tokens * sp / S), r1 = (int)((long long)A.n_tokens * (sp + 1) / S);
-    const int CH = 4;
+    constexpr int CH = G == 4 ? 8 : (sizeof(KT) == 2 ? 16 : 8) / (G >= 4 ? 2 : 1) / (G >= 8 ? 2 : 1);
     for (int r = r0 + warp * CH; r < r1; r += NW * CH) {
+      if constexpr (G == 4)
+        attend_chunk8_g4<KT>(g4, q2, K, V, (size_t)r, min(CH, r1 - r), A.dim, A.dim_v, lane, A.dim, A.dim_v,
+                             A.scale_log2);
+      else
+        attend_chunk<KT, G, CH>(h, qv, K, V, (size_t)r, min(CH, r1 - r), A.dim, A.dim_v, lane, A.dim, A.dim_v,
+                                A.scale_log2);
+    }
+  }
+  if constexpr (G == 4) {
 #pragma unroll
-      for (int u = 0; u < CH; ++u)
-        if (r + u < r1)
-          attend_row<KT, G>(h, qv, K + (size_t)(r + u) * A.dim, V + (size_t)(r + u) * A.dim_v, lane, A.dim,
-                            A.dim_v, A.scale_log2);
+    for (int g = 0; g < 4; ++g) {
+      h[g].m = __shfl_sync(0xffffffffu, g4.m, g);
+      h[g].l = __shfl_sync(0xffffffffu, g4.l, g);
+      h[g].acc = g4.acc[g];
     }
   }
   // combine warps
@@ -313,7 +481,9 @@ int icb_attention_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t G
   if (n <= 0) return ICB_OK;
   if (!valid_g(G)) { icb_set_error(ICB_E_CONFIG, "attention supports 1 <= G <= 8"); return ICB_E_CONFIG; }
   const auto& c = f->cfg;
-  if (splits <= 0) splits = std::max(1, std::min(8, (2 * 148 + n - 1) / n));
+  // one wave: at most 2 CTAs per SM (the kernel's register budget); each warp
+  // keeps a whole row chunk in flight, so one split per tree already streams
+  if (splits <= 0) splits = std::max(1, std::min(8, (2 * 148) / n));
   AttnArgs A{};
   A.n = n; A.G = G; A.dim = c.dim; A.dim_v = c.dim_v; A.splits = splits; A.trees = trees; A.q = queries;
   A.pages = pages; A.pages_cap = pages_cap; A.npages = npages; A.out = out; A.stats = stats;
@@ -333,7 +503,7 @@ int icb_dense_attention_impl(int32_t n, int32_t G, int32_t dim, int32_t dim_v, i
                              int32_t splits, cudaStream_t st) {
   if (n <= 0) return ICB_OK;
   if (!valid_g(G)) { icb_set_error(ICB_E_CONFIG, "attention supports 1 <= G <= 8"); return ICB_E_CONFIG; }
-  if (splits <= 0) splits = std::max(1, std::min((n_tokens + 255) / 256, (4 * 148 + n - 1) / n));
+  if (splits <= 0) splits = std::max(1, std::min((n_tokens + 255) / 256, (2 * 148) / n));   // one wave
   AttnArgs A{};
   A.n = n; A.G = G; A.dim = dim; A.dim_v = dim_v; A.splits = splits; A.q = q; A.k = k; A.v = v; A.ld = ld;
   A.n_tokens = n_tokens; A.out = out;
