@@ -142,6 +142,22 @@ int icb_dense_attention(int32_t n, int32_t G, int32_t dim, int32_t dim_v, int32_
                         const float *q, const void *k, const void *v, int64_t ld,
                         int32_t n_tokens, float *out, int32_t splits, void *stream);
 
+/* CUDA-graph variants: the decode position is read from device memory
+ * (token_dev[0] = the token being decoded), so one captured decode step
+ * replays for every position.  icb_append_window_dev is icb_append_window
+ * (engine.py:425-428); icb_dense_attention_dev attends rows
+ * [0, token_dev[0] + 1) (engine.py:418-422); icb_dense_append writes the
+ * step's K/V row of each skip-layer plane at row token_dev[0] (the K/V
+ * mirror append, engine.py:414-416). */
+int icb_append_window_dev(icb_forest *f, const int32_t *trees, int32_t n, const int32_t *token_dev,
+                          const float *keys, const float *values, void *stream);
+int icb_dense_attention_dev(int32_t n, int32_t G, int32_t dim, int32_t dim_v, int32_t kv_dtype,
+                            const float *q, const void *k, const void *v, int64_t ld,
+                            const int32_t *token_dev, float *out, int32_t splits, void *stream);
+int icb_dense_append(int32_t n, int32_t dim, int32_t dim_v, int32_t kv_dtype, const float *k,
+                     const float *v, void *dense_k, void *dense_v, int64_t ld,
+                     const int32_t *token_dev, void *stream);
+
 /* Per-tree summary (host out[16]): levels, top_node, n_nodes, next_page,
  * n_points, err, n_window, n_sink, query_count, distance_evals, scale_clamps,
  * member_top, own_top, n_dirs, 0, 0.  Synchronizes the device. */

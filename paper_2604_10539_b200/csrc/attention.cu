@@ -43,6 +43,7 @@ struct AttnArgs {
   const void* v;
   long long ld;
   int n_tokens;
+  const int32_t* token_dev;    // dense mode: rows [0, *token_dev + 1) when set (CUDA-graph replays)
   float* out;                  // [n][G][dim_v]
   float* part;                 // [n][splits][G][2 + dim_v]
   unsigned* counter;           // [n]
@@ -368,7 +369,8 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attn_kernel(ForestView F, Att
   } else {
     const KT* K = (const KT*)A.k + (size_t)b * A.ld * A.dim;
     const KT* V = (const KT*)A.v + (size_t)b * A.ld * A.dim_v;
-    const int r0 = (int)((long long)A.n_tokens * sp / S), r1 = (int)((long long)A.n_tokens * (sp + 1) / S);
+    const int ntok = A.token_dev ? *A.token_dev + 1 : A.n_tokens;
+    const int r0 = (int)((long long)ntok * sp / S), r1 = (int)((long long)ntok * (sp + 1) / S);
     constexpr int CH = G == 4 ? 8 : (sizeof(KT) == 2 ? 16 : 8) / (G >= 4 ? 2 : 1) / (G >= 8 ? 2 : 1);
     for (int r = r0 + warp * CH; r < r1; r += NW * CH) {
       if constexpr (G == 4)
@@ -499,14 +501,15 @@ int icb_attention_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t G
 }
 
 int icb_dense_attention_impl(int32_t n, int32_t G, int32_t dim, int32_t dim_v, int32_t kv_dtype, const float* q,
-                             const void* k, const void* v, int64_t ld, int32_t n_tokens, float* out,
+                             const void* k, const void* v, int64_t ld, int32_t n_tokens, const int32_t* token_dev,
+                             float* out,
                              int32_t splits, cudaStream_t st) {
   if (n <= 0) return ICB_OK;
   if (!valid_g(G)) { icb_set_error(ICB_E_CONFIG, "attention supports 1 <= G <= 8"); return ICB_E_CONFIG; }
   if (splits <= 0) splits = std::max(1, std::min((n_tokens + 255) / 256, (2 * 148) / n));   // one wave
   AttnArgs A{};
   A.n = n; A.G = G; A.dim = dim; A.dim_v = dim_v; A.splits = splits; A.q = q; A.k = k; A.v = v; A.ld = ld;
-  A.n_tokens = n_tokens; A.out = out;
+  A.n_tokens = n_tokens; A.token_dev = token_dev; A.out = out;
   A.scale_log2 = (float)(1.4426950408889634 / sqrt((double)dim));
   int rc = ensure_attn_scratch(nullptr, (size_t)n * splits * padded_g(G) * (2 + dim_v), n, &A.part, &A.counter);
   if (rc) return rc;
@@ -514,6 +517,36 @@ int icb_dense_attention_impl(int32_t n, int32_t G, int32_t dim, int32_t dim_v, i
   dim3 grid(n, splits);
   if (kv_dtype == ICB_KV_BF16) launch_attn<__nv_bfloat16, false>(G, grid, st, F, A);
   else launch_attn<float, false>(G, grid, st, F, A);
+  ICB_CUDA(cudaGetLastError());
+  return ICB_OK;
+}
+
+namespace icb {
+// Append one row to each of n dense K/V planes ([n][ld][dkp] / [n][ld][dvp],
+// fp32 or bf16) at the device position *token_dev (the skip layers' cache).
+__global__ void dense_append_kernel(int n, int dim, int dim_v, int bf16, const float* k, const float* v, void* dk,
+                                    void* dv, long long ld, const int32_t* token_dev) {
+  const int b = blockIdx.x;
+  const int tok = *token_dev;
+  if (tok < 0 || tok >= ld) return;
+  const int dkp = (dim + 3) & ~3, dvp = (dim_v + 3) & ~3;
+  for (int j = threadIdx.x; j < dkp + dvp; j += blockDim.x) {
+    const bool isk = j < dkp;
+    const int c = isk ? j : j - dkp;
+    const int lim = isk ? dim : dim_v;
+    const float x = c < lim ? (isk ? k[(size_t)b * dim + c] : v[(size_t)b * dim_v + c]) : 0.f;
+    const size_t o = ((size_t)b * ld + tok) * (isk ? dkp : dvp) + c;
+    if (bf16) (isk ? (__nv_bfloat16*)dk : (__nv_bfloat16*)dv)[o] = __float2bfloat16_rn(x);
+    else (isk ? (float*)dk : (float*)dv)[o] = x;
+  }
+}
+}  // namespace icb
+
+int icb_dense_append_impl(int32_t n, int32_t dim, int32_t dim_v, int32_t kv_dtype, const float* k, const float* v,
+                          void* dense_k, void* dense_v, int64_t ld, const int32_t* token_dev, cudaStream_t st) {
+  if (n <= 0) return ICB_OK;
+  icb::dense_append_kernel<<<n, 128, 0, st>>>(n, dim, dim_v, kv_dtype == ICB_KV_BF16, k, v, dense_k, dense_v, ld,
+                                              token_dev);
   ICB_CUDA(cudaGetLastError());
   return ICB_OK;
 }

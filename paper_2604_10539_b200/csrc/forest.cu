@@ -218,7 +218,13 @@ int icb_rotate_window(icb_forest* f, const int32_t* trees, int32_t n, int32_t sc
 
 int icb_append_window(icb_forest* f, const int32_t* trees, int32_t n, int32_t token, const float* keys,
                       const float* values, void* stream) {
-  return icb_append_impl(f, trees, n, token, keys, values, S_(stream));
+  return icb_append_impl(f, trees, n, token, nullptr, keys, values, S_(stream));
+}
+
+int icb_append_window_dev(icb_forest* f, const int32_t* trees, int32_t n, const int32_t* token_dev, const float* keys,
+                          const float* values, void* stream) {
+  if (!token_dev) { icb_set_error(ICB_E_INPUT, "null device token"); return ICB_E_INPUT; }
+  return icb_append_impl(f, trees, n, 0, token_dev, keys, values, S_(stream));
 }
 
 int icb_sparse_attention(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, const float* queries,
@@ -228,7 +234,7 @@ int icb_sparse_attention(icb_forest* f, const int32_t* trees, int32_t n, int32_t
   if (splits > 0 && splits < min_splits) splits = min_splits;
   if (splits <= 0) splits = -min_splits;   // auto, at least min_splits
   if (splits < 0) {
-    int auto_s = std::max(1, std::min(8, (2 * 148 + n - 1) / std::max(n, 1)));
+    int auto_s = std::max(1, std::min(8, (2 * 148) / std::max(n, 1)));   // one wave at 2 CTAs / SM
     splits = std::max(auto_s, -splits);
   }
   return icb_attention_impl(f, trees, n, G, queries, pages, pages_cap, npages, out, stats, scalar_bytes, splits,
@@ -240,7 +246,24 @@ int icb_dense_attention(int32_t n, int32_t G, int32_t dim, int32_t dim_v, int32_
                         void* stream) {
   if (dim % 4 || dim_v % 4) { icb_set_error(ICB_E_CONFIG, "dense attention needs dims divisible by 4"); return ICB_E_CONFIG; }
   if (n_tokens < 1) { icb_set_error(ICB_E_INPUT, "empty key set"); return ICB_E_INPUT; }
-  return icb_dense_attention_impl(n, G, dim, dim_v, kv_dtype, q, k, v, ld, n_tokens, out, splits, S_(stream));
+  return icb_dense_attention_impl(n, G, dim, dim_v, kv_dtype, q, k, v, ld, n_tokens, nullptr, out, splits,
+                                  S_(stream));
+}
+
+int icb_dense_attention_dev(int32_t n, int32_t G, int32_t dim, int32_t dim_v, int32_t kv_dtype, const float* q,
+                            const void* k, const void* v, int64_t ld, const int32_t* token_dev, float* out,
+                            int32_t splits, void* stream) {
+  if (dim % 4 || dim_v % 4) { icb_set_error(ICB_E_CONFIG, "dense attention needs dims divisible by 4"); return ICB_E_CONFIG; }
+  if (!token_dev || ld < 1) { icb_set_error(ICB_E_INPUT, "null device token / empty capacity"); return ICB_E_INPUT; }
+  // splits sized for the full capacity; each CTA clips its rows to *token_dev + 1
+  return icb_dense_attention_impl(n, G, dim, dim_v, kv_dtype, q, k, v, ld, (int32_t)ld, token_dev, out, splits,
+                                  S_(stream));
+}
+
+int icb_dense_append(int32_t n, int32_t dim, int32_t dim_v, int32_t kv_dtype, const float* k, const float* v,
+                     void* dense_k, void* dense_v, int64_t ld, const int32_t* token_dev, void* stream) {
+  if (!token_dev || !dense_k || !dense_v) { icb_set_error(ICB_E_INPUT, "null argument"); return ICB_E_INPUT; }
+  return icb_dense_append_impl(n, dim, dim_v, kv_dtype, k, v, dense_k, dense_v, ld, token_dev, S_(stream));
 }
 
 int icb_tree_info(icb_forest* f, int32_t tree, int64_t* out) {

@@ -512,8 +512,9 @@ __global__ void __launch_bounds__(NT, 512 / NT) insert_kernel(ForestView F, Inse
 }
 
 // Append one decode token to the first non-full window page of each tree.
-__global__ void append_window_kernel(ForestView F, const int32_t* trees, int n, int token, const float* keys,
-                                     const float* values) {
+__global__ void append_window_kernel(ForestView F, const int32_t* trees, int n, int token_host, const int32_t* token_dev,
+                                     const float* keys, const float* values) {
+  const int token = token_dev ? *token_dev : token_host;   // device position: CUDA-graph replays
   const int b = blockIdx.x;
   const int t = trees[b];
   TreeMeta* m = F.meta + t;
@@ -619,10 +620,10 @@ int icb_insert_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t m, c
   return ICB_OK;
 }
 
-int icb_append_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t token, const float* keys,
-                    const float* values, cudaStream_t st) {
+int icb_append_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t token, const int32_t* token_dev,
+                    const float* keys, const float* values, cudaStream_t st) {
   if (n <= 0) return ICB_OK;
-  append_window_kernel<<<n, 128, 0, st>>>(f->view, trees, n, token, keys, values);
+  append_window_kernel<<<n, 128, 0, st>>>(f->view, trees, n, token, token_dev, keys, values);
   ICB_CUDA(cudaGetLastError());
   return ICB_OK;
 }

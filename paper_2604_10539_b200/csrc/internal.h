@@ -85,8 +85,8 @@ struct Scratch {
 };
 
 void zero_node_sizes(icb_forest* f, const int32_t* trees, int n, cudaStream_t st);
-int icb_append_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t token, const float* keys,
-                    const float* values, cudaStream_t st);
+int icb_append_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t token, const int32_t* token_dev,
+                    const float* keys, const float* values, cudaStream_t st);
 int icb_resident_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t role, int32_t count,
                       int32_t n_tokens, const int32_t* tokens, const float* keys, const float* values,
                       cudaStream_t st);
@@ -103,6 +103,8 @@ int icb_insert_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t m, c
 int icb_attention_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, const float* queries,
                        const int32_t* pages, int32_t pages_cap, const int32_t* npages, float* out,
                        int64_t* stats, int32_t scalar_bytes, int32_t splits, cudaStream_t st);
+int icb_dense_append_impl(int32_t n, int32_t dim, int32_t dim_v, int32_t kv_dtype, const float* k, const float* v,
+                          void* dense_k, void* dense_v, int64_t ld, const int32_t* token_dev, cudaStream_t st);
 int icb_dense_attention_impl(int32_t n, int32_t G, int32_t dim, int32_t dim_v, int32_t kv_dtype,
                              const float* q, const void* k, const void* v, int64_t ld, int32_t n_tokens,
-                             float* out, int32_t splits, cudaStream_t st);
+                             const int32_t* token_dev, float* out, int32_t splits, cudaStream_t st);

@@ -22,13 +22,13 @@ import torch
 
 from . import _native as N
 from .errors import ConfigError, InputError
-from .forest import DeviceForest, ForestCaps, dense_attention
+from .forest import DeviceForest, ForestCaps, dense_append, dense_attention
 
 
 @dataclass
 class EngineConfig:
     """Field names and validation follow engine.py:37-92 verbatim; the last
-    four fields are device options."""
+    five fields are device options."""
 
     layers: int = 4
     kv_heads: int = 2
@@ -53,6 +53,7 @@ class EngineConfig:
     max_tokens: int | None = None  # token capacity (prefill + decode); default prefill + 1024
     layer_serial: bool = False
     overlap_dense: bool = True     # skip layers' dense attention on a side stream, concurrent with the search
+    cuda_graph: bool = False       # replay captured decode steps (metrics=False steps)
 
     def __post_init__(self) -> None:
         if min(self.layers, self.kv_heads, self.query_heads_per_group, self.d, self.d_prime) < 1:
@@ -125,6 +126,10 @@ class Engine:
         self.last_pages = None
         self.last_npages = None
         self._side = None
+        self._graphs = {}
+        self._warmed = set()
+        self._gbuf = None
+        self._io = None
 
     # -- prefill ---------------------------------------------------------------
     def prefill(self, keys, values, n_prefill: int) -> "Engine":
@@ -152,6 +157,9 @@ class Engine:
         dpad = (cfg.d + 3) // 4 * 4
         dvpad = (cfg.d_prime + 3) // 4 * 4
         nd = self.n_dense * cfg.kv_heads
+        self._tok_dev = torch.zeros(1, dtype=torch.int32, device=dev)   # decode position on the device
+        self._dense_res = torch.empty((max(nd, 1), cfg.query_heads_per_group, dvpad), dtype=torch.float32,
+                                      device=dev)   # dense attention output (nd planes)
         self.dense_k = torch.zeros((max(nd, 1), self.max_tokens, dpad), dtype=kvt, device=dev)
         self.dense_v = torch.zeros((max(nd, 1), self.max_tokens, dvpad), dtype=kvt, device=dev)
         if nd:
@@ -215,6 +223,8 @@ class Engine:
         self.npages = torch.empty((T,), dtype=torch.int32, device=dev)
         self.stats = torch.zeros((T, 5), dtype=torch.int64, device=dev)
         self.rot_stats = torch.zeros((T, 2), dtype=torch.int64, device=dev)
+        # per-step outputs live in fixed buffers (no allocation on the step path)
+        self._attn_out = torch.empty((T, G, cfg.d_prime), dtype=torch.float32, device=dev)
 
     # -- selection -------------------------------------------------------------
     def page_select(self, q, layer: int, kv_head: int, budget=None) -> list[int]:
@@ -244,8 +254,15 @@ class Engine:
 
     def decode_step(self, token_id: int, queries, keys, values, *, metrics: bool = True, out=None):
         """One decode token through every layer (engine.py:383-514).
-        queries [L, Hq, d], keys [L, H, d], values [L, H, d'].
-        Returns (outputs [L, Hq, d'] fp32 device tensor, StepMetrics | None)."""
+        queries [L, Hq, d], keys [L, H, d], values [L, H, d'] (device tensors,
+        or host tensors: staged through a copy stream, overlapping the previous
+        step's compute).  Returns (outputs [L, Hq, d'] fp32, StepMetrics |
+        None).  With EngineConfig.cuda_graph and metrics=False the step is a
+        replay of a captured graph and the returned device tensor is the
+        engine's static output buffer (valid until the next step).  `out`: a
+        device tensor receives a copy; a host (pinned) tensor is filled
+        asynchronously on the copy stream (synchronize before reading it) and
+        is returned."""
         if not self.prefilled:
             raise ConfigError("decode_step before prefill")
         cfg = self.cfg
@@ -255,39 +272,35 @@ class Engine:
         if token >= self.max_tokens:
             raise ConfigError("token capacity exhausted (raise EngineConfig.max_tokens)")
         dev = self.device
-        q = _dev(queries, dev)
-        kk = _dev(keys, dev)
-        vv = _dev(values, dev)
-        L, H, G = cfg.layers, cfg.kv_heads, cfg.query_heads_per_group
-        if out is None:
-            out = torch.empty((L, H * G, cfg.d_prime), dtype=torch.float32, device=dev)
         rotate = self.rotation_due()
-        overlap = cfg.overlap_dense and not self.fallback and self.n_dense > 0 and dev.type == "cuda"
-        if not overlap:
-            self._dense_part(q, kk, vv, token, out)
-            dense_hook = None
+        L, H, G = cfg.layers, cfg.kv_heads, cfg.query_heads_per_group
+        self._tok_dev.fill_(token)
+        graph = cfg.cuda_graph and not metrics and dev.type == "cuda"
+        host_in = dev.type == "cuda" and any(isinstance(x, torch.Tensor) and x.device.type == "cpu"
+                                             for x in (queries, keys, values))
+        host_out = out is not None and out.device.type == "cpu"
+        if host_in:
+            queries, keys, values, slot = self._stage_in(queries, keys, values)
+        if graph:
+            res = self._graph_step(rotate, queries, keys, values)
         else:
-            # The skip layers' dense attention depends only on this step's
-            # inputs: it runs on a side stream, issued right after the search
-            # kernel so its CTAs fill the SMs the search leaves idle (the
-            # search runs one CTA per tree, two per SM at most).
-            main = torch.cuda.current_stream(dev)
-            if self._side is None:
-                self._side = torch.cuda.Stream(device=dev)
-            ready, done = torch.cuda.Event(), torch.cuda.Event()
-            ready.record(main)
-
-            def dense_hook():
-                self._side.wait_event(ready)
-                with torch.cuda.stream(self._side):
-                    self._dense_part(q, kk, vv, token, out)
-                done.record(self._side)
-        if not self.fallback:
-            if metrics:
+            q = _dev(queries, dev)
+            kk = _dev(keys, dev)
+            vv = _dev(values, dev)
+            res = out if (out is not None and not host_out) else \
+                torch.empty((L, H * G, cfg.d_prime), dtype=torch.float32, device=dev)
+            if metrics and not self.fallback:
                 self.stats.zero_()
-            self._indexed_part(q, kk, vv, token, rotate, out, dense_hook)
-            if overlap:
-                main.wait_event(done)
+            self._device_step(q, kk, vv, rotate, res)
+        if host_in:
+            self._io["in_free"][slot].record(torch.cuda.current_stream(dev))
+        if host_out:
+            res = self._stage_out(res, out)
+        elif graph and out is not None:
+            out.copy_(res)
+            res = out
+        if not self.fallback:
+            self.selection_queries += self.T * G
             if rotate:
                 start, fill = self._win_start[0], self._win_fills[0]
                 self.indexed_tokens.extend(range(start, start + fill))
@@ -301,24 +314,138 @@ class Engine:
         m = None
         if metrics:
             m = self._metrics(token)
-        return out, m
+        return res, m
 
-    def _dense_part(self, q, kk, vv, token, out):
+    def _device_step(self, q, kk, vv, rotate, out):
+        """All device work of one step (capturable: the position comes from
+        self._tok_dev, every buffer is static)."""
+        cfg, dev = self.cfg, self.device
+        overlap = cfg.overlap_dense and not self.fallback and self.n_dense > 0 and dev.type == "cuda"
+        if not overlap:
+            self._dense_part(q, kk, vv, out)
+            dense_hook = None
+        else:
+            # The skip layers' dense attention depends only on this step's
+            # inputs: it runs on a side stream, issued right after the search
+            # kernel so its CTAs fill the SMs the search leaves idle (the
+            # search runs one CTA per tree, two per SM at most).
+            # The side stream forks after the window append, the search kernel's
+            # own predecessor, and its work is issued after the search launch:
+            # in eager order and in a captured graph alike the search's CTAs
+            # are dispatched first and the dense CTAs fill what is left.
+            main = torch.cuda.current_stream(dev)
+            if self._side is None:
+                self._side = torch.cuda.Stream(device=dev)
+            ready, done = torch.cuda.Event(), torch.cuda.Event()
+
+            def fork():
+                ready.record(main)
+
+            def dense_hook():
+                self._side.wait_event(ready)
+                with torch.cuda.stream(self._side):
+                    self._dense_part(q, kk, vv, out)
+                done.record(self._side)
+        if not self.fallback:
+            self._indexed_part(q, kk, vv, rotate, out, dense_hook, fork if overlap else None)
+            if overlap:
+                main.wait_event(done)
+
+    def _io_init(self):
+        cfg, dev = self.cfg, self.device
+        L, H, G = cfg.layers, cfg.kv_heads, cfg.query_heads_per_group
+        shapes = dict(q=(L, H * G, cfg.d), k=(L, H, cfg.d), v=(L, H, cfg.d_prime))
+        self._io = dict(
+            h2d=torch.cuda.Stream(device=dev), d2h=torch.cuda.Stream(device=dev),
+            stage=[{n: torch.empty(sh, dtype=torch.float32, device=dev) for n, sh in shapes.items()}
+                   for _ in range(2)],
+            outbuf=[torch.empty((L, H * G, cfg.d_prime), dtype=torch.float32, device=dev) for _ in range(2)],
+            in_ready=[torch.cuda.Event() for _ in range(2)], in_free=[torch.cuda.Event() for _ in range(2)],
+            out_ready=[torch.cuda.Event() for _ in range(2)], out_done=[torch.cuda.Event() for _ in range(2)],
+            n_in=0, n_out=0)
+
+    def _stage_in(self, queries, keys, values):
+        """H2D of host inputs on the input copy stream into one of two device slots
+        (the slot's previous step must have consumed it)."""
+        if self._io is None:
+            self._io_init()
+        io = self._io
+        slot = io["n_in"] % 2
+        io["n_in"] += 1
+        cs, main = io["h2d"], torch.cuda.current_stream(self.device)
+        st = io["stage"][slot]
+        cs.wait_event(io["in_free"][slot])
+        with torch.cuda.stream(cs):
+            st["q"].copy_(torch.as_tensor(queries).reshape(st["q"].shape), non_blocking=True)
+            st["k"].copy_(torch.as_tensor(keys).reshape(st["k"].shape), non_blocking=True)
+            st["v"].copy_(torch.as_tensor(values).reshape(st["v"].shape), non_blocking=True)
+        io["in_ready"][slot].record(cs)
+        main.wait_event(io["in_ready"][slot])
+        return st["q"], st["k"], st["v"], slot
+
+    def _stage_out(self, res, out_host):
+        """D2H of the step's output on the output copy stream from a rotating device
+        buffer, so the copy never blocks the next step's compute."""
+        if self._io is None:
+            self._io_init()
+        io = self._io
+        slot = io["n_out"] % 2
+        io["n_out"] += 1
+        cs, main = io["d2h"], torch.cuda.current_stream(self.device)
+        buf = io["outbuf"][slot]
+        main.wait_event(io["out_done"][slot])
+        buf.copy_(res)
+        io["out_ready"][slot].record(main)
+        cs.wait_event(io["out_ready"][slot])
+        with torch.cuda.stream(cs):
+            out_host.copy_(buf, non_blocking=True)
+        io["out_done"][slot].record(cs)
+        return out_host
+
+    def _graph_step(self, rotate, queries, keys, values):
+        cfg, dev = self.cfg, self.device
+        L, H, G = cfg.layers, cfg.kv_heads, cfg.query_heads_per_group
+        if self._gbuf is None:
+            self._gbuf = dict(q=torch.empty((L, H * G, cfg.d), dtype=torch.float32, device=dev),
+                              k=torch.empty((L, H, cfg.d), dtype=torch.float32, device=dev),
+                              v=torch.empty((L, H, cfg.d_prime), dtype=torch.float32, device=dev),
+                              out=torch.empty((L, H * G, cfg.d_prime), dtype=torch.float32, device=dev))
+        b = self._gbuf
+        b["q"].copy_(torch.as_tensor(queries), non_blocking=True)
+        b["k"].copy_(torch.as_tensor(keys), non_blocking=True)
+        b["v"].copy_(torch.as_tensor(values), non_blocking=True)
+        key = bool(rotate)
+        g = self._graphs.get(key)
+        if g is None and key in self._warmed:
+            # second occurrence of this step variant: every lazily allocated
+            # scratch exists (first occurrence ran eagerly) -> capture
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._device_step(b["q"], b["k"], b["v"], rotate, b["out"])
+            self._graphs[key] = g
+        if g is None:
+            self._warmed.add(key)
+            self._device_step(b["q"], b["k"], b["v"], rotate, b["out"])
+        else:
+            g.replay()
+        return b["out"]
+
+    def _dense_part(self, q, kk, vv, out, splits=0):
         cfg = self.cfg
         nd = self.n_dense
         if nd == 0:
             return
         H, G = cfg.kv_heads, cfg.query_heads_per_group
-        kvt = self.dense_k.dtype
-        self.dense_k[:, token, : cfg.d] = kk[:nd].reshape(nd * H, cfg.d).to(kvt)
-        self.dense_v[:, token, : cfg.d_prime] = vv[:nd].reshape(nd * H, cfg.d_prime).to(kvt)
+        dense_append(kk[:nd].reshape(nd * H, cfg.d), vv[:nd].reshape(nd * H, cfg.d_prime), self.dense_k,
+                     self.dense_v, self._tok_dev)
         qd = q[:nd].reshape(nd * H, G, cfg.d)
         if cfg.d % 4:
             qd = torch.nn.functional.pad(qd, (0, (4 - cfg.d % 4) % 4))
-        res = dense_attention(qd.contiguous(), self.dense_k, self.dense_v, token + 1)
+        res = dense_attention(qd.contiguous(), self.dense_k, self.dense_v, self._tok_dev, splits=splits,
+                              out=self._dense_res[: nd * H])
         out[:nd] = res[:, :, : cfg.d_prime].reshape(nd, H * G, cfg.d_prime)
 
-    def _indexed_part(self, q, kk, vv, token, rotate, out, after_query=None):
+    def _indexed_part(self, q, kk, vv, rotate, out, after_query=None, before_query=None):
         cfg, f = self.cfg, self.forest
         s0, H, G = cfg.skip_layers, cfg.kv_heads, cfg.query_heads_per_group
         T = self.T
@@ -331,16 +458,18 @@ class Engine:
             trees = self.trees_dev[a:b]
             if rotate:
                 f.rotate_window(trees, cfg.scalar_bytes, self.rot_stats[a:b])
-            f.append_window(trees, token, ki[a:b], vi[a:b])
+            f.append_window(trees, self._tok_dev, ki[a:b], vi[a:b])
+            if before_query is not None:
+                before_query()
+                before_query = None
             f.query(trees, qi[a:b], k, self.beam, self.visit_cap, k_out=k, pages_cap=self.pages_cap,
                     out=(self.ids[a:b], self.counts[a:b], self.pages[a:b], self.npages[a:b]))
             if after_query is not None:
                 after_query()
                 after_query = None
             o = f.attention(trees, qi[a:b], self.pages[a:b], self.npages[a:b], stats=self.stats[a:b],
-                            scalar_bytes=cfg.scalar_bytes)
+                            scalar_bytes=cfg.scalar_bytes, out=self._attn_out[a:b])
             out[s0 + a // H: s0 + b // H] = o.reshape((b - a) // H, H * G, cfg.d_prime)
-        self.selection_queries += T * G
 
     def _metrics(self, token) -> StepMetrics:
         cfg = self.cfg

@@ -203,10 +203,14 @@ class DeviceForest:
         N.check(N.lib().icb_rotate_window(self.h, _ptr(tr), tr.numel(), scalar_bytes, _ptr(stats), _stream()))
 
     def append_window(self, trees, token, keys, values):
+        """`token`: an int, or an int32 device tensor holding it (CUDA-graph replays)."""
         tr = self._trees(trees)
         n = tr.numel()
-        N.check(N.lib().icb_append_window(self.h, _ptr(tr), n, int(token), _ptr(self._f32(keys, (n, self.dim))),
-                                          _ptr(self._f32(values, (n, self.dim_v))), _stream()))
+        k, v = _ptr(self._f32(keys, (n, self.dim))), _ptr(self._f32(values, (n, self.dim_v)))
+        if isinstance(token, torch.Tensor):
+            N.check(N.lib().icb_append_window_dev(self.h, _ptr(tr), n, _ptr(token), k, v, _stream()))
+        else:
+            N.check(N.lib().icb_append_window(self.h, _ptr(tr), n, int(token), k, v, _stream()))
 
     def attention(self, trees, queries, pages, npages, *, out=None, stats=None, scalar_bytes=4, splits=0):
         tr = self._trees(trees)
@@ -300,7 +304,8 @@ class DeviceForest:
 def dense_attention(q, k, v, n_tokens=None, *, splits=0, out=None):
     """full_attention (attention.py:55-74) over the first n_tokens rows of
     contiguous K/V on the device.  q [n,G,d] fp32; k [n,T,d], v [n,T,d'] fp32
-    or bf16 (same dtype, contiguous)."""
+    or bf16 (same dtype, contiguous).  `n_tokens` may be an int32 device
+    tensor holding the decode position p (rows [0, p + 1) are attended)."""
     n, G, d = q.shape
     dv = v.shape[-1]
     if n_tokens is None:
@@ -309,6 +314,20 @@ def dense_attention(q, k, v, n_tokens=None, *, splits=0, out=None):
         out = torch.empty((n, G, dv), dtype=torch.float32, device=q.device)
     kvd = N.KV_BF16 if k.dtype == torch.bfloat16 else N.KV_F32
     q = q.contiguous()
-    N.check(N.lib().icb_dense_attention(n, G, d, dv, kvd, _ptr(q), _ptr(k), _ptr(v), k.shape[1], int(n_tokens),
-                                        _ptr(out), splits, _stream()))
+    if isinstance(n_tokens, torch.Tensor):
+        N.check(N.lib().icb_dense_attention_dev(n, G, d, dv, kvd, _ptr(q), _ptr(k), _ptr(v), k.shape[1],
+                                                _ptr(n_tokens), _ptr(out), splits, _stream()))
+    else:
+        N.check(N.lib().icb_dense_attention(n, G, d, dv, kvd, _ptr(q), _ptr(k), _ptr(v), k.shape[1],
+                                            int(n_tokens), _ptr(out), splits, _stream()))
     return out
+
+
+def dense_append(k, v, dense_k, dense_v, token_dev):
+    """Write row token_dev[0] of each dense K/V plane: k [n,d], v [n,d'] fp32
+    into dense_k [n,T,ceil4(d)], dense_v [n,T,ceil4(d')] (fp32 or bf16)."""
+    n, d = k.shape
+    dv = v.shape[-1]
+    kvd = N.KV_BF16 if dense_k.dtype == torch.bfloat16 else N.KV_F32
+    N.check(N.lib().icb_dense_append(n, d, dv, kvd, _ptr(k.contiguous()), _ptr(v.contiguous()), _ptr(dense_k),
+                                     _ptr(dense_v), dense_k.shape[1], _ptr(token_dev), _stream()))

@@ -74,3 +74,33 @@ def test_engine_c1(cuda_ok):
         ot = oeng.heads[(0, h)].tree.export()
         assert [tuple(n[:4]) + (n[4],) for n in ex["nodes"]] == \
             [(i, lv, par, own, mem) for i, lv, par, own, mem, _ in ot["nodes"]]
+
+
+def test_cuda_graph_replay_matches_eager(cuda_ok):
+    """Captured decode steps (both variants: plain and rotating) replay to the
+    same outputs and selections as eager steps, bit for bit."""
+    import torch
+    from paper_2604_10539_b200.engine import Engine, EngineConfig
+    from oracle.workload import Spec, generate
+    sk = dict(n_tokens=2048 + 60, d=64, d_prime=64, clusters=16, layers=4, kv_heads=2,
+              query_heads_per_group=4, seed=9)
+    keys, values, queries, _ = generate(Spec(kind="clustered", **sk))
+    shape = dict(layers=4, kv_heads=2, query_heads_per_group=4, d=64, d_prime=64, seed=9)
+    cfg = dict(token_budget=32, skip_layers=1, kv_dtype="bf16", max_tokens=2048 + 60)
+    eager = Engine(EngineConfig(**shape, **cfg)).prefill(keys, values, 2048)
+    graph = Engine(EngineConfig(**shape, **cfg, cuda_graph=True)).prefill(keys, values, 2048)
+    q = torch.as_tensor(queries, device="cuda")
+    k = torch.as_tensor(keys, device="cuda")
+    v = torch.as_tensor(values, device="cuda")
+    for t in range(50):
+        tok = 2048 + t
+        o1, _ = eager.decode_step(tok, q[tok], k[tok], v[tok], metrics=False)
+        o2, _ = graph.decode_step(tok, q[tok], k[tok], v[tok], metrics=False)
+        assert torch.equal(o1, o2), t
+        (i1, c1, p1, n1), (i2, c2, p2, n2) = eager.selected(), graph.selected()
+        assert (c1 == c2).all() and (n1 == n2).all(), t
+        for tr in range(c1.shape[0]):
+            assert list(p1[tr, :n1[tr]]) == list(p2[tr, :n2[tr]]), t
+            for g in range(c1.shape[1]):
+                assert list(i1[tr, g, :c1[tr, g]]) == list(i2[tr, g, :c2[tr, g]]), t
+    assert set(graph._graphs) == {False, True}   # both variants captured and replayed

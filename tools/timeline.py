@@ -18,8 +18,18 @@ ctx = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 C2 = dict(layers=32, kv_heads=8, query_heads_per_group=4, d=128, d_prime=128, page_size=16,
           token_budget=256, promotion_ratio=0.1, sink_pages=1, window_pages=2, skip_layers=2)
 steps = 48
-st = clustered_stream(ctx, steps, 32, 8, 4, 128, 128, device="cuda")
-eng = Engine(EngineConfig(**C2, kv_dtype="bf16", max_tokens=ctx + steps + 1)).prefill(st.keys, st.values, ctx)
+GRAPH_WARM = int(os.environ.get("GRAPH_WARM", "0"))   # replay this many graph steps first
+st = clustered_stream(ctx, steps + GRAPH_WARM, 32, 8, 4, 128, 128, device="cuda")
+eng = Engine(EngineConfig(**C2, kv_dtype="bf16", max_tokens=ctx + steps + GRAPH_WARM + 1)).prefill(
+    st.keys, st.values, ctx)
+if GRAPH_WARM:
+    eng.cfg.cuda_graph = True
+    for i in range(GRAPH_WARM):
+        eng.decode_step(ctx + i, st.queries[i], st.keys[ctx + i], st.values[ctx + i], metrics=False)
+    torch.cuda.synchronize()
+    eng.cfg.cuda_graph = False
+    print("graphs captured:", sorted(eng._graphs))
+base = GRAPH_WARM
 f = eng.forest
 marks = []
 
@@ -49,7 +59,8 @@ rows = collections.defaultdict(list)
 for i in range(steps):
     marks.clear()
     s0 = ev()
-    eng.decode_step(ctx + i, st.queries[i], st.keys[ctx + i], st.values[ctx + i], metrics=False)
+    j = base + i
+    eng.decode_step(ctx + j, st.queries[j], st.keys[ctx + j], st.values[ctx + j], metrics=False)
     s1 = ev()
     torch.cuda.synchronize()
     if i < 8:
@@ -62,3 +73,4 @@ for lab, v in rows.items():
     a = sum(x for x, _ in v) / len(v) * 1e3
     b = sum(y for _, y in v) / len(v) * 1e3
     print(f"{lab:18s} {a:9.1f} {b:9.1f} {b - a:8.1f}")
+
