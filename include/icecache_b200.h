@@ -142,6 +142,15 @@ int icb_dense_attention(int32_t n, int32_t G, int32_t dim, int32_t dim_v, int32_
                         const float *q, const void *k, const void *v, int64_t ld,
                         int32_t n_tokens, float *out, int32_t splits, void *stream);
 
+/* Selection reuse (engine.py:321-363, select_with_reuse): for tree trees[b]
+ * (a non-anchor layer) the page list of the token lists that query output
+ * row src_rows[b] holds (src_ids [rows][G][k_stride], src_counts [rows][G],
+ * as written by icb_query), mapped through trees[b]'s own page table:
+ * sorted unique page ids (find_page_index, pagestore.py:111-113). */
+int icb_pages_from_tokens(icb_forest *f, const int32_t *trees, int32_t n, const int32_t *src_rows,
+                          const int32_t *src_ids, const int32_t *src_counts, int32_t G, int32_t k_stride,
+                          int32_t *out_pages, int32_t pages_cap, int32_t *out_npages, void *stream);
+
 /* CUDA-graph variants: the decode position is read from device memory
  * (token_dev[0] = the token being decoded), so one captured decode step
  * replays for every position.  icb_append_window_dev is icb_append_window

@@ -43,6 +43,7 @@ class OConfig:
     visit_cap: int | None = None
     seed: int = 0
     scalar_bytes: int = 4
+    reuse_stride: int = 0
 
     def budget(self):
         k = self.token_budget
@@ -68,6 +69,7 @@ class OracleEngine:
         self.indexed_tokens: list[int] = []
         self.selection_queries = 0
         self.trace: list[dict] = []   # per step: selected tokens / pages
+        self._anchor_tokens: dict[int, set] = {}
 
     def prefill(self, keys, values, n_prefill):
         """keys [n,L,H,d], values [n,L,H,d'] fp64 (fp32-representable)."""
@@ -169,13 +171,25 @@ class OracleEngine:
                 tgt.values.append(values[layer, h])
             for h in range(cfg.kv_heads):
                 st = self.heads[(layer, h)]
-                per = []
-                for g in range(G):
-                    qh = h * G + g
-                    toks = self.select_tokens(queries[layer, qh], layer, h)
-                    trace["tokens"][(layer, qh)] = toks
-                    per.append(find_page_index(toks, st.store.token_to_page))
-                sel = sorted(set().union(*per))
+                if cfg.reuse_stride >= 2 and (layer - cfg.skip_layers) % cfg.reuse_stride != 0:
+                    # select_with_reuse (engine.py:331-363): the latest anchor's
+                    # token union, mapped through this layer's page table
+                    toks = self._anchor_tokens[h]
+                    for g in range(G):
+                        trace["tokens"][(layer, h * G + g)] = sorted(toks)
+                    sel = find_page_index(sorted(toks), st.store.token_to_page)
+                else:
+                    per = []
+                    union = set()
+                    for g in range(G):
+                        qh = h * G + g
+                        toks = self.select_tokens(queries[layer, qh], layer, h)
+                        trace["tokens"][(layer, qh)] = toks
+                        union.update(toks)
+                        per.append(find_page_index(toks, st.store.token_to_page))
+                    if cfg.reuse_stride >= 2:
+                        self._anchor_tokens[h] = union
+                    sel = sorted(set().union(*per))
                 trace["pages"][(layer, h)] = sel
                 delta = st.store.backload(sel)
                 ents_k, ents_v = [], []

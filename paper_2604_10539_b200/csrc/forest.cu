@@ -260,6 +260,21 @@ int icb_dense_attention_dev(int32_t n, int32_t G, int32_t dim, int32_t dim_v, in
                                   S_(stream));
 }
 
+int icb_pages_from_tokens(icb_forest* f, const int32_t* trees, int32_t n, const int32_t* src_rows,
+                          const int32_t* src_ids, const int32_t* src_counts, int32_t G, int32_t k_stride,
+                          int32_t* out_pages, int32_t pages_cap, int32_t* out_npages, void* stream) {
+  if (!f || (n > 0 && (!trees || !src_rows || !src_ids || !src_counts || !out_pages || !out_npages))) {
+    icb_set_error(ICB_E_INPUT, "null argument");
+    return ICB_E_INPUT;
+  }
+  if (G < 1 || G > ICB_MAX_G || k_stride < 1 || pages_cap < 1) {
+    icb_set_error(ICB_E_CONFIG, "bad G / k_stride / pages_cap");
+    return ICB_E_CONFIG;
+  }
+  return icb_pages_from_tokens_impl(f, trees, n, src_rows, src_ids, src_counts, G, k_stride, out_pages, pages_cap,
+                                    out_npages, S_(stream));
+}
+
 int icb_dense_append(int32_t n, int32_t dim, int32_t dim_v, int32_t kv_dtype, const float* k, const float* v,
                      void* dense_k, void* dense_v, int64_t ld, const int32_t* token_dev, void* stream) {
   if (!token_dev || !dense_k || !dense_v) { icb_set_error(ICB_E_INPUT, "null argument"); return ICB_E_INPUT; }

@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) query_kernel(ForestView F, Query
   const int b = blockIdx.x;
   const int t = A.trees[b];
   const int G = A.G;
+  const long long tk0 = clock64();
   double* dirs_tmp;
   unsigned* pbits;
   SearchScratch SS = slot_scratch(scratch + (size_t)b * SL.total, SL, F.tok_cap, &dirs_tmp, &pbits);
@@ -79,15 +80,16 @@ __global__ void __launch_bounds__(NT, 512 / NT) query_kernel(ForestView F, Query
     if (threadIdx.x == 0 && A.out_npages) A.out_npages[b] = 0;
     return;
   }
+  if (A.P.prof && threadIdx.x == 0) atomicAdd(A.P.prof + 3, (unsigned long long)(clock64() - tk0));   // lift
   tree_search<NT, GP>(S, GSA, RG, F, SS, t, A.P, dirs_tmp);
   if (F.meta[t].err & ICB_ERR_CAP_SCRATCH) return;
   // final ranked top-k per head, token -> page bits
+  long long tk1 = 0;
   if (A.P.k <= kBuf) {
     constexpr int NTG = NT / GP;
     const int grp = threadIdx.x / NTG, gtid = threadIdx.x % NTG;
-    long long t0 = clock64();
+    tk1 = clock64();
     const int n = finalize_groups<NT, GP>(S, GSA, F, SS, G, A.P.k);
-    if (A.P.prof && threadIdx.x == 0) atomicAdd(A.P.prof + 7, (unsigned long long)(clock64() - t0));
     if (grp < G) {
       const GroupSmem& GS = GSA[grp];
       const int nw = min(n, A.k_out);
@@ -146,6 +148,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) query_kernel(ForestView F, Query
     __syncthreads();
   }
   if (threadIdx.x == 0) A.out_npages[b] = min(carry, A.pages_cap);
+  if (A.P.prof && threadIdx.x == 0 && A.P.k <= kBuf) atomicAdd(A.P.prof + 7, (unsigned long long)(clock64() - tk1));
 }
 
 }  // namespace icb
@@ -226,6 +229,68 @@ int icb_query_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, co
     ICB_LAUNCH_Q(8)
 #undef ICB_LAUNCH_Q
   }
+  ICB_CUDA(cudaGetLastError());
+  return ICB_OK;
+}
+
+namespace icb {
+// select_with_reuse for a non-anchor layer (engine.py:331-363): the anchor
+// tree's ranked token lists (all G heads) mapped through THIS tree's page
+// table, sorted unique (find_page_index, pagestore.py:111-113).  One CTA per
+// tree; the page bitmap lives in shared memory.
+__global__ void __launch_bounds__(256) pages_from_tokens_kernel(ForestView F, const int32_t* trees,
+                                                                 const int32_t* src_rows, const int32_t* src_ids,
+                                                                 const int32_t* src_counts, int G, int k_stride,
+                                                                 int32_t* out_pages, int pages_cap,
+                                                                 int32_t* out_npages) {
+  extern __shared__ unsigned pbits_s[];
+  __shared__ int wsum[256 / 32 + 1];
+  __shared__ int carry;
+  const int b = blockIdx.x, t = trees[b], sr = src_rows[b];
+  const int nwords = F.page_cap / 32 + 1;
+  for (int w = threadIdx.x; w < nwords; w += blockDim.x) pbits_s[w] = 0u;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int g = 0; g < G; ++g) {
+    const int cnt = src_counts[(size_t)sr * G + g];
+    const int32_t* ids = src_ids + ((size_t)sr * G + g) * k_stride;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const int tok = ids[i];
+      const int p = (tok >= 0 && tok < F.tok_cap) ? F.tok2page[F.tk(t, tok)] : -1;
+      if (p < 0 || p >= F.page_cap) set_err(F.meta + t, ICB_ERR_UNMAPPED);
+      else atomicOr(pbits_s + (p >> 5), 1u << (p & 31));
+    }
+  }
+  __syncthreads();
+  for (int base = 0; base < nwords; base += blockDim.x) {
+    const int w = base + threadIdx.x;
+    unsigned bits = w < nwords ? pbits_s[w] : 0u;
+    int tot;
+    const int ex = block_exclusive_scan<256>(__popc(bits), wsum, tot);
+    int pos = carry + ex;
+    while (bits) {
+      const int bit = __ffs(bits) - 1;
+      bits &= bits - 1;
+      if (pos < pages_cap) out_pages[(size_t)b * pages_cap + pos] = w * 32 + bit;
+      ++pos;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out_npages[b] = min(carry, pages_cap);
+}
+}  // namespace icb
+
+int icb_pages_from_tokens_impl(icb_forest* f, const int32_t* trees, int32_t n, const int32_t* src_rows,
+                               const int32_t* src_ids, const int32_t* src_counts, int32_t G, int32_t k_stride,
+                               int32_t* out_pages, int32_t pages_cap, int32_t* out_npages, cudaStream_t st) {
+  if (n <= 0) return ICB_OK;
+  const size_t smem = (size_t)(f->cfg.page_cap / 32 + 1) * 4;
+  if (smem > 200 * 1024) { icb_set_error(ICB_E_CONFIG, "page bitmap exceeds shared memory"); return ICB_E_CONFIG; }
+  ICB_CUDA(cudaFuncSetAttribute(pages_from_tokens_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  pages_from_tokens_kernel<<<n, 256, smem, st>>>(f->view, trees, src_rows, src_ids, src_counts, G, k_stride,
+                                                 out_pages, pages_cap, out_npages);
   ICB_CUDA(cudaGetLastError());
   return ICB_OK;
 }

@@ -1186,7 +1186,6 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
       if (S.M[g] > SS.ccap) { if (tid == 0) set_err(F.meta + t, ICB_ERR_CAP_SCRATCH); return; }
     ICB_MARK(2);
     const int R = S.misc[6];
-    ICB_MARK(3);
     // (3b) stream the rows through shared memory.  Every warp owns a private
     //      kSub-slot ring (two batches of 8 rows): it issues the async copies
     //      (cp.async, one 512-byte row per instruction) of its batch after

@@ -210,6 +210,8 @@ class Engine:
         self.beam, self.visit_cap = int(min(beam, 2**62)), int(min(cap, 2**62))
         G = cfg.query_heads_per_group
         self.pages_cap = int(min(f.caps.page_cap, G * self.k_eff))
+        if cfg.reuse_stride >= 2 and cfg.layer_serial:
+            raise ConfigError("reuse_stride is supported with layers batched per step (layer_serial=False)")
         self._alloc_step_buffers()
         self.prefilled = True
         return self
@@ -225,8 +227,43 @@ class Engine:
         self.rot_stats = torch.zeros((T, 2), dtype=torch.int64, device=dev)
         # per-step outputs live in fixed buffers (no allocation on the step path)
         self._attn_out = torch.empty((T, G, cfg.d_prime), dtype=torch.float32, device=dev)
+        if cfg.reuse_stride >= 2:
+            # selection reuse (engine.py:321-363): anchor trees are searched,
+            # the others map their anchor's tokens through their own pages
+            H = cfg.kv_heads
+            anchors = [t for t in range(T) if self.is_anchor_layer(cfg.skip_layers + t // H)]
+            reuse = [t for t in range(T) if t not in set(anchors)]
+            src = [((t // H) // cfg.reuse_stride * cfg.reuse_stride) * H + t % H for t in reuse]
+            ix = lambda v: torch.tensor(v, dtype=torch.int64, device=dev)   # noqa: E731
+            self._anchor_rows, self._reuse_rows = ix(anchors), ix(reuse)
+            self._anchor_trees = self.trees_dev[self._anchor_rows].contiguous()
+            self._reuse_trees = self.trees_dev[self._reuse_rows].contiguous()
+            self._reuse_src = torch.tensor(src, dtype=torch.int32, device=dev)
+            nA, nR = len(anchors), len(reuse)
+            self._ids_a = torch.empty((nA, G, self.k_eff), dtype=torch.int32, device=dev)
+            self._counts_a = torch.empty((nA, G), dtype=torch.int32, device=dev)
+            self._pages_a = torch.empty((nA, max(1, self.pages_cap)), dtype=torch.int32, device=dev)
+            self._npages_a = torch.empty((nA,), dtype=torch.int32, device=dev)
+            self._pages_r = torch.empty((max(1, nR), max(1, self.pages_cap)), dtype=torch.int32, device=dev)
+            self._npages_r = torch.empty((max(1, nR),), dtype=torch.int32, device=dev)
 
     # -- selection -------------------------------------------------------------
+    def is_anchor_layer(self, layer: int) -> bool:
+        """engine.py:321-325."""
+        if self.cfg.reuse_stride < 2:
+            raise ConfigError("selection reuse is disabled")
+        return layer >= self.cfg.skip_layers and (layer - self.cfg.skip_layers) % self.cfg.reuse_stride == 0
+
+    def anchor_layers(self) -> list[int]:
+        """engine.py:327-329."""
+        return [l for l in range(self.cfg.skip_layers, self.cfg.layers) if self.is_anchor_layer(l)]
+
+    def _queries_per_step(self) -> int:
+        G = self.cfg.query_heads_per_group
+        if self.cfg.reuse_stride >= 2:
+            return len(self.anchor_layers()) * self.cfg.kv_heads * G
+        return self.T * G
+
     def page_select(self, q, layer: int, kv_head: int, budget=None) -> list[int]:
         """Pages holding the tree's top-budget tokens for one query (engine.py:305-310)."""
         tokens = self.select_tokens(q, layer, kv_head, budget)
@@ -300,7 +337,7 @@ class Engine:
             out.copy_(res)
             res = out
         if not self.fallback:
-            self.selection_queries += self.T * G
+            self.selection_queries += self._queries_per_step()
             if rotate:
                 start, fill = self._win_start[0], self._win_fills[0]
                 self.indexed_tokens.extend(range(start, start + fill))
@@ -462,14 +499,34 @@ class Engine:
             if before_query is not None:
                 before_query()
                 before_query = None
-            f.query(trees, qi[a:b], k, self.beam, self.visit_cap, k_out=k, pages_cap=self.pages_cap,
-                    out=(self.ids[a:b], self.counts[a:b], self.pages[a:b], self.npages[a:b]))
+            if cfg.reuse_stride >= 2:
+                self._select_with_reuse(qi)
+            else:
+                f.query(trees, qi[a:b], k, self.beam, self.visit_cap, k_out=k, pages_cap=self.pages_cap,
+                        out=(self.ids[a:b], self.counts[a:b], self.pages[a:b], self.npages[a:b]))
             if after_query is not None:
                 after_query()
                 after_query = None
             o = f.attention(trees, qi[a:b], self.pages[a:b], self.npages[a:b], stats=self.stats[a:b],
                             scalar_bytes=cfg.scalar_bytes, out=self._attn_out[a:b])
             out[s0 + a // H: s0 + b // H] = o.reshape((b - a) // H, H * G, cfg.d_prime)
+
+    def _select_with_reuse(self, qi):
+        """engine.py:331-363, all layers of the step at once: anchors' searches,
+        then every other layer's pages from its anchor's token lists."""
+        f, k = self.forest, self.k_eff
+        f.query(self._anchor_trees, qi.index_select(0, self._anchor_rows), k, self.beam, self.visit_cap, k_out=k,
+                pages_cap=self.pages_cap, out=(self._ids_a, self._counts_a, self._pages_a, self._npages_a))
+        self.ids.index_copy_(0, self._anchor_rows, self._ids_a)
+        self.counts.index_copy_(0, self._anchor_rows, self._counts_a)
+        self.pages.index_copy_(0, self._anchor_rows, self._pages_a)
+        self.npages.index_copy_(0, self._anchor_rows, self._npages_a)
+        nR = self._reuse_rows.numel()
+        if nR:
+            f.pages_from_tokens(self._reuse_trees, self._reuse_src, self.ids, self.counts, self._pages_r[:nR],
+                                self._npages_r[:nR])
+            self.pages.index_copy_(0, self._reuse_rows, self._pages_r[:nR])
+            self.npages.index_copy_(0, self._reuse_rows, self._npages_r[:nR])
 
     def _metrics(self, token) -> StepMetrics:
         cfg = self.cfg
@@ -479,7 +536,7 @@ class Engine:
         else:
             self.forest.check()
             st = self.stats.sum(0).tolist()
-            dq = self.T * cfg.query_heads_per_group
+            dq = self._queries_per_step()
         return StepMetrics(step=self.steps_done - 1, token_id=token, recall_at_k=1.0, page_hit_rate=1.0,
                            covered_attention_mass=1.0, approx_rel_error=0.0, pages_selected=int(st[0]),
                            pages_loaded=int(st[2]), tokens_loaded=int(st[1]), bytes_moved=int(st[3]),

@@ -198,6 +198,16 @@ class DeviceForest:
                                    _stream()))
         return out
 
+    def pages_from_tokens(self, trees, src_rows, ids, counts, out_pages, out_npages):
+        """select_with_reuse's page lists (engine.py:331-363): tree trees[b]'s
+        sorted unique pages of the token lists in query-output row src_rows[b]
+        (ids [rows][G][k], counts [rows][G] as written by query())."""
+        tr = self._trees(trees)
+        n = tr.numel()
+        G, ks = ids.shape[1], ids.shape[2]
+        N.check(N.lib().icb_pages_from_tokens(self.h, _ptr(tr), n, _ptr(src_rows), _ptr(ids), _ptr(counts), G, ks,
+                                              _ptr(out_pages), out_pages.shape[1], _ptr(out_npages), _stream()))
+
     def rotate_window(self, trees, scalar_bytes=4, stats=None):
         tr = self._trees(trees)
         N.check(N.lib().icb_rotate_window(self.h, _ptr(tr), tr.numel(), scalar_bytes, _ptr(stats), _stream()))

@@ -106,11 +106,17 @@ def engine_cases():
         ("c1", dict(n_tokens=4096 + 16, d=128, d_prime=128, clusters=32, layers=1, kv_heads=8,
                     query_heads_per_group=4, seed=0),
          dict(token_budget=256, skip_layers=0), 4096, 16),
+        # selection reuse (engine.py:321-363): anchors every 3rd indexed layer
+        ("reuse", dict(n_tokens=1024 + 40, d=32, d_prime=16, clusters=8, layers=8, kv_heads=2,
+                       query_heads_per_group=2, seed=11),
+         dict(token_budget=24, skip_layers=2, reuse_stride=3), 1024, 40),
     ]
 
 
-def make_engine_goldens():
+def make_engine_goldens(only=None):
     for name, sk, ck, n_prefill, steps in engine_cases():
+        if only and name not in only:
+            continue
         spec = ic.WorkloadSpec(kind="clustered", **sk)
         wl = ic.generate_workload(spec)
         wl.keys[:] = f32(wl.keys)
@@ -147,4 +153,4 @@ if __name__ == "__main__":
     if "tree" in which:
         make_tree_goldens()
     if "engine" in which:
-        make_engine_goldens()
+        make_engine_goldens([w for w in which if w not in ("tree", "engine")] or None)

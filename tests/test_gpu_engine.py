@@ -42,7 +42,8 @@ def _run(name, kv="fp32", tol=1e-3, layer_serial=False, steps=None):
         for layer in range(ocfg.skip_layers, ocfg.layers):
             for h in range(H):
                 tr = (layer - ocfg.skip_layers) * H + h
-                for g in range(G):
+                reuse_layer = ocfg.reuse_stride >= 2 and (layer - ocfg.skip_layers) % ocfg.reuse_stride
+                for g in range(G if not reuse_layer else 0):   # reuse layers run no query
                     want = trace["tokens"][(layer, h * G + g)]
                     assert list(ids[tr, g, :counts[tr, g]]) == want, (t, layer, h, g)
                 assert list(pages[tr, :npages[tr]]) == trace["pages"][(layer, h)], (t, layer, h)
@@ -60,6 +61,14 @@ def test_engine_mini_fp32(cuda_ok):
 
 def test_engine_mini_bf16(cuda_ok):
     _run("mini", kv="bf16", tol=1e-2)
+
+
+def test_engine_selection_reuse(cuda_ok):
+    """select_with_reuse (engine.py:321-363), reference golden 'reuse': anchors
+    every 3rd indexed layer search; the others map the anchor's token union
+    through their own page table (pages, metrics and dci_queries equal)."""
+    eng, _ = _run("reuse")
+    assert eng.anchor_layers() == [2, 5]
 
 
 def test_engine_mini_layer_serial(cuda_ok):

@@ -104,7 +104,7 @@ def test_inserts_match_reference(name):
         assert _near_tie_ok(tree, q32, tree.query(q32, SENTINEL, k, 2 * k, 4 * k), want)
 
 
-@pytest.mark.parametrize("name", ["mini", "c1"])
+@pytest.mark.parametrize("name", ["mini", "c1", "reuse"])
 def test_engine_matches_reference(name):
     z, meta = load_golden(f"engine_{name}.npz")
     sk, ck = meta["spec"], meta["cfg"]
@@ -125,7 +125,10 @@ def test_engine_matches_reference(name):
         # per query head ranked token lists, in the reference's call order
         calls = meta["tokens"][t]
         idx = 0
+        stride = cfg.reuse_stride
         for layer in range(cfg.skip_layers, cfg.layers):
+            if stride >= 2 and (layer - cfg.skip_layers) % stride:
+                continue   # reuse layer: no query (select_with_reuse, engine.py:331-363)
             for h in range(cfg.kv_heads):
                 for g in range(G):
                     rl, rh, want = calls[idx]
@@ -133,6 +136,7 @@ def test_engine_matches_reference(name):
                     assert (rl, rh) == (layer, h)
                     got = trace["tokens"][(layer, h * G + g)]
                     assert set(got) == set(want), (t, layer, h, g)
+        assert idx == len(calls)
         ref_out = z["outputs"][t]
         err = np.linalg.norm(out - ref_out, axis=-1) / np.linalg.norm(ref_out, axis=-1)
         assert err.max() < 1e-10
