@@ -50,7 +50,9 @@ def parse():
     ap.add_argument("--ctx", type=int, default=32768)
     ap.add_argument("--kv", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--layer-serial", action="store_true")
-    ap.add_argument("--no-graph", action="store_true", help="eager steps in the timed region (no CUDA graphs)")
+    ap.add_argument("--no-graph", action="store_true", help="e2e leg without CUDA graphs")
+    ap.add_argument("--reuse-stride", type=int, default=0,
+                    help="selection reuse (anchor layers, engine.py:321-363); 0 = the reference default (off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
     return ap.parse_args()
@@ -140,7 +142,7 @@ def run_ours(args, rank, world):
     stream = clustered_stream(n0, total_steps, C2["layers"], C2["kv_heads"], C2["query_heads_per_group"],
                               C2["d"], C2["d_prime"], seed=args.seed + rank, device=dev)
     cfg = EngineConfig(**C2, seed=args.seed + rank, kv_dtype=args.kv, max_tokens=n0 + total_steps + 1,
-                       layer_serial=args.layer_serial, cuda_graph=graph)
+                       layer_serial=args.layer_serial, cuda_graph=graph, reuse_stride=args.reuse_stride)
     t0 = time.time()
     eng = Engine(cfg, device=dev).prefill(stream.keys, stream.values, n0)
     torch.cuda.synchronize()
@@ -248,6 +250,7 @@ def run_ours(args, rank, world):
                    "step_execution": "timed region: eager launches; e2e: CUDA-graph replays (plain / rotating "
                                      "step variants)" if graph else "eager launches",
                    "rotations_in_timed_region": rotations,
+                   "reuse_stride": args.reuse_stride,
                    "l2": "per-step working set ~1.4 GB > 126 MB L2; no flush",
                    "prefill_s": round(prefill_s, 2)},
         "roofline": {"bound": "hbm", "kernel": "query_kernel (DCI search + top-k + page union)",
