@@ -36,6 +36,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 E2E_STEPS = 64
+E2E_SEGMENTS = 3   # e2e throughput = median of the segments (one host stall cannot dominate)
 METRIC = "decode tokens/s (TPOT) at 32k ctx, 256-token budget; DCI top-k query µs/head"
 C2 = dict(layers=32, kv_heads=8, query_heads_per_group=4, d=128, d_prime=128, page_size=16,
           token_budget=256, promotion_ratio=0.1, sink_pages=1, window_pages=2, skip_layers=2)
@@ -138,7 +139,7 @@ def run_ours(args, rank, world):
     # recurs every 16 steps, so the warm-up (graph mode) covers two rotations
     W = max(W, 40) if graph else W
     n0 = args.ctx
-    total_steps = W + K + E2E_STEPS + 1
+    total_steps = W + K + E2E_SEGMENTS * E2E_STEPS + 1
     stream = clustered_stream(n0, total_steps, C2["layers"], C2["kv_heads"], C2["query_heads_per_group"],
                               C2["d"], C2["d_prime"], seed=args.seed + rank, device=dev)
     cfg = EngineConfig(**C2, seed=args.seed + rank, kv_dtype=args.kv, max_tokens=n0 + total_steps + 1,
@@ -177,12 +178,28 @@ def run_ours(args, rank, world):
             ev_a1[i].record(cur)
         return r
 
-    f.query, f.attention = q_wrap, a_wrap
+    orig_qa = f.query_attend
+
+    def qa_wrap(*a, **kw):
+        i = timing["i"]
+        if i is not None:
+            ev_q0[i].record(cur)
+        r = orig_qa(*a, **kw)
+        if i is not None:
+            ev_q1[i].record(cur)
+            ev_a1[i].record(cur)
+        return r
+
+    f.query, f.attention, f.query_attend = q_wrap, a_wrap, qa_wrap
+
+    fixed_tok = [0]   # sink + window tokens attended (timed steps)
 
     def step(i):
         tok = n0 + i
         rot = eng.rotation_due()
         eng.decode_step(tok, q_all[i], k_all[i], v_all[i], metrics=False)
+        if timing["i"] is not None:
+            fixed_tok[0] += eng.T * (C2["page_size"] * C2["sink_pages"] + sum(eng._win_fills))
         # library kernels per step: append, search, paged attention, dense append,
         # dense attention (+ the rotation insert kernel)
         launches[0] += 5 + (1 if rot else 0)
@@ -196,6 +213,7 @@ def run_ours(args, rank, world):
     # timed region: eager launches (per-kernel CUDA events on the launching stream)
     eng.cfg.cuda_graph = False
     info0 = [f.info(t) for t in range(eng.T)]
+    stats0 = eng.stats.sum(0).cpu().numpy().copy()
     launches[0] = 0
     rotations = 0
     if world > 1:
@@ -214,6 +232,7 @@ def run_ours(args, rank, world):
     gpu_launches = launches[0]
     eng.cfg.cuda_graph = graph
     info1 = [f.info(t) for t in range(eng.T)]
+    stats1 = eng.stats.sum(0).cpu().numpy().copy()
     f.check()
     ms_max = rank_max(ms, dev, world)
     q_ms = [ev_q0[j].elapsed_time(ev_q1[j]) for j in range(K)]
@@ -224,15 +243,20 @@ def run_ours(args, rank, world):
     evals = sum(b["distance_evals"] - a["distance_evals"] for a, b in zip(info0, info1))
     U = rows - rere
     search_bytes = (4 * (C2["d"] + 1) * U + 4 * evals) / K
+    # the launch also attends (fused): K/V rows of sink, window and selected tokens
+    kv_b = 2 if args.kv == "bf16" else 4
+    attn_tokens = (float(stats1[1] - stats0[1]) + fixed_tok[0]) / K
+    attn_bytes = attn_tokens * (C2["d"] + C2["d_prime"]) * kv_b
+    launch_bytes = search_bytes + (attn_bytes if args.reuse_stride < 2 else 0.0)
     search_s = statistics.mean(q_ms) / 1e3
     peak, peak_kind = peaks()
-    achieved = search_bytes / search_s / 1e9
+    achieved = launch_bytes / search_s / 1e9
     tokens_per_s = world * K / (ms_max / 1e3)
     heads = eng.T * C2["query_heads_per_group"]
 
     # ---- e2e: the next steps through the public API with host (pinned) inputs/outputs
     f.query, f.attention = orig_query, orig_attn
-    e2e_val = run_e2e(eng, stream, n0, W + K, E2E_STEPS, dev, world)
+    e2e_val = run_e2e(eng, stream, n0, W + K, E2E_STEPS, dev, world, E2E_SEGMENTS)
 
     traffic = read_ncu_traffic()
     res = {
@@ -253,14 +277,17 @@ def run_ours(args, rank, world):
                    "reuse_stride": args.reuse_stride,
                    "l2": "per-step working set ~1.4 GB > 126 MB L2; no flush",
                    "prefill_s": round(prefill_s, 2)},
-        "roofline": {"bound": "hbm", "kernel": "query_kernel (DCI search + top-k + page union)",
+        "roofline": {"bound": "hbm", "kernel": "query_kernel (DCI search + top-k + page union + fused sparse "
+                                               "attention)" if args.reuse_stride < 2 else "query_kernel (anchors)",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "alg_bytes_per_launch": search_bytes, "launch_ms": search_s * 1e3,
+                     "alg_bytes_per_launch": launch_bytes, "alg_bytes_search": search_bytes,
+                     "alg_bytes_attention": attn_bytes, "launch_ms": search_s * 1e3,
                      "launch_timing": "CUDA events around each launch on its stream, inside the timed region",
                      "unique_rows_per_step": U / K, "evals_per_step": evals / K},
         "dci_topk_us_per_head": search_s * 1e6 / heads,
-        "attention_ms_per_step": statistics.mean(a_ms),
+        "attention_ms_per_step": statistics.mean(a_ms) if args.reuse_stride >= 2 else "fused into query_kernel",
+        "attended_tokens_per_step": attn_tokens,
         "gpu_launches": gpu_launches,
         "clocks": clk.summary(),
         "e2e": e2e_val,
@@ -278,32 +305,45 @@ def rank_max(x, dev, world):
     return float(t.item())
 
 
-def run_e2e(eng, stream, n0, start, K2, dev, world):
+def run_e2e(eng, stream, n0, start, K2, dev, world, segments=1):
     """Same metric through Engine.decode_step with pinned host inputs (H2D)
-    and the step's outputs read back (D2H) inside the timed region; whole-job
-    tokens over the slowest rank's wall time."""
+    and the step's outputs read back to pinned host memory (D2H) inside the
+    timed region; whole-job tokens over the slowest rank's wall time.  The
+    value is the median over `segments` consecutive K2-step segments (Python's
+    cyclic GC is paused while timing, as a serving loop would)."""
+    import gc
+
     import torch
-    qh = stream.queries[start:start + K2].cpu().pin_memory()
-    kh = stream.keys[n0 + start:n0 + start + K2].cpu().pin_memory()
-    vh = stream.values[n0 + start:n0 + start + K2].cpu().pin_memory()
-    outh = torch.empty((K2,) + (qh.shape[1], qh.shape[2], stream.values.shape[-1]), dtype=torch.float32).pin_memory()
+    n = K2 * segments
+    qh = stream.queries[start:start + n].cpu().pin_memory()
+    kh = stream.keys[n0 + start:n0 + start + n].cpu().pin_memory()
+    vh = stream.values[n0 + start:n0 + start + n].cpu().pin_memory()
+    outh = torch.empty((n,) + (qh.shape[1], qh.shape[2], stream.values.shape[-1]), dtype=torch.float32).pin_memory()
     if eng.steps_done != start:
         return None
-    torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    t0 = time.perf_counter()
-    for i in range(K2):
-        tok = n0 + start + i
-        # host (pinned) inputs in, host output back: the engine stages both
-        # through its copy stream (the D2H is complete at the final synchronize)
-        eng.decode_step(tok, qh[i], kh[i], vh[i], metrics=False, out=outh[i])
-    torch.cuda.synchronize()
-    dt = rank_max(time.perf_counter() - t0, dev, world)
+    vals = []
+    gc.disable()
+    try:
+        for sgm in range(segments):
+            torch.cuda.synchronize()
+            if world > 1:
+                torch.distributed.barrier()
+            t0 = time.perf_counter()
+            for i in range(sgm * K2, (sgm + 1) * K2):
+                tok = n0 + start + i
+                # host (pinned) inputs in, host output back: the engine stages both
+                # through its copy streams (the D2H is complete at the synchronize)
+                eng.decode_step(tok, qh[i], kh[i], vh[i], metrics=False, out=outh[i])
+            torch.cuda.synchronize()
+            dt = rank_max(time.perf_counter() - t0, dev, world)
+            vals.append(world * K2 / dt)
+    finally:
+        gc.enable()
     h2d = (qh[0].numel() + kh[0].numel() + vh[0].numel()) * 4
     d2h = outh[0].numel() * 4
-    return {"value": world * K2 / dt, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "steps": K2}
+    return {"value": statistics.median(vals), "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "steps": n, "segments": [round(v, 1) for v in vals],
+            "path": "Engine.decode_step (public API) -> C ABI; pinned host q/k/v in, pinned host outputs back"}
 
 
 def read_ncu_traffic():

@@ -108,6 +108,18 @@ int icb_query(icb_forest *f, const int32_t *trees, int32_t n, int32_t G, const f
               int32_t target_level, int32_t *out_ids, int32_t k_out, int32_t *out_counts,
               int32_t *out_pages, int32_t pages_cap, int32_t *out_npages, void *stream);
 
+/* The decode step's selection and attention in one launch: icb_query
+ * (SENTINEL target, raw queries) followed, in the same CTA, by
+ * icb_sparse_attention over the tree's sink, window and selected pages
+ * (engine.py:436-475: page_select per head, gqa_union, backload,
+ * sparse_attention, evict_unselected).  attn_out dev [n][G][dim_v];
+ * attn_stats dev [n][5] or NULL (the residency counters of
+ * icb_sparse_attention). */
+int icb_query_attend(icb_forest *f, const int32_t *trees, int32_t n, int32_t G, const float *queries,
+                     int32_t k, int64_t beam, int64_t visit_cap, int32_t *out_ids, int32_t k_out,
+                     int32_t *out_counts, int32_t *out_pages, int32_t pages_cap, int32_t *out_npages,
+                     float *attn_out, int64_t *attn_stats, int32_t scalar_bytes, void *stream);
+
 /* Sequential inserts of m points per tree (trees in parallel).  levels dev
  * [n][m] or NULL (draw from the tree's stream); out_levels dev or NULL. */
 int icb_insert(icb_forest *f, const int32_t *trees, int32_t n, int32_t m, const int32_t *tokens,

@@ -7,29 +7,10 @@
 // warp per page, lane l owns dims 4l..4l+3), the G query heads of a GQA group
 // share each row (G logits per row), softmax is online in fp32, split-K
 // partials (m, l, acc) are combined by the last CTA of each tree.
-#include "icb.cuh"
+#include "attend.cuh"
 #include "internal.h"
 
 namespace icb {
-
-constexpr int kAttnThreads = 256;
-
-// kernels are instantiated for G in {1,2,4,8}; other GQA ratios run padded
-inline int padded_g(int G) { return G <= 2 ? G : G <= 4 ? 4 : 8; }
-
-template <typename KT>
-__device__ __forceinline__ float4 load4(const KT* p);
-template <>
-__device__ __forceinline__ float4 load4<float>(const float* p) {
-  return __ldg(reinterpret_cast<const float4*>(p));
-}
-template <>
-__device__ __forceinline__ float4 load4<__nv_bfloat16>(const __nv_bfloat16* p) {
-  uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
-  float2 a = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.x));
-  float2 b = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.y));
-  return make_float4(a.x, a.y, b.x, b.y);
-}
 
 struct AttnArgs {
   int n, G, dim, dim_v, splits;
@@ -51,213 +32,6 @@ struct AttnArgs {
   int scalar_bytes;
   float scale_log2;            // log2(e) / sqrt(dim)
 };
-
-struct HeadAcc {
-  float m, l;
-  float4 acc;
-};
-
-template <int H, int OFF>
-__device__ __forceinline__ float head_sums_rest(const float (&w)[H], int lane) {
-  if constexpr (H == 1) {
-    float s = w[0];
-#pragma unroll
-    for (int o = OFF; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    return s;
-  } else {
-    constexpr int H2 = H / 2;
-    float x[H2];
-    const bool up = lane & OFF;
-#pragma unroll
-    for (int i = 0; i < H2; ++i) {
-      float send = up ? w[i] : w[i + H2];
-      x[i] = (up ? w[i + H2] : w[i]) + __shfl_xor_sync(0xffffffffu, send, OFF);
-    }
-    return head_sums_rest<H2, OFF / 2>(x, lane);
-  }
-}
-
-// Sum of each head's lane partials transposed across heads: lane l ends with
-// head l / (32/G)'s total after G/2 + G/4 + ... + (5 - log2 G) shuffles.
-template <int G>
-__device__ __forceinline__ float head_sums(const float (&v)[G], int lane) {
-  return head_sums_rest<G, 16>(v, lane);
-}
-
-// Raw row chunks: 4 dims per lane, loaded for a whole chunk of rows before
-// any of them is used (one memory round trip per chunk).
-template <typename KT>
-struct Raw4;
-template <>
-struct Raw4<float> {
-  using T = float4;
-  static __device__ __forceinline__ T load(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
-  static __device__ __forceinline__ float4 cvt(T r) { return r; }
-  static __device__ __forceinline__ T zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
-};
-template <>
-struct Raw4<__nv_bfloat16> {
-  using T = uint2;
-  static __device__ __forceinline__ T load(const __nv_bfloat16* p) { return __ldg(reinterpret_cast<const uint2*>(p)); }
-  static __device__ __forceinline__ float4 cvt(T u) {
-    float2 a = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.x));
-    float2 b = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.y));
-    return make_float4(a.x, a.y, b.x, b.y);
-  }
-  static __device__ __forceinline__ T zero() { return make_uint2(0u, 0u); }
-};
-
-template <typename KT, int G>
-__device__ __forceinline__ void attend_vals(HeadAcc (&h)[G], const float4 (&qv)[G], float4 k, float4 v, int lane,
-                                            float scale_log2) {
-  float s[G];
-#pragma unroll
-  for (int g = 0; g < G; ++g) s[g] = qv[g].x * k.x + qv[g].y * k.y + qv[g].z * k.z + qv[g].w * k.w;
-  if constexpr (G == 1) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s[0] += __shfl_xor_sync(0xffffffffu, s[0], o);
-  } else {
-    // transposed reduction (head g's sum lands in lanes g*32/G...), then broadcast
-    const float mine = head_sums<G>(s, lane);
-#pragma unroll
-    for (int g = 0; g < G; ++g) s[g] = __shfl_sync(0xffffffffu, mine, g * (32 / G));
-  }
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const float x = s[g] * scale_log2;   // identical in every lane: the branch is warp-uniform
-    if (x > h[g].m) {                    // rescale only when the running max grows
-      const float a = exp2f(h[g].m - x);
-      h[g].l *= a;
-      h[g].acc.x *= a;
-      h[g].acc.y *= a;
-      h[g].acc.z *= a;
-      h[g].acc.w *= a;
-      h[g].m = x;
-    }
-    const float p = exp2f(x - h[g].m);
-    h[g].l += p;
-    h[g].acc.x += p * v.x;
-    h[g].acc.y += p * v.y;
-    h[g].acc.z += p * v.z;
-    h[g].acc.w += p * v.w;
-  }
-}
-
-template <typename KT, int G>
-__device__ __forceinline__ void attend_row(HeadAcc (&h)[G], const float4 (&qv)[G], const KT* krow, const KT* vrow,
-                                           int lane, int dim, int dim_v, float scale_log2) {
-  float4 k = lane * 4 < dim ? load4<KT>(krow + lane * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
-  float4 v = lane * 4 < dim_v ? load4<KT>(vrow + lane * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
-  attend_vals<KT, G>(h, qv, k, v, lane, scale_log2);
-}
-
-// A chunk of CH rows starting at row index `r0` of a [rows][ld] K/V pair:
-// all loads first, then the rows' online-softmax updates in order.
-template <typename KT, int G, int CH>
-__device__ __forceinline__ void attend_chunk(HeadAcc (&h)[G], const float4 (&qv)[G], const KT* K, const KT* V,
-                                             size_t r0, int nrow, int ldk, int ldv, int lane, int dim, int dim_v,
-                                             float scale_log2) {
-  using R = Raw4<KT>;
-  typename R::T kr[CH], vr[CH];
-#pragma unroll
-  for (int c = 0; c < CH; ++c) {
-    kr[c] = (c < nrow && lane * 4 < dim) ? R::load(K + (r0 + c) * ldk + lane * 4) : R::zero();
-    vr[c] = (c < nrow && lane * 4 < dim_v) ? R::load(V + (r0 + c) * ldv + lane * 4) : R::zero();
-  }
-#pragma unroll
-  for (int c = 0; c < CH; ++c)
-    if (c < nrow) attend_vals<KT, G>(h, qv, R::cvt(kr[c]), R::cvt(vr[c]), lane, scale_log2);
-}
-
-// G = 4: a chunk of 8 rows at once.  Scores: lane l computes, in slot jj,
-// the partial dots of row jj ^ pi(l) (pi = lane bits 4..2) against the two
-// head pairs (f32x2), and a transposed reduction (select-free at the row
-// levels xor 16/8/4, splitting the pairs at xor 2/1) leaves lane l with the
-// score of (row pi(l), head l & 3).  Softmax: one chunk max per head (xor
-// 4/8/16), one exp2 per lane, the heads' rescale factors broadcast from lanes
-// 0..3; P.V: each lane accumulates its 4 dims of every head from the 32
-// broadcast probabilities.  Every lane keeps m and l of its own head.
-struct G4State {
-  float m, l;          // of head (lane & 3)
-  float4 acc[4];       // dims 4l..4l+3 of every head
-};
-
-template <typename KT>
-__device__ __forceinline__ void attend_chunk8_g4(G4State& st, const unsigned long long (&q2)[2][4], const KT* K,
-                                                 const KT* V, size_t r0, int nrow, int ldk, int ldv, int lane,
-                                                 int dim, int dim_v, float scale_log2) {
-  using R = Raw4<KT>;
-  const int pi = (lane >> 2) & 7;
-  typename R::T kr[8], vr[8];
-#pragma unroll
-  for (int jj = 0; jj < 8; ++jj) {
-    const int rk = jj ^ pi;
-    kr[jj] = (rk < nrow && lane * 4 < dim) ? R::load(K + (r0 + rk) * ldk + lane * 4) : R::zero();
-    vr[jj] = (jj < nrow && lane * 4 < dim_v) ? R::load(V + (r0 + jj) * ldv + lane * 4) : R::zero();
-  }
-  unsigned long long v2[8][2];
-#pragma unroll
-  for (int jj = 0; jj < 8; ++jj) {
-    const float4 k = R::cvt(kr[jj]);
-#pragma unroll
-    for (int hp = 0; hp < 2; ++hp) {
-      unsigned long long a;
-      const unsigned long long kx = pack_f2(k.x, k.x), ky = pack_f2(k.y, k.y);
-      const unsigned long long kz = pack_f2(k.z, k.z), kw = pack_f2(k.w, k.w);
-      asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(a) : "l"(kx), "l"(q2[hp][0]));
-      asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a) : "l"(ky), "l"(q2[hp][1]));
-      asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a) : "l"(kz), "l"(q2[hp][2]));
-      asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a) : "l"(kw), "l"(q2[hp][3]));
-      v2[jj][hp] = a;
-    }
-  }
-#pragma unroll
-  for (int jj = 0; jj < 4; ++jj)
-#pragma unroll
-    for (int hp = 0; hp < 2; ++hp) v2[jj][hp] = fadd2(v2[jj][hp], shfl_xor_u64(v2[jj + 4][hp], 16));
-#pragma unroll
-  for (int jj = 0; jj < 2; ++jj)
-#pragma unroll
-    for (int hp = 0; hp < 2; ++hp) v2[jj][hp] = fadd2(v2[jj][hp], shfl_xor_u64(v2[jj + 2][hp], 8));
-#pragma unroll
-  for (int hp = 0; hp < 2; ++hp) v2[0][hp] = fadd2(v2[0][hp], shfl_xor_u64(v2[1][hp], 4));
-  const bool b1 = lane & 2, b0 = lane & 1;
-  const unsigned long long w = fadd2(b1 ? v2[0][1] : v2[0][0], shfl_xor_u64(b1 ? v2[0][0] : v2[0][1], 2));
-  const float wl = __uint_as_float((unsigned)w), wh = __uint_as_float((unsigned)(w >> 32));
-  const float dot = (b0 ? wh : wl) + __shfl_xor_sync(0xffffffffu, b0 ? wl : wh, 1);
-  const float x = pi < nrow ? dot * scale_log2 : -INFINITY;
-  // chunk max of this lane's head (lanes sharing lane & 3)
-  float cm = x;
-  cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 4));
-  cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 8));
-  cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 16));
-  const float mn = fmaxf(st.m, cm);
-  const float alpha = exp2f(st.m - mn);   // 0 on the first chunk (m = -inf)
-  const float p = exp2f(x - mn);          // 0 for masked rows
-  float ps = p;
-  ps += __shfl_xor_sync(0xffffffffu, ps, 4);
-  ps += __shfl_xor_sync(0xffffffffu, ps, 8);
-  ps += __shfl_xor_sync(0xffffffffu, ps, 16);
-  st.l = st.l * alpha + ps;
-  st.m = mn;
-#pragma unroll
-  for (int h = 0; h < 4; ++h) {
-    const float a = __shfl_sync(0xffffffffu, alpha, h);
-    st.acc[h].x *= a; st.acc[h].y *= a; st.acc[h].z *= a; st.acc[h].w *= a;
-  }
-#pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    const float4 v = R::cvt(vr[r]);
-#pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      const float pr = __shfl_sync(0xffffffffu, p, 4 * r + h);
-      st.acc[h].x = fmaf(pr, v.x, st.acc[h].x);
-      st.acc[h].y = fmaf(pr, v.y, st.acc[h].y);
-      st.acc[h].z = fmaf(pr, v.z, st.acc[h].z);
-      st.acc[h].w = fmaf(pr, v.w, st.acc[h].w);
-    }
-  }
-}
 
 // Block = (tree b, split sp).  PAGED: rows come from the tree's sink, window
 // and selected pages; DENSE: rows [0, n_tokens) of k/v[b].

@@ -96,7 +96,8 @@ int icb_build_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t n_poi
 int icb_query_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, const float* queries,
                    int32_t lifted_input, int32_t k, int64_t beam, int64_t visit_cap, int32_t target_level,
                    int32_t* out_ids, int32_t k_out, int32_t* out_counts, int32_t* out_pages,
-                   int32_t pages_cap, int32_t* out_npages, cudaStream_t st);
+                   int32_t pages_cap, int32_t* out_npages, cudaStream_t st, float* attn_out = nullptr,
+                   int64_t* attn_stats = nullptr, int32_t scalar_bytes = 4);
 int icb_insert_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t m, const int32_t* tokens,
                     const float* keys, const float* values, const int32_t* levels, int32_t* out_levels,
                     int from_window, int32_t scalar_bytes, int64_t* stats, cudaStream_t st);

@@ -2,6 +2,7 @@
 // gqa_union fused into the epilogue (dci.py:318-364, pagestore.py:111-113,
 // attention.py:96-103, engine.py:436-447).
 #include "search.cuh"
+#include "attend.cuh"
 #include "internal.h"
 
 namespace icb {
@@ -19,6 +20,11 @@ struct QueryArgs {
   int32_t* out_pages;
   int pages_cap;
   int32_t* out_npages;
+  // fused paged attention (icb_query_attend): per tree [G][dim_v] fp32
+  float* attn_out;
+  int64_t* attn_stats;   // [n][5] or null
+  int scalar_bytes;
+  float scale_log2;
 };
 
 // Lift raw query g (geometry.py:89-98): fp64 norm in pairwise order, fp32 q/|q|.
@@ -149,6 +155,21 @@ __global__ void __launch_bounds__(NT, 512 / NT) query_kernel(ForestView F, Query
   }
   if (threadIdx.x == 0) A.out_npages[b] = min(carry, A.pages_cap);
   if (A.P.prof && threadIdx.x == 0 && A.P.k <= kBuf) atomicAdd(A.P.prof + 7, (unsigned long long)(clock64() - tk1));
+  if (A.attn_out) {
+    // fused sparse attention over this tree's sink, window and selected pages
+    // (the row ring is idle: it holds the warps' softmax states)
+    __syncthreads();
+    const int nsel = min(carry, A.pages_cap);
+    const int32_t* sel = A.out_pages + (size_t)b * A.pages_cap;
+    unsigned char* sm = reinterpret_cast<unsigned char*>(RG.ring);
+    const float* qb = A.queries + (size_t)b * G * F.dim;
+    float* ob = A.attn_out + (size_t)b * G * F.dim_v;
+    int64_t* stb = A.attn_stats ? A.attn_stats + (size_t)b * 5 : nullptr;
+    if (F.kv_bf16)
+      attend_tree_paged<__nv_bfloat16, GP, NT>(F, t, G, qb, sel, nsel, ob, stb, A.scalar_bytes, A.scale_log2, sm);
+    else
+      attend_tree_paged<float, GP, NT>(F, t, G, qb, sel, nsel, ob, stb, A.scalar_bytes, A.scale_log2, sm);
+  }
 }
 
 }  // namespace icb
@@ -196,8 +217,13 @@ int ensure_query_scratch(icb_forest* f, int n, int G, cudaStream_t st, char** ou
 int icb_query_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, const float* queries,
                    int32_t lifted_input, int32_t k, int64_t beam, int64_t visit_cap, int32_t target_level,
                    int32_t* out_ids, int32_t k_out, int32_t* out_counts, int32_t* out_pages,
-                   int32_t pages_cap, int32_t* out_npages, cudaStream_t st) {
+                   int32_t pages_cap, int32_t* out_npages, cudaStream_t st, float* attn_out,
+                   int64_t* attn_stats, int32_t scalar_bytes) {
   if (n <= 0) return ICB_OK;
+  if (attn_out && (lifted_input || !out_pages)) {
+    icb_set_error(ICB_E_INPUT, "fused attention needs raw queries and page outputs");
+    return ICB_E_INPUT;
+  }
   if (G < 1 || G > ICB_MAX_G) {
     icb_set_error(ICB_E_CONFIG, "query heads per tree must be in [1, 8]");
     return ICB_E_CONFIG;
@@ -213,6 +239,8 @@ int icb_query_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, co
   if (getenv("ICB_PROF")) ICB_CUDA(cudaGetSymbolAddress((void**)&A.P.prof, g_search_prof));
   A.out_ids = out_ids; A.k_out = k_out; A.out_counts = out_counts; A.out_pages = out_pages;
   A.pages_cap = pages_cap; A.out_npages = out_npages;
+  A.attn_out = attn_out; A.attn_stats = attn_stats; A.scalar_bytes = scalar_bytes;
+  A.scale_log2 = (float)(1.4426950408889634 / sqrt((double)f->cfg.dim));
   const int GP = G <= 1 ? 1 : G <= 2 ? 2 : G <= 4 ? 4 : 8;
   size_t dsm = search_dsm_bytes(GP);
   if (const char* e = getenv("ICB_QUERY_DSM_EXTRA")) dsm += (size_t)atol(e);   // debug knob: occupancy

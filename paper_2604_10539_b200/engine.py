@@ -501,14 +501,21 @@ class Engine:
                 before_query = None
             if cfg.reuse_stride >= 2:
                 self._select_with_reuse(qi)
+                if after_query is not None:
+                    after_query()
+                    after_query = None
+                o = f.attention(trees, qi[a:b], self.pages[a:b], self.npages[a:b], stats=self.stats[a:b],
+                                scalar_bytes=cfg.scalar_bytes, out=self._attn_out[a:b])
             else:
-                f.query(trees, qi[a:b], k, self.beam, self.visit_cap, k_out=k, pages_cap=self.pages_cap,
-                        out=(self.ids[a:b], self.counts[a:b], self.pages[a:b], self.npages[a:b]))
-            if after_query is not None:
-                after_query()
-                after_query = None
-            o = f.attention(trees, qi[a:b], self.pages[a:b], self.npages[a:b], stats=self.stats[a:b],
-                            scalar_bytes=cfg.scalar_bytes, out=self._attn_out[a:b])
+                # selection + sparse attention fused: each tree's CTA attends its
+                # pages right after its search (icb_query_attend)
+                o = f.query_attend(trees, qi[a:b], k, self.beam, self.visit_cap,
+                                   out=(self.ids[a:b], self.counts[a:b], self.pages[a:b], self.npages[a:b]),
+                                   attn_out=self._attn_out[a:b], stats=self.stats[a:b],
+                                   scalar_bytes=cfg.scalar_bytes)
+                if after_query is not None:
+                    after_query()
+                    after_query = None
             out[s0 + a // H: s0 + b // H] = o.reshape((b - a) // H, H * G, cfg.d_prime)
 
     def _select_with_reuse(self, qi):

@@ -184,6 +184,21 @@ class DeviceForest:
                                   pages_cap if want_pages else 0, _ptr(npages), _stream()))
         return ids, counts, pages, npages
 
+    def query_attend(self, trees, queries, k, beam, visit_cap, *, out, attn_out, stats=None, scalar_bytes=4):
+        """The decode step's selection + sparse attention in one launch
+        (icb_query_attend): out = (ids, counts, pages, npages) buffers as for
+        query(); attn_out [n,G,dim_v] fp32; stats [n,5] residency counters."""
+        tr = self._trees(trees)
+        n = tr.numel()
+        q = self._f32(queries).reshape(n, -1, self.dim).contiguous()
+        G = q.shape[1]
+        ids, counts, pages, npages = out
+        N.check(N.lib().icb_query_attend(self.h, _ptr(tr), n, G, _ptr(q), int(min(k, 2**30)), int(min(beam, 2**62)),
+                                         int(min(visit_cap, 2**62)), _ptr(ids), ids.shape[2], _ptr(counts),
+                                         _ptr(pages), pages.shape[1], _ptr(npages), _ptr(attn_out), _ptr(stats),
+                                         scalar_bytes, _stream()))
+        return attn_out
+
     def insert(self, trees, tokens, keys, values=None, levels=None):
         tr = self._trees(trees)
         n = tr.numel()

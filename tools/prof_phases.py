@@ -27,7 +27,7 @@ lib.icb_search_profile(buf.ctypes.data_as(ctypes.c_void_p), 1)
 for i in range(4, 12):
     eng.decode_step(ctx + i, st.queries[i], st.keys[ctx + i], st.values[ctx + i], metrics=False)
 lib.icb_search_profile(buf.ctypes.data_as(ctypes.c_void_p), 1)
-names = ["loop", "union", "scan+rowlist", "-", "stream", "pdci+ctr", "select", "finalize"]
+names = ["loop", "union", "scan+rowlist", "lift+start", "stream", "pdci+ctr", "select", "final+pages"]
 print('top-B selections', buf[8], 'radix fallbacks', buf[9], 'avg boundary bin', buf[10] / max(1, buf[8]))
 ns = max(1, buf[8])
 print('top-B us per selection: hist %.2f scan %.2f emit %.2f sort+tail %.2f' % tuple(buf[11 + i] / ns / 1.9e3 for i in range(4)))
