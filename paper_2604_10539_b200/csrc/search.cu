@@ -161,14 +161,16 @@ __global__ void __launch_bounds__(NT, 512 / NT) query_kernel(ForestView F, Query
     __syncthreads();
     const int nsel = min(carry, A.pages_cap);
     const int32_t* sel = A.out_pages + (size_t)b * A.pages_cap;
-    unsigned char* sm = reinterpret_cast<unsigned char*>(RG.ring);
+    unsigned char* sm = reinterpret_cast<unsigned char*>(RG.ring);   // the idle row ring: warps' softmax states
     const float* qb = A.queries + (size_t)b * G * F.dim;
     float* ob = A.attn_out + (size_t)b * G * F.dim_v;
     int64_t* stb = A.attn_stats ? A.attn_stats + (size_t)b * 5 : nullptr;
+    const long long ta = clock64();
     if (F.kv_bf16)
       attend_tree_paged<__nv_bfloat16, GP, NT>(F, t, G, qb, sel, nsel, ob, stb, A.scalar_bytes, A.scale_log2, sm);
     else
       attend_tree_paged<float, GP, NT>(F, t, G, qb, sel, nsel, ob, stb, A.scalar_bytes, A.scale_log2, sm);
+    if (A.P.prof && threadIdx.x == 0) atomicAdd(A.P.prof + 8, (unsigned long long)(clock64() - ta));
   }
 }
 
@@ -176,16 +178,18 @@ __global__ void __launch_bounds__(NT, 512 / NT) query_kernel(ForestView F, Query
 
 using namespace icb;
 
-// Phase cycle counters of the search (enabled by ICB_PROF=1): union, scans,
-// row list, row stream, P-DCI + counters, selection, level tail, finalize.
+// Phase cycle counters of the search (enabled by ICB_PROF=1; debug tool, not
+// in the public header): out[0..kPhases) = loop, union, scan + row list,
+// lift + start, stream, P-DCI + counters, selection, final top-k + pages,
+// fused attention; out[kPhases..kPhases + 8) = selection statistics.
 extern "C" int icb_search_profile(unsigned long long* out, int reset) {
   ICB_CUDA(cudaDeviceSynchronize());
   ICB_CUDA(cudaMemcpyFromSymbol(out, g_search_prof, sizeof(unsigned long long) * kPhases));
   ICB_CUDA(cudaMemcpyFromSymbol(out + kPhases, g_topb_stats, sizeof(unsigned long long) * 8));
   if (reset) {
-    unsigned long long z[kPhases] = {};
-    ICB_CUDA(cudaMemcpyToSymbol(g_search_prof, z, sizeof(z)));
-    ICB_CUDA(cudaMemcpyToSymbol(g_topb_stats, z, sizeof(unsigned long long) * kPhases));
+    unsigned long long z[kPhases + 8] = {};
+    ICB_CUDA(cudaMemcpyToSymbol(g_search_prof, z, sizeof(unsigned long long) * kPhases));
+    ICB_CUDA(cudaMemcpyToSymbol(g_topb_stats, z, sizeof(unsigned long long) * 8));
   }
   return ICB_OK;
 }

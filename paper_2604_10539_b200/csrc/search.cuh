@@ -811,7 +811,7 @@ struct SearchParams {
   unsigned long long* prof;   // optional per-phase cycle counters (kPhases), thread 0 of each CTA adds
 };
 
-constexpr int kPhases = 8;
+constexpr int kPhases = 9;   // + fused attention (search.cu)
 #define ICB_MARK(k)                                       \
   do {                                                    \
     if (P.prof && threadIdx.x == 0) {                     \

@@ -20,18 +20,18 @@ st = clustered_stream(ctx, 40, 32, 8, 4, 128, 128, device="cuda")
 eng = Engine(EngineConfig(**C2, kv_dtype="bf16", max_tokens=ctx + 64)).prefill(st.keys, st.values, ctx)
 lib = N.lib()
 lib.icb_search_profile.argtypes = [ctypes.c_void_p, ctypes.c_int]
-buf = np.zeros(16, dtype=np.uint64)
+buf = np.zeros(17, dtype=np.uint64)
 for i in range(4):
     eng.decode_step(ctx + i, st.queries[i], st.keys[ctx + i], st.values[ctx + i], metrics=False)
 lib.icb_search_profile(buf.ctypes.data_as(ctypes.c_void_p), 1)
 for i in range(4, 12):
     eng.decode_step(ctx + i, st.queries[i], st.keys[ctx + i], st.values[ctx + i], metrics=False)
 lib.icb_search_profile(buf.ctypes.data_as(ctypes.c_void_p), 1)
-names = ["loop", "union", "scan+rowlist", "lift+start", "stream", "pdci+ctr", "select", "final+pages"]
-print('top-B selections', buf[8], 'radix fallbacks', buf[9], 'avg boundary bin', buf[10] / max(1, buf[8]))
-ns = max(1, buf[8])
-print('top-B us per selection: hist %.2f scan %.2f emit %.2f sort+tail %.2f' % tuple(buf[11 + i] / ns / 1.9e3 for i in range(4)))
-buf = buf[:8]
+names = ["loop", "union", "scan+rowlist", "lift+start", "stream", "pdci+ctr", "select", "final+pages", "attention"]
+print('top-B selections', buf[9], 'radix fallbacks', buf[10], 'avg boundary bin', buf[11] / max(1, buf[9]))
+ns = max(1, buf[9])
+print('top-B us per selection: hist %.2f scan %.2f emit %.2f sort+tail %.2f' % tuple(buf[12 + i] / ns / 1.9e3 for i in range(4)))
+buf = buf[:9]
 tot = buf.sum()
 per_cta_us = buf / (8 * eng.T) / 1.9e3
 for n, v, u in zip(names, buf, per_cta_us):
