@@ -373,6 +373,7 @@ __device__ void insert_points(SearchSmem& S, GroupSmem* GSA, const RingView& RG,
   TreeMeta* m = F.meta + t;
   WarpSearchBuf* WB = reinterpret_cast<WarpSearchBuf*>(RG.ring);   // the ring is idle during inserts
   __shared__ int s_par[NW], s_ok[NW], s_wpage[NW], s_wslot[NW];
+  __shared__ int s_rc[NW], s_rsz[NW], s_rcap[NW], s_roff[NW], s_rlv[NW], s_rlp[NW], s_rfill[NW];
   __shared__ unsigned long long s_ev[NW];
   __shared__ InsertPoint s_pt[NW + 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -426,15 +427,81 @@ __device__ void insert_points(SearchSmem& S, GroupSmem* GSA, const RingView& RG,
       }
     }
     mark(2);
-    // the run's bookkeeping in insertion order (one thread, no barriers),
-    // then its K/V slot writes in parallel (one warp per point)
+    // The run's bookkeeping in insertion order.  Each point's container and
+    // its node / last-page fields are fetched in parallel (one thread per
+    // point); one thread then applies the points in order from those copies
+    // (updating later points that share a container), so page ids and slots
+    // equal the sequential inserts'.  Then the K/V slot writes, one warp per
+    // point.
+    if (tid < nr) {
+      const int par = s_par[tid];
+      const int c = par >= 0 ? F.own(t, par, 1) : m->top_node;
+      const size_t x = F.nd(t, c);
+      const int lp = F.node_lastpage[x];
+      s_rc[tid] = c;
+      s_rsz[tid] = F.node_size[x];
+      s_rcap[tid] = F.node_capm[x];
+      s_roff[tid] = F.node_off[x];
+      s_rlv[tid] = F.node_level[x];
+      s_rlp[tid] = lp;
+      s_rfill[tid] = lp >= 0 ? F.page_fill[F.pg(t, lp)] : 0;
+    }
+    __syncthreads();
     if (tid == 0)
       for (int w = 0; w < nr; ++w) {
-        const int par = s_par[w];
-        const int container = par >= 0 ? F.own(t, par, 1) : m->top_node;
-        int slot = 0;
-        s_wpage[w] = finish_book(F, t, s_pt[w].tok, 1, container, 0, true, &slot);
-        s_wslot[w] = slot;
+        const int tok = s_pt[w].tok, c = s_rc[w];
+        const size_t x = F.nd(t, c);
+        note_point_level(F, t, tok, 1);
+        // add_member (insert.cu:add_member) from the cached node fields
+        int sz = s_rsz[w], cap = s_rcap[w], off = s_roff[w];
+        int* mem = F.mem(t);
+        bool ok = true;
+        if (sz == cap) {
+          const int ncap = cap < 4 ? 4 : 2 * cap;
+          const int noff = m->member_top;
+          if (noff + ncap > F.member_cap) { set_err(m, ICB_ERR_CAP_MEMBERS); ok = false; }
+          else {
+            m->member_top = noff + ncap;
+            for (int i = 0; i < sz; ++i) mem[noff + i] = mem[off + i];
+            off = noff;
+            cap = ncap;
+            F.node_off[x] = off;
+            F.node_capm[x] = cap;
+          }
+        }
+        if (ok) {
+          mem[off + sz] = tok;
+          F.node_size[x] = sz + 1;
+          note_node_size(m, s_rlv[w], sz + 1);
+          ++sz;
+        }
+        // page placement (dci.py:368-381)
+        int page = s_rlp[w], fill = s_rfill[w];
+        if (page < 0 || fill >= F.s) {
+          page = m->next_page;
+          if (page >= F.page_cap) { set_err(m, ICB_ERR_CAP_PAGES); page = -1; }
+          else {
+            m->next_page = page + 1;
+            F.page_fill[F.pg(t, page)] = 0;
+            F.page_role[F.pg(t, page)] = ICB_ROLE_INDEXED;
+            F.node_lastpage[x] = page;
+            fill = 0;
+          }
+        }
+        s_wpage[w] = page;
+        s_wslot[w] = fill;
+        if (page >= 0) {
+          F.page_tok[F.pg(t, page) * F.s + fill] = tok;
+          F.page_fill[F.pg(t, page)] = fill + 1;
+          F.tok2page[F.tk(t, tok)] = page;
+          ++fill;
+        }
+        m->n_points += 1;
+        for (int w2 = w + 1; w2 < nr; ++w2)
+          if (s_rc[w2] == c) {
+            s_rsz[w2] = sz; s_rcap[w2] = cap; s_roff[w2] = off;
+            s_rlp[w2] = page; s_rfill[w2] = fill;
+          }
       }
     __syncthreads();
     if (warp < nr && s_wpage[warp] >= 0)
