@@ -1053,7 +1053,15 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
     int* stage_up = reinterpret_cast<int*>(RG.ring);   // [NT * NPT] (the ring is idle outside the stream)
     int* stage_off = stage_up + NT * NPT;
     int* stage_opos = stage_off + NT * NPT;
-    if (lv == start && start < L) {
+    // start level 2: the upper list is exactly the row set (every entry has
+    // top >= 2); the stream reads tokens from it directly (no row list)
+    const bool rows_from_upper = lv == start && start == 2 && start < L;
+    if (rows_from_upper) {
+      if (tid == 0) S.scan_carry[GP] = F.meta[t].n_upper;
+      __syncthreads();
+      if (tid < G) { S.scan_carry[tid] = S.scan_carry[GP]; SS.uoff[(size_t)tid * F.node_cap] = 0; }
+      if (tid == 0) SS.upre[0] = 0;
+    } else if (lv == start && start < L) {
       // rows of the start level: the upper points of top >= start, as one
       // virtual union entry 0 requested by every head
       const int nu = F.meta[t].n_upper;
@@ -1220,12 +1228,18 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
         int upre;
         int uo[GP];
       };
+      const int* upl_t = F.upl(t);
       auto load_a = [&](int kb) {
         RowTok a{0, -1};
         const int j = warp + kb * NW;
         if (j < nb && lane < 8 && 8 * j + lane < R) {
-          a.tok = SS.rlist[2 * (size_t)(8 * j + lane)];
-          a.ix = SS.rlist[2 * (size_t)(8 * j + lane) + 1];
+          if (rows_from_upper) {
+            a.tok = upl_t[8 * j + lane];
+            a.ix = 0;
+          } else {
+            a.tok = SS.rlist[2 * (size_t)(8 * j + lane)];
+            a.ix = SS.rlist[2 * (size_t)(8 * j + lane) + 1];
+          }
         }
         return a;
       };
