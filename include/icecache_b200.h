@@ -206,6 +206,9 @@ int icb_errors(icb_forest *f, int32_t *out, int32_t clear);
 int icb_clear_errors(icb_forest *f, int32_t tree);
 /* KeyScale.c of a built tree (host out). */
 int icb_read_meta_c(icb_forest *f, int32_t tree, double *c);
+/* KeyScale c of an empty tree that grows by inserts only (DciTree(dim, scale,
+ * ...), dci.py:164-176; geometry.py:47-56).  A build sets c itself. */
+int icb_set_scale(icb_forest *f, int32_t tree, double c);
 /* Host-side restatement check: n PCG64 doubles of SeedSequence(words, spawn). */
 int icb_host_pcg_doubles(const uint32_t *words, int32_t n_words, const uint32_t *spawn,
                          int32_t n_spawn, int32_t n, double *out);

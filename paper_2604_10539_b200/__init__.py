@@ -9,5 +9,7 @@ sparse paged attention run as sm_100a kernels behind a C ABI
 from .errors import (ConfigError, ConsistencyError, DegenerateQueryError, IceCacheError, InputError,
                      InvariantViolation, PolicyError, ScaleViolationError)
 from .forest import DeviceForest, ForestCaps, dense_attention, entropy_words
+from .dci import (PARENT_BUDGET, SENTINEL_LEVEL, DciTree, KeyScale, SearchBudget, assign_level, dci_indexing,
+                  gqa_union, query_raw, transform_query)
 
 __version__ = "0.1.0"

@@ -334,6 +334,14 @@ int icb_read_meta_c(icb_forest* f, int32_t tree, double* c) {
   return ICB_OK;
 }
 
+int icb_set_scale(icb_forest* f, int32_t tree, double c) {
+  if (!f || tree < 0 || tree >= f->cfg.n_trees) { icb_set_error(ICB_E_INPUT, "bad tree"); return ICB_E_INPUT; }
+  if (!(c > 0.0)) { icb_set_error(ICB_E_CONFIG, "scale must be positive"); return ICB_E_CONFIG; }
+  ICB_CUDA(cudaMemcpy((char*)(f->view.meta + tree) + offsetof(TreeMeta, c), &c, sizeof(double),
+                      cudaMemcpyHostToDevice));
+  return ICB_OK;
+}
+
 int icb_export_tree(icb_forest* f, int32_t tree, int32_t* node_level, int32_t* node_parent, int32_t* node_owner,
                     int32_t* node_off, int32_t* node_size, int32_t* node_lastpage, int32_t* members,
                     int32_t* page_fill, int8_t* page_role, int32_t* page_tok, int32_t* tok2page, int8_t* level,
