@@ -154,6 +154,13 @@ int icb_dense_attention(int32_t n, int32_t G, int32_t dim, int32_t dim_v, int32_
                         const float *q, const void *k, const void *v, int64_t ld,
                         int32_t n_tokens, float *out, int32_t splits, void *stream);
 
+/* DciTree.pdci_query (dci.py:282-298): the k nearest members of one node to
+ * a lifted query (q_lifted dev [dim + 1]), ranked by (d2, id); P-DCI visit
+ * list of visit_cap members for nodes above EXHAUSTIVE_NODE_LIMIT that the cap
+ * does not cover.  out_ids dev [>= min(k, node size)], out_count dev [1]. */
+int icb_node_query(icb_forest *f, int32_t tree, int32_t node, const float *q_lifted, int32_t k,
+                   int64_t visit_cap, int32_t *out_ids, int32_t *out_count, void *stream);
+
 /* Selection reuse (engine.py:321-363, select_with_reuse): for tree trees[b]
  * (a non-anchor layer) the page list of the token lists that query output
  * row src_rows[b] holds (src_ids [rows][G][k_stride], src_counts [rows][G],

@@ -272,6 +272,16 @@ int icb_dense_attention_dev(int32_t n, int32_t G, int32_t dim, int32_t dim_v, in
                                   S_(stream));
 }
 
+int icb_node_query(icb_forest* f, int32_t tree, int32_t node, const float* q_lifted, int32_t k, int64_t visit_cap,
+                   int32_t* out_ids, int32_t* out_count, void* stream) {
+  if (!f || tree < 0 || tree >= f->cfg.n_trees || !q_lifted || !out_ids || !out_count) {
+    icb_set_error(ICB_E_INPUT, "bad argument");
+    return ICB_E_INPUT;
+  }
+  if (k < 1 || visit_cap < k) { icb_set_error(ICB_E_CONFIG, "need 1 <= k <= visit_cap"); return ICB_E_CONFIG; }
+  return icb_node_query_impl(f, tree, node, q_lifted, k, visit_cap, out_ids, out_count, S_(stream));
+}
+
 int icb_pages_from_tokens(icb_forest* f, const int32_t* trees, int32_t n, const int32_t* src_rows,
                           const int32_t* src_ids, const int32_t* src_counts, int32_t G, int32_t k_stride,
                           int32_t* out_pages, int32_t pages_cap, int32_t* out_npages, void* stream) {

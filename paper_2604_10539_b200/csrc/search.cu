@@ -326,3 +326,62 @@ int icb_pages_from_tokens_impl(icb_forest* f, const int32_t* trees, int32_t n, c
   ICB_CUDA(cudaGetLastError());
   return ICB_OK;
 }
+
+namespace icb {
+// DciTree.pdci_query (dci.py:282-298, :300-314): the k nearest members of one
+// node to a lifted query, ranked by (d2, id) -- all members when the node is
+// small or the visit cap covers it, else its P-DCI visit list (visit_cap
+// evaluations).  One CTA.
+template <int NT>
+__global__ void __launch_bounds__(NT) node_query_kernel(ForestView F, int t, int node, const float* q, long long k,
+                                                        long long visit_cap, int32_t* out_ids, int32_t* out_count,
+                                                        char* scratch, SlotLayout SL) {
+  __shared__ SearchSmem S;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  const RingView RG = ring_view(dsm, 1);
+  if (threadIdx.x == 0) S.sortbuf = reinterpret_cast<unsigned long long*>(RG.ring);
+  double* dirs_tmp;
+  unsigned* pbits;
+  SearchScratch SS = slot_scratch(scratch, SL, F.tok_cap, &dirs_tmp, &pbits);
+  TreeMeta* m = F.meta + t;
+  if (node < 0 || node >= m->n_nodes) {
+    if (threadIdx.x == 0) { set_err(m, ICB_ERR_EMPTY_TREE); *out_count = 0; }
+    return;
+  }
+  for (int u = threadIdx.x; u < ICB_DPAD; u += NT) S.q[0][u] = u < F.dim ? q[u] : 0.0f;
+  if (threadIdx.x == 0) S.qt[0] = q[F.dim];
+  __syncthreads();
+  const size_t x = F.nd(t, node);
+  const int sz = F.node_size[x];
+  const int* list = F.mem(t) + F.node_off[x];
+  int cnt = sz;
+  if (sz > ICB_EXHAUSTIVE && (long long)sz > visit_cap) {
+    cnt = pdci_visit<NT>(S, F, SS, t, node, 0, visit_cap, dirs_tmp);
+    list = SS.vis;
+  }
+  eval_list_one_head<NT>(S, F, t, list, cnt, 0, SS.cand);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicAdd(&m->distance_evals, (unsigned long long)cnt);
+  int n = (int)min((long long)cnt, k);
+  if (n > kSortMax) { if (threadIdx.x == 0) set_err(m, ICB_ERR_CAP_SCRATCH); n = kSortMax; }
+  const int got = block_select<NT>(S, SS.cand, cnt, n, S.sortbuf, nullptr, 0, nullptr);
+  block_sort<NT>(S, got);
+  for (int i = threadIdx.x; i < got; i += NT) out_ids[i] = key_id(S.sortbuf[i]);
+  if (threadIdx.x == 0) *out_count = got;
+}
+}  // namespace icb
+
+int icb_node_query_impl(icb_forest* f, int32_t tree, int32_t node, const float* q_lifted, int32_t k,
+                        int64_t visit_cap, int32_t* out_ids, int32_t* out_count, cudaStream_t st) {
+  char* scratch;
+  SlotLayout SL;
+  int rc = ensure_query_scratch(f, 1, 1, st, &scratch, &SL);
+  if (rc) return rc;
+  const size_t dsm = search_dsm_bytes(1);
+  ICB_CUDA(cudaFuncSetAttribute(node_query_kernel<kSearchThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)dsm));
+  node_query_kernel<kSearchThreads><<<1, kSearchThreads, dsm, st>>>(f->view, tree, node, q_lifted, k, visit_cap,
+                                                                    out_ids, out_count, scratch, SL);
+  ICB_CUDA(cudaGetLastError());
+  return ICB_OK;
+}

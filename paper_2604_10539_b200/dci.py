@@ -213,6 +213,26 @@ class DciTree:
         self.forest.check()
         return [int(x) for x in ids[0, 0, : int(counts[0, 0])].cpu().tolist()]
 
+    def pdci_query(self, q_vec, node, k: int, budget: SearchBudget | None = None) -> list[int]:
+        """dci.py:282-298: the node's k nearest members to a lifted query
+        (exact up to EXHAUSTIVE_NODE_LIMIT members or when the visit cap covers
+        the node; else the P-DCI order truncated at visit_cap evaluations)."""
+        from .forest import _ptr, _stream
+        node_id = node.node_id if isinstance(node, DciNode) else int(node)
+        if budget is None:
+            budget = SearchBudget.for_k(k)
+        q = np.asarray(q_vec, dtype=np.float64).reshape(-1)
+        if q.shape != (self.dim + 1,):
+            raise InputError(f"lifted query must have shape ({self.dim + 1},), got {q.shape}")
+        dev = self.forest.device
+        qd = torch.as_tensor(q.astype(np.float32), device=dev)
+        ids = torch.empty(max(1, min(int(k), self.capacity)), dtype=torch.int32, device=dev)
+        cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+        N.check(N.lib().icb_node_query(self.forest.h, 0, node_id, _ptr(qd), int(min(k, ids.numel())),
+                                       int(min(budget.visit_cap, 2**62)), _ptr(ids), _ptr(cnt), _stream()))
+        self.forest.check()
+        return [int(x) for x in ids[: int(cnt.item())].cpu().tolist()]
+
     # -- insert --------------------------------------------------------------------
     def insert(self, point_id: int, key, value=None, *, rng: np.random.Generator | None = None,
                level: int | None = None) -> int:

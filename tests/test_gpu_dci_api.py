@@ -195,3 +195,63 @@ def test_identical_seeds_build_identical_trees(cuda_ok):
     assert a.point_level == b.point_level
     assert {(n.node_id, n.level, n.owner_id, tuple(n.member_ids)) for n in a.nodes.values()} == \
         {(n.node_id, n.level, n.owner_id, tuple(n.member_ids)) for n in b.nodes.values()}
+
+
+def test_pdci_query_single_member_node(cuda_ok):
+    D = _api()
+    tree = D.dci_indexing([(3, np.array([1.0, 2.0]))], 0.5, seed=6)
+    top = tree.nodes[tree.top_node_id]
+    assert tree.pdci_query(np.array([0.0, 0.0, 1.0]), top, 5) == [3]
+
+
+def test_pdci_query_exhaustive_cap_matches_brute_force(cuda_ok):
+    D = _api()
+    rng = np.random.default_rng(7)
+    keys = rng.normal(size=(256, 10))
+    tree = D.dci_indexing(_pairs(keys), 1e-9, seed=7)   # one flat node
+    top = tree.nodes[tree.top_node_id]
+    assert len(top.member_ids) == 256
+    lifted = np.stack([tree.lifted(p) for p in range(256)])
+    for _ in range(10):
+        tq = D.transform_query(rng.normal(size=10))
+        got = tree.pdci_query(tq, top, 8, D.SearchBudget(8, 16, 256))
+        d2 = ((lifted - tq) ** 2).sum(axis=1)
+        want = [int(i) for i in np.lexsort((np.arange(256), d2))[:8]]
+        assert got == want
+
+
+def test_pdci_query_full_k_returns_all_ranked(cuda_ok):
+    D = _api()
+    rng = np.random.default_rng(8)
+    keys = rng.normal(size=(40, 6))
+    tree = D.dci_indexing(_pairs(keys), 1e-9, seed=8)
+    top = tree.nodes[tree.top_node_id]
+    q = D.transform_query(rng.normal(size=6))
+    got = tree.pdci_query(q, top, 40)
+    assert sorted(got) == list(range(40))
+    d2 = [float(((tree.lifted(p) - q) ** 2).sum()) for p in got]
+    assert d2 == sorted(d2)
+
+
+def test_pdci_projection_path_matches_oracle_and_cap(cuda_ok):
+    """P-DCI visit order (visit_cap < size): same visited set / ranking as the
+    oracle's heap merge, exactly visit_cap evaluations (reference test
+    test_pdci_projection_path_respects_visit_cap)."""
+    D = _api()
+    from oracle import numerics as nm
+    rng = np.random.default_rng(9)
+    keys = rng.normal(size=(500, 8))
+    tree = D.dci_indexing(_pairs(keys), 1e-9, seed=9)
+    top = tree.nodes[tree.top_node_id]
+    assert len(top.member_ids) > D.EXHAUSTIVE_NODE_LIMIT
+    ot = obuild(_pairs(keys), 1e-9, seed=9)
+    q = D.transform_query(rng.normal(size=8))
+    before = tree.distance_evals
+    got = tree.pdci_query(q, top, 4, D.SearchBudget(4, 8, 100))
+    assert tree.distance_evals - before == 100
+    q32 = np.zeros(nm.DPAD, np.float32)
+    q32[:8] = q[:8].astype(np.float32)    # the lifted query as the device holds it (tail 0)
+    q64 = np.concatenate([q32[:8].astype(np.float64), [0.0]])
+    ids, d2 = ot._candidates(ot.nodes[ot.top], q32, np.float32(0.0), q64, 100)
+    want = [int(ids[i]) for i in np.lexsort((ids, d2))[:4]]
+    assert got == want
