@@ -154,6 +154,12 @@ int icb_dense_attention(int32_t n, int32_t G, int32_t dim, int32_t dim_v, int32_
                         const float *q, const void *k, const void *v, int64_t ld,
                         int32_t n_tokens, float *out, int32_t splits, void *stream);
 
+/* Evaluation support (engine.py:536-566): mask dev [n][tok_cap] uint8 set to 1
+ * for every token of tree trees[b]'s sink, window and selected pages (the
+ * attended set of sparse_attention), 0 elsewhere. */
+int icb_attended_mask(icb_forest *f, const int32_t *trees, int32_t n, const int32_t *pages, int32_t pages_cap,
+                      const int32_t *npages, uint8_t *mask, void *stream);
+
 /* DciTree.pdci_query (dci.py:282-298): the k nearest members of one node to
  * a lifted query (q_lifted dev [dim + 1]), ranked by (d2, id); P-DCI visit
  * list of visit_cap members for nodes above EXHAUSTIVE_NODE_LIMIT that the cap

@@ -272,6 +272,12 @@ int icb_dense_attention_dev(int32_t n, int32_t G, int32_t dim, int32_t dim_v, in
                                   S_(stream));
 }
 
+int icb_attended_mask(icb_forest* f, const int32_t* trees, int32_t n, const int32_t* pages, int32_t pages_cap,
+                      const int32_t* npages, uint8_t* mask, void* stream) {
+  if (!f || (n > 0 && (!trees || !pages || !npages || !mask))) { icb_set_error(ICB_E_INPUT, "null argument"); return ICB_E_INPUT; }
+  return icb_attended_mask_impl(f, trees, n, pages, pages_cap, npages, mask, S_(stream));
+}
+
 int icb_node_query(icb_forest* f, int32_t tree, int32_t node, const float* q_lifted, int32_t k, int64_t visit_cap,
                    int32_t* out_ids, int32_t* out_count, void* stream) {
   if (!f || tree < 0 || tree >= f->cfg.n_trees || !q_lifted || !out_ids || !out_count) {

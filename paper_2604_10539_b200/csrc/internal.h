@@ -104,6 +104,8 @@ int icb_insert_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t m, c
 int icb_attention_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, const float* queries,
                        const int32_t* pages, int32_t pages_cap, const int32_t* npages, float* out,
                        int64_t* stats, int32_t scalar_bytes, int32_t splits, cudaStream_t st);
+int icb_attended_mask_impl(icb_forest* f, const int32_t* trees, int32_t n, const int32_t* pages, int32_t pages_cap,
+                           const int32_t* npages, uint8_t* mask, cudaStream_t st);
 int icb_node_query_impl(icb_forest* f, int32_t tree, int32_t node, const float* q_lifted, int32_t k,
                         int64_t visit_cap, int32_t* out_ids, int32_t* out_count, cudaStream_t st);
 int icb_pages_from_tokens_impl(icb_forest* f, const int32_t* trees, int32_t n, const int32_t* src_rows,

@@ -385,3 +385,32 @@ int icb_node_query_impl(icb_forest* f, int32_t tree, int32_t node, const float* 
   ICB_CUDA(cudaGetLastError());
   return ICB_OK;
 }
+
+namespace icb {
+// Attended-token masks for evaluation (engine.py:536-566): mask[b][tok] = 1
+// for every token of tree trees[b]'s sink, window and selected pages.
+__global__ void attended_mask_kernel(ForestView F, const int32_t* trees, const int32_t* pages, int pages_cap,
+                                     const int32_t* npages, uint8_t* mask) {
+  const int b = blockIdx.x, t = trees[b];
+  const TreeMeta* m = F.meta + t;
+  uint8_t* mk = mask + (size_t)b * F.tok_cap;
+  const int nsink = m->n_sink, nfix = nsink + m->n_window, total = nfix + npages[b];
+  for (int i = threadIdx.x / 32; i < total; i += blockDim.x / 32) {
+    const int p = i < nsink ? m->sink[i] : i < nfix ? m->win[i - nsink] : pages[(size_t)b * pages_cap + i - nfix];
+    const int fill = F.page_fill[F.pg(t, p)];
+    for (int r = threadIdx.x & 31; r < fill; r += 32) {
+      const int tok = F.page_tok[F.pg(t, p) * F.s + r];
+      if (tok >= 0 && tok < F.tok_cap) mk[tok] = 1;
+    }
+  }
+}
+}  // namespace icb
+
+int icb_attended_mask_impl(icb_forest* f, const int32_t* trees, int32_t n, const int32_t* pages, int32_t pages_cap,
+                           const int32_t* npages, uint8_t* mask, cudaStream_t st) {
+  if (n <= 0) return ICB_OK;
+  ICB_CUDA(cudaMemsetAsync(mask, 0, (size_t)n * f->cfg.tok_cap, st));
+  attended_mask_kernel<<<n, 256, 0, st>>>(f->view, trees, pages, pages_cap, npages, mask);
+  ICB_CUDA(cudaGetLastError());
+  return ICB_OK;
+}

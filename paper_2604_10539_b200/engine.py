@@ -76,6 +76,8 @@ class EngineConfig:
             raise ConfigError("scalar_bytes must be >= 1")
         if self.kv_dtype not in ("fp32", "bf16"):
             raise ConfigError("kv_dtype must be fp32 or bf16")
+        if self.compare_baseline:
+            raise ConfigError("compare_baseline (TokenOrderBaseline, engine.py:148-182) is outside the device path")
 
     @property
     def n_query_heads(self) -> int:
@@ -158,6 +160,14 @@ class Engine:
         dvpad = (cfg.d_prime + 3) // 4 * 4
         nd = self.n_dense * cfg.kv_heads
         self._tok_dev = torch.zeros(1, dtype=torch.int32, device=dev)   # decode position on the device
+        if cfg.evaluate:
+            # exact-reference mirrors of every layer (engine.py:536-566, _full_reference)
+            self._mk = torch.zeros((cfg.layers, cfg.kv_heads, self.max_tokens, cfg.d), dtype=torch.float32, device=dev)
+            self._mv = torch.zeros((cfg.layers, cfg.kv_heads, self.max_tokens, cfg.d_prime), dtype=torch.float32,
+                                   device=dev)
+            self._mk[:, :, :n_prefill] = keys.permute(1, 2, 0, 3)
+            self._mv[:, :, :n_prefill] = values.permute(1, 2, 0, 3)
+            self._indexed_mask = torch.zeros(self.max_tokens, dtype=torch.bool, device=dev)
         self._dense_res = torch.empty((max(nd, 1), cfg.query_heads_per_group, dvpad), dtype=torch.float32,
                                       device=dev)   # dense attention output (nd planes)
         self.dense_k = torch.zeros((max(nd, 1), self.max_tokens, dpad), dtype=kvt, device=dev)
@@ -174,6 +184,8 @@ class Engine:
         win_start = (pages - cfg.window_pages) * s
         self.sink_tokens = list(range(sink_end))
         self.indexed_tokens = list(range(sink_end, win_start))
+        if cfg.evaluate:
+            self._indexed_mask[sink_end:win_start] = True
         Li = cfg.layers - cfg.skip_layers
         H = cfg.kv_heads
         T = Li * H
@@ -320,6 +332,9 @@ class Engine:
             queries, keys, values, slot = self._stage_in(queries, keys, values)
         if graph:
             res = self._graph_step(rotate, queries, keys, values)
+            if cfg.evaluate:
+                self._mk[:, :, token] = self._gbuf["k"]
+                self._mv[:, :, token] = self._gbuf["v"]
         else:
             q = _dev(queries, dev)
             kk = _dev(keys, dev)
@@ -328,6 +343,9 @@ class Engine:
                 torch.empty((L, H * G, cfg.d_prime), dtype=torch.float32, device=dev)
             if metrics and not self.fallback:
                 self.stats.zero_()
+            if cfg.evaluate:
+                self._mk[:, :, token] = kk
+                self._mv[:, :, token] = vv
             self._device_step(q, kk, vv, rotate, res)
         if host_in:
             self._io["in_free"][slot].record(torch.cuda.current_stream(dev))
@@ -341,6 +359,8 @@ class Engine:
             if rotate:
                 start, fill = self._win_start[0], self._win_fills[0]
                 self.indexed_tokens.extend(range(start, start + fill))
+                if cfg.evaluate:
+                    self._indexed_mask[start:start + fill] = True
                 self._win_fills = self._win_fills[1:] + [0]
                 self._win_start = self._win_start[1:] + [token]
             i = next(j for j, fl in enumerate(self._win_fills) if fl < cfg.page_size)
@@ -351,6 +371,9 @@ class Engine:
         m = None
         if metrics:
             m = self._metrics(token)
+            if cfg.evaluate and not self.fallback and not graph:
+                rec, hit, mass, rel = self._evaluate(token, q, res)
+                m.recall_at_k, m.page_hit_rate, m.covered_attention_mass, m.approx_rel_error = rec, hit, mass, rel
         return res, m
 
     def _device_step(self, q, kk, vv, rotate, out):
@@ -534,6 +557,54 @@ class Engine:
                                 self._npages_r[:nR])
             self.pages.index_copy_(0, self._reuse_rows, self._pages_r[:nR])
             self.npages.index_copy_(0, self._reuse_rows, self._npages_r[:nR])
+
+    def _evaluate(self, token, q, out):
+        """_evaluate_head (engine.py:536-566) for every indexed layer and query
+        head, on the device in fp64: recall of the exact top-k over indexed
+        tokens (exact_topk, geometry.py:107-126: descending score, ties to the
+        smaller token), hit rate of the exact top-k over all tokens in the
+        attended set, covered attention mass, relative output error; averaged
+        over heads."""
+        cfg, dev = self.cfg, self.device
+        H, G, d = cfg.kv_heads, cfg.query_heads_per_group, cfg.d
+        n = token + 1
+        att = self.forest.attended_mask(self.trees_dev, self.pages, self.npages,
+                                        torch.empty((self.T, self.forest.caps.tok_cap), dtype=torch.uint8,
+                                                    device=dev))[:, :n].bool()
+        idx_mask = self._indexed_mask[:n]
+        k_eff = min(cfg.token_budget, len(self.indexed_tokens))
+        k_all = min(cfg.token_budget, n)
+        rec, hit, mass, rel = [], [], [], []
+        for layer in range(cfg.skip_layers, cfg.layers):
+            li = layer - cfg.skip_layers
+            K = self._mk[layer, :, :n].double()
+            V = self._mv[layer, :, :n].double()
+            ql = q[layer].double().reshape(H, G, d)
+            scores = torch.einsum("hnd,hgd->hgn", K, ql)
+            w = torch.softmax(scores / (d ** 0.5), dim=-1)
+            ref = torch.einsum("hgn,hnv->hgv", w, V)
+            order_idx = torch.sort(-scores.masked_fill(~idx_mask, float("-inf")), dim=-1, stable=True).indices
+            order_all = torch.sort(-scores, dim=-1, stable=True).indices[..., :k_all]
+            # each head's selected tokens (reuse layers: the anchor's union, engine.py:358-361)
+            src = li if cfg.reuse_stride < 2 else (li // cfg.reuse_stride) * cfg.reuse_stride
+            sel = torch.zeros((H, G, n + 1), dtype=torch.bool, device=dev)   # column n: padding slots
+            ids = self.ids[src * H:(src + 1) * H].long()
+            cnt = self.counts[src * H:(src + 1) * H]
+            valid = torch.arange(ids.shape[-1], device=dev)[None, None, :] < cnt[..., None]
+            if cfg.reuse_stride >= 2 and li != src:
+                ids = ids.reshape(H, 1, -1).expand(H, G, -1)
+                valid = valid.reshape(H, 1, -1).expand(H, G, -1)
+            ok = valid & (ids >= 0) & (ids < n)
+            sel.scatter_(-1, torch.where(ok, ids, torch.full_like(ids, n)), ok)
+            sel = sel[..., :n]
+            a = att[li * H:(li + 1) * H][:, None, :].expand(H, G, n)
+            rec.append(sel.gather(-1, order_idx[..., :k_eff]).sum(-1).double() / max(k_eff, 1))
+            hit.append(a.gather(-1, order_all).sum(-1).double() / k_all)
+            mass.append((w * a).sum(-1))
+            o = out[layer].double().reshape(H, G, -1)
+            rel.append(torch.linalg.norm(o - ref, dim=-1) / torch.linalg.norm(ref, dim=-1).clamp_min(1e-300))
+        f = lambda xs: float(torch.cat([x.reshape(-1) for x in xs]).mean())   # noqa: E731
+        return f(rec), f(hit), f(mass), f(rel)
 
     def _metrics(self, token) -> StepMetrics:
         cfg = self.cfg

@@ -223,6 +223,14 @@ class DeviceForest:
         N.check(N.lib().icb_pages_from_tokens(self.h, _ptr(tr), n, _ptr(src_rows), _ptr(ids), _ptr(counts), G, ks,
                                               _ptr(out_pages), out_pages.shape[1], _ptr(out_npages), _stream()))
 
+    def attended_mask(self, trees, pages, npages, out):
+        """out uint8 [n, tok_cap]: 1 for tokens of the sink, window and
+        selected pages of each tree (the attended set)."""
+        tr = self._trees(trees)
+        N.check(N.lib().icb_attended_mask(self.h, _ptr(tr), tr.numel(), _ptr(pages), pages.shape[1], _ptr(npages),
+                                          _ptr(out), _stream()))
+        return out
+
     def rotate_window(self, trees, scalar_bytes=4, stats=None):
         tr = self._trees(trees)
         N.check(N.lib().icb_rotate_window(self.h, _ptr(tr), tr.numel(), scalar_bytes, _ptr(stats), _stream()))

@@ -110,6 +110,13 @@ def engine_cases():
         ("reuse", dict(n_tokens=1024 + 40, d=32, d_prime=16, clusters=8, layers=8, kv_heads=2,
                        query_heads_per_group=2, seed=11),
          dict(token_budget=24, skip_layers=2, reuse_stride=3), 1024, 40),
+        # evaluation metrics (engine.py:536-566): recall / hit rate / mass / error
+        ("eval", dict(n_tokens=700, d=32, d_prime=16, clusters=8, layers=3, kv_heads=2,
+                      query_heads_per_group=2, seed=3),
+         dict(token_budget=24, skip_layers=1, evaluate=True), 512, 20),
+        ("eval_reuse", dict(n_tokens=1024 + 40, d=32, d_prime=16, clusters=8, layers=8, kv_heads=2,
+                            query_heads_per_group=2, seed=11),
+         dict(token_budget=24, skip_layers=2, reuse_stride=3, evaluate=True), 1024, 20),
     ]
 
 

@@ -113,3 +113,34 @@ def test_cuda_graph_replay_matches_eager(cuda_ok):
             for g in range(c1.shape[1]):
                 assert list(i1[tr, g, :c1[tr, g]]) == list(i2[tr, g, :c2[tr, g]]), t
     assert set(graph._graphs) == {False, True}   # both variants captured and replayed
+
+
+@pytest.mark.parametrize("name", ["eval", "eval_reuse"])
+def test_engine_evaluation_metrics(cuda_ok, name):
+    """evaluate=True (engine.py:536-566) on the device: recall@k, page hit rate,
+    covered attention mass and relative error against the reference's golden
+    step metrics (set metrics exact up to fp64 near-ties; mass / error within
+    fp32-output tolerance)."""
+    from paper_2604_10539_b200.engine import Engine, EngineConfig
+    z, meta = load_golden(f"engine_{name}.npz")
+    sk, ck = meta["spec"], meta["cfg"]
+    keys, values, queries, _ = generate(Spec(kind="clustered", **sk))
+    shape = dict(layers=sk["layers"], kv_heads=sk["kv_heads"], query_heads_per_group=sk["query_heads_per_group"],
+                 d=sk["d"], d_prime=sk["d_prime"], seed=sk["seed"])
+    n0 = meta["n_prefill"]
+    eng = Engine(EngineConfig(**shape, **ck, kv_dtype="fp32", max_tokens=n0 + meta["steps"] + 1)).prefill(
+        keys, values, n0)
+    k = ck["token_budget"]
+    for t in range(meta["steps"]):
+        tok = n0 + t
+        out, m = eng.decode_step(tok, queries[tok], keys[tok], values[tok])
+        row = meta["rows"][t]
+        for key in KEYS:
+            assert getattr(m, key) == row[key], (t, key)
+        assert abs(m.recall_at_k - row["recall_at_k"]) <= 1.0 / k + 1e-9, (t, m.recall_at_k, row["recall_at_k"])
+        assert abs(m.page_hit_rate - row["page_hit_rate"]) <= 1.0 / k + 1e-9, (t, m.page_hit_rate)
+        assert abs(m.covered_attention_mass - row["covered_attention_mass"]) < 1e-6, t
+        assert abs(m.approx_rel_error - row["approx_rel_error"]) < 1e-4 * max(1.0, row["approx_rel_error"]), t
+        ref = z["outputs"][t]
+        o = out.cpu().numpy()
+        assert (np.linalg.norm(o - ref, axis=-1) / np.linalg.norm(ref, axis=-1)).max() < 1e-3
