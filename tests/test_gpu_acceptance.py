@@ -149,3 +149,26 @@ def test_odd_shapes_match_oracle(cuda_ok, G, d):
                 assert list(ids[h, g, :counts[h, g]]) == trace["tokens"][(1, h * G + g)]
         o = out.cpu().numpy()
         assert (np.linalg.norm(o - oout, axis=-1) / np.linalg.norm(oout, axis=-1)).max() < 1e-3
+
+
+def test_selection_reuse_acceptance(cuda_ok):
+    """Acceptance 9 (reference tests/test_acceptance.py:210-238) on the device:
+    reuse stride 3 issues ceil(6/3) = 2 DCI queries per step (6 vanilla) and
+    loses at most 0.10 recall (evaluate=True metrics computed on the device)."""
+    sk = dict(n_tokens=4100, d=64, d_prime=32, clusters=32, cluster_spread=0.1, layers=8, kv_heads=1, seed=109)
+    keys, values, queries, _ = generate(Spec(kind="clustered", **sk))
+    base = dict(layers=8, kv_heads=1, d=64, d_prime=32, token_budget=64, evaluate=True, seed=109)
+    recalls, queries_per_step = {}, {}
+    for label, stride in (("vanilla", 0), ("reuse", 3)):
+        eng = _engine({}, reuse_stride=stride, kv_dtype="fp32", max_tokens=4100, **base).prefill(keys, values, 4000)
+        r, qc = [], []
+        for t in range(60):
+            tok = 4000 + t
+            _, m = eng.decode_step(tok, queries[tok], keys[tok], values[tok])
+            r.append(m.recall_at_k)
+            qc.append(m.dci_queries)
+        recalls[label] = float(np.mean(r))
+        queries_per_step[label] = qc
+    assert all(q == 2 for q in queries_per_step["reuse"])
+    assert all(q == 6 for q in queries_per_step["vanilla"])
+    assert recalls["vanilla"] - recalls["reuse"] <= 0.10, recalls
