@@ -995,6 +995,9 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
       // 8 independent (survivor -> own base -> own node) chains per thread
       constexpr int UU = 8;
       const int* ownl = F.own_list + (size_t)t * F.own_cap;
+      unsigned slo[GP], shi[GP];   // survivors' d2 range per head (this thread)
+#pragma unroll
+      for (int h = 0; h < GP; ++h) { slo[h] = 0xffffffffu; shi[h] = 0u; }
       for (int fb = 0; fb < pre[GP]; fb += NT * UU) {   // block-uniform trip count (ballots below)
         const int f0 = fb + tid;
         int gg[UU], x[UU];
@@ -1013,8 +1016,10 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
               // the survivor owns exactly the node it requests here: its key for
               // head g opens g's candidate list (one entry per requested node)
               SS.cand[(size_t)g * SS.ccap + fl - pre[g]] = sk;
-              atomicMin(&GSA[g].lo, (unsigned)(sk >> 32));
-              atomicMax(&GSA[g].hi, (unsigned)(sk >> 32));
+              const unsigned hb = (unsigned)(sk >> 32);
+#pragma unroll
+              for (int h = 0; h < GP; ++h)
+                if (h == g) { slo[h] = min(slo[h], hb); shi[h] = max(shi[h], hb); }
             }
           }
         }
@@ -1032,6 +1037,14 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
           if (lane == 0 && bal) at = atomicAdd(&S.U, __popc(bal));
           at = __shfl_sync(0xffffffffu, at, 0);
           if (fresh) SS.ulist[at + __popc(bal & ((1u << lane) - 1))] = x[u];
+        }
+      }
+      if (oskip) {   // one shared atomic per head per warp (redux over the warp first)
+#pragma unroll
+        for (int h = 0; h < GP; ++h) {
+          const unsigned lo_w = __reduce_min_sync(0xffffffffu, slo[h]);
+          const unsigned hi_w = __reduce_max_sync(0xffffffffu, shi[h]);
+          if (lane == 0 && h < G && hi_w >= lo_w) { atomicMin(&GSA[h].lo, lo_w); atomicMax(&GSA[h].hi, hi_w); }
         }
       }
       __syncthreads();
@@ -1053,6 +1066,8 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
     int* stage_up = reinterpret_cast<int*>(RG.ring);   // [NT * NPT] (the ring is idle outside the stream)
     int* stage_off = stage_up + NT * NPT;
     int* stage_opos = stage_off + NT * NPT;
+    int* row_node = stage_opos + NT * NPT;   // row -> node of the pass (direct lookup when it fits)
+    constexpr int kRowNodeCap = (kRing * ICB_ROWF * 4) / 4 - 3 * NT * NPT;
     // start level 2: the upper list is exactly the row set (every entry has
     // top >= 2); the stream reads tokens from it directly (no row list)
     const bool rows_from_upper = lv == start && start == 2 && start < L;
@@ -1125,6 +1140,8 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
         v[GP] += sz[u];
       }
       block_scan_multi<NT, GP + 1>(v, ex, tot, S.wsum2);
+      const int r0p = S.scan_carry[GP];          // rows before this pass
+      const bool direct = tot[GP] <= kRowNodeCap;
       int run[GP + 1];
 #pragma unroll
       for (int g = 0; g <= GP; ++g) run[g] = S.scan_carry[g] + ex[g];
@@ -1142,6 +1159,8 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
         stage_up[i - base] = run[GP];     // row prefix / member offset of the pass's nodes (idle ring smem)
         stage_off[i - base] = off[u];
         stage_opos[i - base] = skip_owner ? op[u] : 0x7fffffff;
+        if (direct)
+          for (int j = 0; j < s; ++j) row_node[run[GP] - r0p + j] = i - base;
         run[GP] += s;
       }
       __syncthreads();
@@ -1156,12 +1175,16 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const int r = rb + u * NT;
-            int lo = 0, hi = nn;   // first index with prefix > r, minus one
-            while (lo < hi) {
-              const int mid = (lo + hi) >> 1;
-              if (stage_up[mid] <= r) lo = mid + 1; else hi = mid;
+            if (direct) {
+              ix[u] = r < r1 ? row_node[r - r0] : 0;
+            } else {
+              int lo = 0, hi = nn;   // first index with prefix > r, minus one
+              while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (stage_up[mid] <= r) lo = mid + 1; else hi = mid;
+              }
+              ix[u] = lo - 1;
             }
-            ix[u] = lo - 1;
             if (r < r1) {
               const int j = r - stage_up[ix[u]];   // member index with the owner skipped
               src[u] = stage_off[ix[u]] + j + (j >= stage_opos[ix[u]] ? 1 : 0);
