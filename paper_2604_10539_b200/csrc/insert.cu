@@ -37,6 +37,9 @@ struct InsertArgs {
 };
 
 __device__ unsigned long long g_insert_prof[8];
+// per-tree rotation cycles (ICB_PROF): the kernel ends with its slowest tree
+__device__ unsigned long long g_insert_tree_cycles[4096];
+__device__ unsigned g_insert_tree_fallbacks[4096];
 
 __device__ int new_node(const ForestView& F, int t, int level, int parent, int owner, int first_member) {
   TreeMeta* m = F.meta + t;
@@ -421,6 +424,7 @@ __device__ void insert_points(SearchSmem& S, GroupSmem* GSA, const RingView& RG,
     }
     for (int w = 0; w < nsearch; ++w) {
       if (!s_ok[w]) {   // block-uniform; rare (a node the reference visits with P-DCI)
+        if (prof && tid == 0 && t < 4096) atomicAdd(&g_insert_tree_fallbacks[t], 1u);
         const int par = block_parent_search<NT>(S, GSA, RG, F, SS, t, w, w < nr ? 2 : single + 1, dirs_tmp);
         if (tid == 0) s_par[w] = par;
         __syncthreads();
@@ -542,6 +546,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) insert_kernel(ForestView F, Inse
     if (old < 0) return;
     // the oldest window page's entries in slot order; raw keys were stashed in
     // the tokens' lifted rows, K/V are copied from the page slot
+    const long long tt0 = clock64();
     insert_points<NT>(S, GSA, RG, F, SS, t, dirs_tmp, s_fill, [&](int e) {
       InsertPoint p;
       p.tok = F.page_tok[F.pg(t, old) * F.s + e];
@@ -551,6 +556,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) insert_kernel(ForestView F, Inse
       p.given_level = 0;
       return p;
     }, (int32_t*)nullptr, A.prof);
+    if (A.prof && threadIdx.x == 0 && t < 4096) g_insert_tree_cycles[t] += (unsigned long long)(clock64() - tt0);
     if (threadIdx.x == 0) {
       // release (pagestore.py:157-162) then a fresh window page
       F.page_role[F.pg(t, old)] = 0;
@@ -706,6 +712,14 @@ int icb_resident_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t ro
 
 // Insert phase cycle counters (enabled by ICB_PROF=1): prepare, warp
 // searches, block fallbacks, finish/place, segments.
+extern "C" int icb_insert_tree_profile(unsigned long long* cycles, unsigned* fallbacks, int n) {
+  ICB_CUDA(cudaDeviceSynchronize());
+  n = n < 4096 ? n : 4096;
+  ICB_CUDA(cudaMemcpyFromSymbol(cycles, g_insert_tree_cycles, sizeof(unsigned long long) * n));
+  ICB_CUDA(cudaMemcpyFromSymbol(fallbacks, g_insert_tree_fallbacks, sizeof(unsigned) * n));
+  return ICB_OK;
+}
+
 extern "C" int icb_insert_profile(unsigned long long* out, int reset) {
   ICB_CUDA(cudaDeviceSynchronize());
   ICB_CUDA(cudaMemcpyFromSymbol(out, g_insert_prof, sizeof(unsigned long long) * 8));

@@ -50,3 +50,16 @@ if os.environ.get("ICB_PROF"):
     nrot = len(ms) * eng.T
     print("per tree-rotation us: prepare %.1f search %.1f fallback %.1f finish %.1f | segments %.2f" % (
         *(buf[i] / nrot / 1.9e3 for i in range(4)), buf[4] / nrot))
+
+    cyc = np.zeros(eng.T, dtype=np.uint64)
+    fb = np.zeros(eng.T, dtype=np.uint32)
+    lib.icb_insert_tree_profile.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+    lib.icb_insert_tree_profile(cyc.ctypes.data_as(ctypes.c_void_p), fb.ctypes.data_as(ctypes.c_void_p), eng.T)
+    us = cyc / len(ms) / 1.9e3
+    order = np.argsort(-us)
+    print("per-tree rotation us: mean %.1f  p50 %.1f  p90 %.1f  max %.1f" % (us.mean(), np.median(us),
+                                                                          np.percentile(us, 90), us.max()))
+    print("slowest trees (us, fallbacks/rotation):", [(int(t), round(float(us[t]), 1), round(fb[t] / len(ms), 2))
+                                                      for t in order[:8]])
+    print("mean fallbacks per tree-rotation %.2f; slowest-10%% trees %.2f" % (fb.mean() / len(ms),
+                                                                          fb[order[:24]].mean() / len(ms)))
