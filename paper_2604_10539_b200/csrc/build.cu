@@ -11,6 +11,8 @@
 #include "icb.cuh"
 #include "internal.h"
 #include <cub/cub.cuh>
+#include <cuda_fp16.h>
+#include <climits>
 
 namespace icb {
 
@@ -320,6 +322,336 @@ __global__ void __launch_bounds__(256) nn_parent_kernel(ForestView F, BuildArgs 
   }
 }
 
+// ---------------------------------------------------------------- K2' filtered exact 1-NN
+// The argmin of nn_parent_kernel, found without evaluating every candidate in
+// fp64.  Two passes over the candidates of the point's level:
+//  pass 0: tensor-core (mma.sync f16 x f16 -> f32) approximate
+//          d2~ = |c|^2 - 2 p.c and its per-point minimum m~;
+//  pass 1: the same d2~ again; every candidate with d2~ <= m~ + W gets the
+//          exact fp64 d2 of nn_parent_kernel (the same sequential FMA chain,
+//          evaluated by the thread holding that accumulator), and the exact
+//          (d2, index) minimum wins, first index on ties.
+// Exactness: lifted rows have norm <= 1, so |d2~ - d2| <= E with
+//   E = 2 * (2^-10 [f16 rounding of both operands] + 129 * 2^-18 [f32 tensor
+//   accumulation, generous]) + 2^-20 [epilogue] < 3.0e-3.
+// The exact argmin j* satisfies d2~(j*) <= d2(j*) + E <= d2(j~) + E <= m~ + 2E,
+// and so does every exact tie of it, so W = 2E rounded up keeps them all.  The
+// window costs nothing in correctness, only verification work (on clustered
+// 128-d keys about 80 candidates per point fall inside it, of ~3k).
+#define NF_K 144                 // (dim + 1) padded to a multiple of 16
+#define NF_KS (NF_K + 8)         // smem row stride (halves): conflict-free ldmatrix
+#define NF_BM 64
+#define NF_BN 128
+#define NF_WINDOW 6.5e-3f
+#define NF_CAP 256               // window hits kept per point; more -> verify all candidates
+
+// ICB_PROF diagnostics: points verified, exact chains run, windows that overflowed
+__device__ unsigned long long g_build_prof[4];
+
+// one warp per row: lifted fp64 point rows (p64, for verification) and f16
+// copies of point and candidate rows, zero padded to NF_K
+__global__ void nn_half_kernel(ForestView F, BuildArgs A, const double* nsq, const int* pts,
+                               const int* pts_off, const double* cand64, const int* cand_off, int stride,
+                               double* p64, __half* p16, __half* c16) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.y;
+  const int t = A.trees[b];
+  const int L = F.meta[t].levels;
+  if (L < 2) return;
+  const int r = blockIdx.x * 8 + warp;
+  const int npts = pts_off[(size_t)b * 64 + L];
+  const int ncand = cand_off[(size_t)b * 64 + L];
+  if (r < npts) {
+    double* row = p64 + ((size_t)b * A.n_points + r) * (ICB_DPAD + 1);
+    lift64_row(F, A, b, pts[(size_t)b * A.n_points + r], F.meta[t].c, nsq, row, lane, 32);
+    __syncwarp();
+    __half* dst = p16 + ((size_t)b * A.n_points + r) * NF_K;
+    for (int u = lane; u < NF_K; u += 32) dst[u] = __double2half(u <= F.dim ? row[u] : 0.0);
+  }
+  if (r < ncand && r < stride) {
+    const double* src = cand64 + ((size_t)b * stride + r) * (ICB_DPAD + 1);
+    __half* dst = c16 + ((size_t)b * stride + r) * NF_K;
+    for (int u = lane; u < NF_K; u += 32) dst[u] = __double2half(u <= F.dim ? src[u] : 0.0);
+  }
+}
+
+__device__ __forceinline__ void ldsm_x4(unsigned addr, unsigned& r0, unsigned& r1, unsigned& r2, unsigned& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float* c, const unsigned* a, unsigned b0, unsigned b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+               "{%0,%1,%2,%3};\n"
+               : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ int f2ord(float f) {   // order-preserving float -> int
+  int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
+
+__device__ __forceinline__ void nn_better(double d, int j, double& best, int& arg) {
+  if (arg < 0 || d < best || (d == best && j < arg)) { best = d; arg = j; }
+}
+
+struct NfSmem {
+  __half a[NF_BM][NF_KS];
+  __half bt[2][NF_BN][NF_KS];
+  float csq[2][NF_BN];
+  int rmin[NF_BM];
+  int lv[NF_BM];
+  int cnt[NF_BM];                  // window hits per row
+};
+
+// One warp per point entry: the exact fp64 d2 of nn_parent_kernel over the
+// point's window hits (all of its level's candidates when the window held more
+// than NF_CAP), first index on ties.  The point row is broadcast from smem.
+template <typename IdxT>
+__global__ void __launch_bounds__(128) nn_verify_kernel(ForestView F, BuildArgs A, const int* pts,
+                                                        const int* pts_off, const int* cands, const int* cand_off,
+                                                        const double* p64, const double* cand64,
+                                                        const double* cand_sq, int stride, const IdxT* list,
+                                                        const int* cnt, int* parent_pos,
+                                                        unsigned long long* prof) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.y;
+  const int t = A.trees[b];
+  const int L = F.meta[t].levels;
+  if (L < 2) return;
+  const int e = blockIdx.x * 4 + warp;
+  const int npts = pts_off[(size_t)b * 64 + L];
+  if (e >= npts) return;
+  // per warp: the point row (broadcast) and two 32-candidate x 32-coordinate
+  // chunks of candidate rows (cp.async double buffer over the flattened
+  // (round of 32 candidates, coordinate chunk) sequence); every lane runs one
+  // candidate's sequential chain through the chunks, acc in its register
+  extern __shared__ double nv_smem[];
+  double* p = nv_smem + warp * (ICB_DPAD + 1);
+  double (*T)[32][33] = reinterpret_cast<double (*)[32][33]>(nv_smem + 4 * (ICB_DPAD + 1)) + warp * 2;
+  const int D1 = F.dim + 1;
+  const double* src = p64 + ((size_t)b * A.n_points + e) * (ICB_DPAD + 1);
+  for (int u = lane; u < D1; u += 32) p[u] = src[u];
+  int lv = 1;
+  while (lv < L - 1 && pts_off[(size_t)b * 64 + lv + 1] <= e) ++lv;
+  const int c0 = cand_off[(size_t)b * 64 + lv];
+  const int nc = cand_off[(size_t)b * 64 + lv + 1] - c0;
+  const int c = cnt[(size_t)b * A.n_points + e];
+  const bool all = c > NF_CAP;
+  const int m = all ? nc : c;
+  const double* c64base = cand64 + ((size_t)b * stride + c0) * (ICB_DPAD + 1);
+  const IdxT* lst = list + ((size_t)b * A.n_points + e) * NF_CAP;
+  if (prof && lane == 0) {
+    atomicAdd(prof + 0, 1ull);
+    atomicAdd(prof + 1, (unsigned long long)m);
+    atomicAdd(prof + 2, all ? 1ull : 0ull);
+  }
+  double best = 0.0;
+  int arg = -1;
+  // chunks of 32 coordinates; a final remainder of 1 joins the last chunk (33 wide)
+  const int nch = D1 > 32 && D1 % 32 == 1 ? D1 >> 5 : (D1 + 31) >> 5;
+  auto chunk_w = [&](int ch) { return ch == nch - 1 ? D1 - ch * 32 : 32; };
+  const int steps = ((m + 31) >> 5) * nch;
+  auto cand = [&](int rd) -> int {
+    const int i = rd * 32 + lane;
+    return i < m ? (all ? i : (int)lst[i]) : 0;
+  };
+  auto issue = [&](int st) {
+    const int rd = st / nch, u0 = (st - rd * nch) * 32;
+    const int nr = min(32, m - rd * 32), un = chunk_w(st - rd * nch);
+    const int jl = cand(rd);
+    double (*B)[33] = T[st & 1];
+    for (int r = 0; r < nr; ++r) {
+      const int j = __shfl_sync(0xffffffffu, jl, r);
+      const double* row = c64base + (size_t)j * (ICB_DPAD + 1) + u0;
+      if (lane < un)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(&B[r][lane])), "l"(row + lane));
+      if (lane == 0 && un == 33)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(&B[r][32])), "l"(row + 32));
+    }
+    asm volatile("cp.async.commit_group;\n");
+  };
+  if (steps > 0) issue(0);
+  int jr = cand(0);
+  double acc = 0.0;
+  for (int st = 0; st < steps; ++st) {
+    if (st + 1 < steps) {
+      issue(st + 1);
+      asm volatile("cp.async.wait_group 1;\n");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n");
+    }
+    __syncwarp();
+    const int rd = st / nch, ch = st - rd * nch, u0 = ch * 32;
+    const int nr = min(32, m - rd * 32), un = chunk_w(ch);
+    if (ch == 0) { acc = 0.0; jr = cand(rd); }
+    const double (*B)[33] = T[st & 1];
+    if (lane < nr) {
+      if (un == 32) {
+#pragma unroll
+        for (int u = 0; u < 32; ++u) acc = __fma_rn(p[u0 + u], B[lane][u], acc);
+      } else {
+        for (int u = 0; u < un; ++u) acc = __fma_rn(p[u0 + u], B[lane][u], acc);
+      }
+      if (ch == nch - 1)
+        nn_better(__dsub_rn(cand_sq[(size_t)b * stride + c0 + jr], __dmul_rn(2.0, acc)), jr, best, arg);
+    }
+    __syncwarp();   // buffer st & 1 is refilled by issue(st + 2)
+  }
+  for (int o = 16; o; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+    if (oa >= 0) nn_better(ob, oa, best, arg);
+  }
+  if (lane == 0 && arg >= 0)
+    parent_pos[(size_t)b * A.n_points + pts[(size_t)b * A.n_points + e]] = cands[(size_t)b * A.n_points + c0 + arg];
+}
+
+// Block: NF_BM point entries x all candidates of their level, NF_BN at a time;
+// 8 warps = 4 (16 rows) x 2 (64 candidates).
+template <typename IdxT>
+__global__ void __launch_bounds__(256, 2) nn_filter_kernel(ForestView F, BuildArgs A, const int* pts_off,
+                                                          const int* cand_off, const __half* p16,
+                                                          const __half* c16, const double* cand_sq, int stride,
+                                                          IdxT* list, int* cnt) {
+  extern __shared__ __align__(16) unsigned char nf_raw[];
+  NfSmem& S = *reinterpret_cast<NfSmem*>(nf_raw);
+  const int b = blockIdx.y;
+  const int t = A.trees[b];
+  const int L = F.meta[t].levels;
+  if (L < 2) return;
+  const int npts = pts_off[(size_t)b * 64 + L];
+  const int e0 = blockIdx.x * NF_BM;
+  if (e0 >= npts) return;
+  const int e1 = min(npts, e0 + NF_BM);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = warp & 3, wn = warp >> 2;
+  for (int e = e0 + tid; e < e0 + NF_BM; e += blockDim.x) {
+    int lv = -1;
+    if (e < e1) {
+      lv = 1;
+      while (lv < L - 1 && pts_off[(size_t)b * 64 + lv + 1] <= e) ++lv;
+    }
+    S.lv[e - e0] = lv;
+  }
+  // A tile (rows past e1 repeat the last row; masked below)
+  for (int x = tid; x < NF_BM * (NF_K / 8); x += blockDim.x) {
+    const int r = x / (NF_K / 8), ch = x % (NF_K / 8);
+    const int e = min(e0 + r, e1 - 1);
+    cp_async16(&S.a[r][ch * 8], p16 + ((size_t)b * A.n_points + e) * NF_K + ch * 8);
+  }
+  asm volatile("cp.async.commit_group;\n");
+  __syncthreads();
+  const __half* cbase = c16 + (size_t)b * stride * NF_K;
+  const double* sqbase = cand_sq + (size_t)b * stride;
+  // rows of this thread's fragments: r_lo = wm*16 + lane/4, r_hi = r_lo + 8
+  const int r_lo = wm * 16 + (lane >> 2), r_hi = r_lo + 8;
+  int seg = e0;
+  while (seg < e1) {
+    const int lv = S.lv[seg - e0];
+    int segend = seg;
+    while (segend < e1 && S.lv[segend - e0] == lv) ++segend;
+    const int c0 = cand_off[(size_t)b * 64 + lv];
+    const int nc = cand_off[(size_t)b * 64 + lv + 1] - c0;
+    const int ntile = (nc + NF_BN - 1) / NF_BN;
+    if (ntile == 0) { seg = segend; continue; }
+    __syncthreads();
+    for (int x = tid; x < NF_BM; x += blockDim.x) {
+      S.rmin[x] = INT_MAX;
+      S.cnt[x] = 0;
+    }
+    auto stage = [&](int tile, int buf) {
+      const int j0 = tile * NF_BN;
+      for (int x = tid; x < NF_BN * (NF_K / 8); x += blockDim.x) {
+        const int r = x / (NF_K / 8), ch = x % (NF_K / 8);
+        const int j = min(j0 + r, nc - 1);
+        cp_async16(&S.bt[buf][r][ch * 8], cbase + (size_t)(c0 + j) * NF_K + ch * 8);
+      }
+      for (int x = tid; x < NF_BN; x += blockDim.x)
+        S.csq[buf][x] = j0 + x < nc ? (float)sqbase[c0 + j0 + x] : 0.f;
+      asm volatile("cp.async.commit_group;\n");
+    };
+    const bool ok_lo = e0 + r_lo >= seg && e0 + r_lo < segend;
+    const bool ok_hi = e0 + r_hi >= seg && e0 + r_hi < segend;
+    for (int pass = 0; pass < 2; ++pass) {
+      float thr_lo = 0.f, thr_hi = 0.f;
+      if (pass == 1) {
+        thr_lo = ord2f(S.rmin[r_lo]) + NF_WINDOW;
+        thr_hi = ord2f(S.rmin[r_hi]) + NF_WINDOW;
+      }
+      float m_lo = INFINITY, m_hi = INFINITY;
+      __syncthreads();
+      stage(0, 0);
+      for (int tile = 0; tile < ntile; ++tile) {
+        const int buf = tile & 1;
+        if (tile + 1 < ntile) {
+          stage(tile + 1, buf ^ 1);
+          asm volatile("cp.async.wait_group 1;\n");
+        } else {
+          asm volatile("cp.async.wait_group 0;\n");
+        }
+        __syncthreads();
+        float acc[8][4];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.f;
+        const int mi = lane >> 3, ri = lane & 7;
+#pragma unroll
+        for (int k0 = 0; k0 < NF_K; k0 += 16) {
+          unsigned a[4];
+          ldsm_x4(smem_u32(&S.a[wm * 16 + ri + 8 * (mi & 1)][k0 + 8 * (mi >> 1)]), a[0], a[1], a[2], a[3]);
+#pragma unroll
+          for (int q = 0; q < 8; q += 2) {
+            unsigned b0, b1, b2, b3;
+            ldsm_x4(smem_u32(&S.bt[buf][wn * 64 + (q + (mi >> 1)) * 8 + ri][k0 + 8 * (mi & 1)]), b0, b1, b2, b3);
+            mma16816(acc[q], a, b0, b1);
+            mma16816(acc[q + 1], a, b2, b3);
+          }
+        }
+        const int jt = tile * NF_BN;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int jl = wn * 64 + q * 8 + 2 * (lane & 3) + h;
+            const int j = jt + jl;
+            const float cs = S.csq[buf][jl];
+            const float d_lo = cs - 2.f * acc[q][h], d_hi = cs - 2.f * acc[q][2 + h];
+            if (pass == 0) {
+              if (j < nc) {
+                m_lo = fminf(m_lo, d_lo);
+                m_hi = fminf(m_hi, d_hi);
+              }
+            } else {
+              if (j < nc && ok_lo && d_lo <= thr_lo) {
+                const int k = atomicAdd(&S.cnt[r_lo], 1);
+                if (k < NF_CAP) list[((size_t)b * A.n_points + e0 + r_lo) * NF_CAP + k] = (IdxT)j;
+              }
+              if (j < nc && ok_hi && d_hi <= thr_hi) {
+                const int k = atomicAdd(&S.cnt[r_hi], 1);
+                if (k < NF_CAP) list[((size_t)b * A.n_points + e0 + r_hi) * NF_CAP + k] = (IdxT)j;
+              }
+            }
+          }
+        }
+        __syncthreads();   // buffer `buf` is restaged by the next iteration
+      }
+      if (pass == 0) {
+        m_lo = fminf(m_lo, __shfl_xor_sync(0xffffffffu, m_lo, 1));
+        m_lo = fminf(m_lo, __shfl_xor_sync(0xffffffffu, m_lo, 2));
+        m_hi = fminf(m_hi, __shfl_xor_sync(0xffffffffu, m_hi, 1));
+        m_hi = fminf(m_hi, __shfl_xor_sync(0xffffffffu, m_hi, 2));
+        if ((lane & 3) == 0) {
+          atomicMin(&S.rmin[r_lo], f2ord(m_lo));
+          atomicMin(&S.rmin[r_hi], f2ord(m_hi));
+        }
+      }
+    }
+    __syncthreads();
+    if (tid < NF_BM && e0 + tid >= seg && e0 + tid < segend) cnt[(size_t)b * A.n_points + e0 + tid] = S.cnt[tid];
+    seg = segend;
+  }
+}
+
 // ---------------------------------------------------------------- K3 nodes
 // entry key: tree(12) | (63 - lv)(6) | firstpos(23) | pos(23)
 __device__ __forceinline__ unsigned long long node_key(int b, int lv, int fp, int pos) {
@@ -569,6 +901,15 @@ int icb_build_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t n_poi
   A.scales = scales;
   // scratch
   Scratch S(st);
+  {
+    // keep build scratch mapped between calls (a prefill issues several builds)
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      unsigned long long thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   double* nsq = S.alloc<double>((size_t)n * P);
   unsigned long long* maxbits = S.alloc<unsigned long long>(n);
   int* top = S.alloc<int>((size_t)n * P);
@@ -603,12 +944,47 @@ int icb_build_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t n_poi
   if (!S.ok()) return S.fail();
   build_cand64_kernel<<<dim3((stride + 7) / 8, n), 256, 0, st>>>(F, A, nsq, cands, cand_off, cand64,
                                                                  cand_sq, stride);
-  {
+  static const bool exact_only = getenv("ICB_BUILD_EXACT_NN") != nullptr;   // A/B and test knob
+  if (exact_only || F.dim + 1 > NF_K) {
     const int D1 = F.dim + 1, PS = D1 | 1;
     size_t sm = sizeof(double) * (NN_BM * PS + NN_BN * (NN_KC + 1));
     ICB_CUDA(cudaFuncSetAttribute(nn_parent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     nn_parent_kernel<<<dim3((P + NN_BM - 1) / NN_BM, n), 256, sm, st>>>(
         F, A, nsq, pts, pts_off, cands, cand_off, cand64, cand_sq, stride, parent_pos);
+  } else {
+    double* p64 = S.alloc<double>((size_t)n * P * (ICB_DPAD + 1));
+    __half* p16 = S.alloc<__half>((size_t)n * P * NF_K);
+    __half* c16 = S.alloc<__half>((size_t)n * stride * NF_K);
+    int* nf_cnt = S.alloc<int>((size_t)n * P);
+    if (!S.ok()) return S.fail();
+    unsigned long long* prof = nullptr;
+    if (getenv("ICB_PROF")) ICB_CUDA(cudaGetSymbolAddress((void**)&prof, g_build_prof));
+    nn_half_kernel<<<dim3((P + 7) / 8, n), 256, 0, st>>>(F, A, nsq, pts, pts_off, cand64, cand_off, stride, p64,
+                                                         p16, c16);
+    // candidate indices of a level are < P: 16-bit lists when they fit
+    auto run = [&](auto* list) -> int {
+      using IdxT = typename std::remove_pointer<decltype(list)>::type;
+      const int sm = (int)sizeof(NfSmem);
+      ICB_CUDA(cudaFuncSetAttribute(nn_filter_kernel<IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      nn_filter_kernel<IdxT><<<dim3((P + NF_BM - 1) / NF_BM, n), 256, sm, st>>>(
+          F, A, pts_off, cand_off, p16, c16, cand_sq, stride, list, nf_cnt);
+      const int nv_sm = (int)sizeof(double) * (4 * (ICB_DPAD + 1) + 4 * 2 * 32 * 33);
+      ICB_CUDA(cudaFuncSetAttribute(nn_verify_kernel<IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize, nv_sm));
+      nn_verify_kernel<IdxT><<<dim3((P + 3) / 4, n), 128, nv_sm, st>>>(
+          F, A, pts, pts_off, cands, cand_off, p64, cand64, cand_sq, stride, list, nf_cnt, parent_pos, prof);
+      return ICB_OK;
+    };
+    int rc;
+    if (P <= 65536) {
+      unsigned short* l16 = S.alloc<unsigned short>((size_t)n * P * NF_CAP);
+      if (!S.ok()) return S.fail();
+      rc = run(l16);
+    } else {
+      int* l32 = S.alloc<int>((size_t)n * P * NF_CAP);
+      if (!S.ok()) return S.fail();
+      rc = run(l32);
+    }
+    if (rc != ICB_OK) return rc;
   }
   // node construction
   int* firstpos = S.alloc<int>((size_t)n * P);
@@ -679,4 +1055,14 @@ int icb_build_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t n_poi
   build_summary_kernel<<<n, 256, 0, st>>>(F, A);
   ICB_CUDA(cudaGetLastError());
   return S.finish();
+}
+
+extern "C" int icb_build_profile(unsigned long long* out, int reset) {
+  ICB_CUDA(cudaDeviceSynchronize());
+  ICB_CUDA(cudaMemcpyFromSymbol(out, icb::g_build_prof, sizeof(unsigned long long) * 4));
+  if (reset) {
+    unsigned long long z[4] = {};
+    ICB_CUDA(cudaMemcpyToSymbol(icb::g_build_prof, z, sizeof(z)));
+  }
+  return ICB_OK;
 }

@@ -78,6 +78,32 @@ def test_build_matches_oracle(cuda_ok, name):
     assert np.array_equal(ex["tail"][:n], tail32)
 
 
+def _filter_case(kind, n, d, rng):
+    if kind == "duplicates":      # exact ties everywhere: windows overflow, first-index tie break
+        base = rng.standard_normal((24, d))
+        return base[rng.integers(0, 24, n)]
+    if kind == "near_ties":       # every candidate inside the f16 error window
+        return rng.standard_normal(d)[None, :] + 1e-5 * rng.standard_normal((n, d))
+    if kind == "tiny_norms":      # coordinates in f16's subnormal range
+        return rng.standard_normal((n, d)) * 10.0 ** rng.uniform(-6, 0, (n, 1))
+    return rng.standard_normal((n, d)) + 3.0 * rng.standard_normal((8, d))[rng.integers(0, 8, n)]
+
+
+@pytest.mark.parametrize("kind,r", [("duplicates", 0.1), ("near_ties", 0.1), ("tiny_norms", 0.1),
+                                    ("clustered", 0.3)])
+def test_build_parent_filter_edge_cases(cuda_ok, kind, r):
+    """The tensor-core parent filter (build.cu nn_filter_kernel) must pick the
+    exact fp64 1-NN parent, first index on ties, on inputs built to defeat it."""
+    n, d = 3000, 128
+    rng = np.random.default_rng(hash(kind) % 2**32)
+    keys = _filter_case(kind, n, d, rng).astype(np.float32)
+    vals = rng.standard_normal((n, 4)).astype(np.float32)
+    meta = {"n": n, "d": d, "r": r, "seed": 7, "page_size": 16}
+    otree, ostore = _oracle({"keys": keys, "values": vals}, meta)
+    f = _device_build({"keys": keys, "values": vals}, meta, 0)
+    _compare_structure(f, otree, ostore)
+
+
 @pytest.mark.parametrize("name", TREES)
 def test_query_matches_oracle(cuda_ok, name):
     z, meta = load_golden(f"tree_{name}.npz")
