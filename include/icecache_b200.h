@@ -225,6 +225,10 @@ int icb_set_scale(icb_forest *f, int32_t tree, double c);
 /* Host-side restatement check: n PCG64 doubles of SeedSequence(words, spawn). */
 int icb_host_pcg_doubles(const uint32_t *words, int32_t n_words, const uint32_t *spawn,
                          int32_t n_spawn, int32_t n, double *out);
+/* The same stream after a jump of `skip` draws (the LCG jump the device level
+ * draw uses to split the stream across threads). */
+int icb_host_pcg_jump_doubles(const uint32_t *words, int32_t n_words, const uint32_t *spawn,
+                              int32_t n_spawn, int64_t skip, int32_t n, double *out);
 
 #ifdef __cplusplus
 }

@@ -82,6 +82,7 @@ EXPORTS = {
     "icb_read_meta_c": ([P, I32, P], ctypes.c_int),
     "icb_set_scale": ([P, I32, ctypes.c_double], ctypes.c_int),
     "icb_host_pcg_doubles": ([P, I32, P, I32, I32, P], ctypes.c_int),
+    "icb_host_pcg_jump_doubles": ([P, I32, P, I32, ctypes.c_int64, I32, P], ctypes.c_int),
 }
 
 

@@ -85,24 +85,102 @@ __global__ void build_lift_kernel(ForestView F, BuildArgs A, const double* nsq) 
   }
 }
 
-// one thread per tree: draw levels in input order from the continuing stream
-__global__ void build_levels_kernel(ForestView F, BuildArgs A, int* drawn, unsigned long long* occ) {
-  int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= A.n) return;
+// Level draws in input order from the tree's continuing stream (assign_level,
+// dci.py:81-88): point i consumes uniforms until the first one >= r (its
+// "stop"); its level is the number of draws it consumed.  One CTA per tree
+// walks the stream in chunks of NT * LV_K draws -- each thread LV_K
+// consecutive draws from a jump-ahead state -- and assigns the stops to
+// points with a block scan; level = gap to the previous stop.  The stream is
+// left just past point P-1's stop, as the sequential draw leaves it.
+#define LV_K 4
+template <int NT>
+__global__ void __launch_bounds__(NT) build_levels_kernel(ForestView F, BuildArgs A, int* drawn,
+                                                          unsigned long long* occ) {
+  __shared__ int sm[NT / 32 + 1];
+  __shared__ long long smx[NT / 32 + 1];
+  __shared__ unsigned long long s_mask;
+  __shared__ long long s_last;          // draw index of the last stop so far (-1: none)
+  __shared__ int s_done;                // points assigned so far
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   TreeMeta* m = F.meta + A.trees[b];
-  Pcg64 g = m->rng;
-  unsigned long long mask = 0;
-  for (int i = 0; i < A.n_points; ++i) {
-    int lv = icb_draw_level(g, F.r);
-    if (lv > 62) lv = 62;
-    drawn[(size_t)b * A.n_points + i] = lv;
-    mask |= 1ull << lv;
+  const Pcg64 g0 = m->rng;
+  const int P = A.n_points;
+  // threshold on the 53-bit integer: u < r  <=>  (x >> 11) < ceil(r * 2^53)
+  // exactly, since u = (x >> 11) * 2^-53 is exact; compare doubles to be literal
+  const double r = F.r;
+  icb_u128 At, Ct, Ach, Cch;
+  icb_pcg_jump((unsigned long long)tid * LV_K, g0.inc, At, Ct);
+  icb_pcg_jump((unsigned long long)NT * LV_K, g0.inc, Ach, Cch);
+  if (tid == 0) { s_mask = 0; s_last = -1; s_done = 0; }
+  __syncthreads();
+  icb_u128 base = g0.state;             // state before the chunk's first draw
+  long long d0 = 0;                     // index of the chunk's first draw
+  while (s_done < P) {
+    icb_u128 st = At * base + Ct;
+    unsigned stops = 0;                 // bit k: draw d0 + tid*K + k is a stop
+    for (int k = 0; k < LV_K; ++k) {
+      st = st * icb_pcg_mult() + g0.inc;
+      const double u = (double)(icb_pcg_output(st) >> 11) * (1.0 / 9007199254740992.0);
+      if (!(u < r)) stops |= 1u << k;
+    }
+    const int nst = __popc(stops);
+    int tot;
+    const int ex = block_exclusive_scan<NT>(nst, sm, tot);
+    // previous stop before this thread's draws: max over lower threads' last stop
+    long long mylast = stops ? d0 + (long long)tid * LV_K + (31 - __clz(stops)) : -1;
+    long long inc = mylast;
+    for (int o = 1; o < 32; o <<= 1) {
+      long long v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o && v > inc) inc = v;
+    }
+    if (lane == 31) smx[wid] = inc;
+    __syncthreads();
+    long long prev = s_last;
+    for (int w = 0; w < wid; ++w) prev = smx[w] > prev ? smx[w] : prev;
+    {
+      long long v = __shfl_up_sync(0xffffffffu, inc, 1);
+      if (lane > 0 && v > prev) prev = v;
+    }
+    const int done = s_done;
+    unsigned long long mask = 0;
+    int idx = done + ex;
+    for (int k = 0; k < LV_K; ++k) {
+      if (!(stops >> k & 1u)) continue;
+      const long long d = d0 + (long long)tid * LV_K + k;
+      if (idx < P) {
+        int lv = (int)(d - prev);
+        if (lv > 62) lv = 62;
+        drawn[(size_t)b * P + idx] = lv;
+        mask |= 1ull << lv;
+        if (idx == P - 1) {             // leave the stream just past this stop
+          icb_u128 Aj, Cj;
+          icb_pcg_jump((unsigned long long)(d + 1), g0.inc, Aj, Cj);
+          m->rng.state = Aj * g0.state + Cj;
+        }
+      }
+      prev = d;
+      ++idx;
+    }
+    if (mask) atomicOr(&s_mask, mask);
+    __syncthreads();
+    if (tid == NT - 1) {
+      long long last = smx[0];
+      for (int w = 1; w < NT / 32; ++w) last = smx[w] > last ? smx[w] : last;
+      if (last > s_last) s_last = last;
+      s_done = done + tot;
+    }
+    base = Ach * base + Cch;
+    d0 += (long long)NT * LV_K;
+    __syncthreads();
   }
-  m->rng = g;
-  occ[b] = mask;
-  m->levels = __popcll(mask);
-  m->n_points = A.n_points;
-  m->top_node = 0;
+  if (tid == 0) {
+    occ[b] = s_mask;
+    m->levels = __popcll(s_mask);
+    m->n_points = P;
+    m->top_node = 0;
+    if (P == 0) m->rng = g0;
+  }
 }
 
 __global__ void build_compact_kernel(ForestView F, BuildArgs A, int* drawn, const unsigned long long* occ) {
@@ -931,7 +1009,7 @@ int icb_build_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t n_poi
   build_norms_kernel<<<g8, 256, 0, st>>>(F, A, nsq, maxbits);
   build_scale_kernel<<<(n + 127) / 128, 128, 0, st>>>(F, A, maxbits);
   build_lift_kernel<<<g8, 256, 0, st>>>(F, A, nsq);
-  build_levels_kernel<<<(n + 63) / 64, 64, 0, st>>>(F, A, top, occ);
+  build_levels_kernel<1024><<<n, 1024, 0, st>>>(F, A, top, occ);
   dim3 g256((P + 255) / 256, n);
   build_compact_kernel<<<g256, 256, 0, st>>>(F, A, top, occ);
   build_pos_of_kernel<<<g256, 256, 0, st>>>(F, A);

@@ -431,4 +431,16 @@ int icb_host_pcg_doubles(const uint32_t* words, int32_t n_words, const uint32_t*
   return ICB_OK;
 }
 
+int icb_host_pcg_jump_doubles(const uint32_t* words, int32_t n_words, const uint32_t* spawn, int32_t n_spawn,
+                              int64_t skip, int32_t n, double* out) {
+  uint64_t st[4];
+  icb_seedseq_u64x4(words, n_words, spawn, n_spawn, st);
+  Pcg64 g = icb_pcg_seed(st);
+  icb_u128 A, C;
+  icb_pcg_jump((unsigned long long)skip, g.inc, A, C);
+  g.state = A * g.state + C;
+  for (int i = 0; i < n; ++i) out[i] = icb_pcg_double(g);
+  return ICB_OK;
+}
+
 }  // extern "C"

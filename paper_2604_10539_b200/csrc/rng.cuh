@@ -102,6 +102,30 @@ ICB_HD double icb_pcg_double(Pcg64& g) {
   return (double)(icb_pcg_next64(g) >> 11) * (1.0 / 9007199254740992.0);
 }
 
+// LCG jump: the state after `delta` steps is A * state + C (the standard
+// O(log delta) power-of-the-affine-map construction).
+ICB_HD void icb_pcg_jump(unsigned long long delta, icb_u128 inc, icb_u128& A, icb_u128& C) {
+  icb_u128 am = 1, ap = 0, cm = icb_pcg_mult(), cp = inc;
+  while (delta) {
+    if (delta & 1ull) {
+      am *= cm;
+      ap = ap * cm + cp;
+    }
+    cp = (cm + 1) * cp;
+    cm *= cm;
+    delta >>= 1;
+  }
+  A = am;
+  C = ap;
+}
+
+ICB_HD uint64_t icb_pcg_output(icb_u128 state) {
+  uint64_t hi = (uint64_t)(state >> 64), lo = (uint64_t)state;
+  uint64_t x = hi ^ lo;
+  unsigned rot = (unsigned)(hi >> 58);
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
 // assign_level (dci.py:81-88): 1 + number of consecutive uniforms below r.
 ICB_HD int icb_draw_level(Pcg64& g, double r) {
   int level = 1;

@@ -53,6 +53,27 @@ def test_host_seedseq_pcg64_matches_numpy(entropy, spawn):
     assert np.array_equal(out, g.random(64))
 
 
+@pytest.mark.parametrize("skip", [0, 1, 7, 4096, 123457, 2**40 + 3])
+def test_host_pcg64_jump_matches_numpy(skip):
+    """The LCG jump that splits the level-draw stream across device threads
+    (rng.cuh icb_pcg_jump) lands where NumPy's PCG64 does after `skip` draws."""
+    from paper_2604_10539_b200.forest import entropy_words
+    words = np.array(entropy_words([3, 5, 7]), dtype=np.uint32)
+    sp = np.array((0,), dtype=np.uint32)
+    out = np.zeros(16)
+    rc = _lib().icb_host_pcg_jump_doubles(words.ctypes.data_as(ctypes.c_void_p), len(words),
+                                          sp.ctypes.data_as(ctypes.c_void_p), len(sp), skip, len(out),
+                                          out.ctypes.data_as(ctypes.c_void_p))
+    assert rc == 0
+    ss = np.random.SeedSequence([3, 5, 7])
+    bg = np.random.PCG64(np.random.SeedSequence(entropy=ss.entropy, spawn_key=(0,)))
+    if skip < 200000:
+        assert np.array_equal(out, np.random.Generator(bg).random(skip + 16)[skip:])
+    else:
+        bg.advance(skip)
+        assert np.array_equal(out, np.random.Generator(bg).random(16))
+
+
 def test_embedded_ziggurat_tables_are_numpys():
     import importlib.util
     spec = importlib.util.spec_from_file_location("gz", os.path.join(ROOT, "tools", "gen_ziggurat.py"))
