@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--kv", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--layer-serial", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="e2e leg without CUDA graphs")
+    ap.add_argument("--fuse-rotation", action="store_true",
+                    help="rotation steps as one icb_step_attend launch (A/B; off by default)")
     ap.add_argument("--reuse-stride", type=int, default=0,
                     help="selection reuse (anchor layers, engine.py:321-363); 0 = the reference default (off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -144,7 +146,8 @@ def run_ours(args, rank, world):
     stream = clustered_stream(n0, total_steps, C2["layers"], C2["kv_heads"], C2["query_heads_per_group"],
                               C2["d"], C2["d_prime"], seed=args.seed + rank, device=dev)
     cfg = EngineConfig(**C2, seed=args.seed + rank, kv_dtype=args.kv, max_tokens=n0 + total_steps + 1,
-                       layer_serial=args.layer_serial, cuda_graph=graph, reuse_stride=args.reuse_stride)
+                       layer_serial=args.layer_serial, cuda_graph=graph, reuse_stride=args.reuse_stride,
+                       fuse_rotation=args.fuse_rotation)
     t0 = time.time()
     eng = Engine(cfg, device=dev).prefill(stream.keys, stream.values, n0)
     torch.cuda.synchronize()
@@ -192,6 +195,7 @@ def run_ours(args, rank, world):
         return r
 
     f.query, f.attention, f.query_attend = q_wrap, a_wrap, qa_wrap
+    fused_rot = eng.cfg.fuse_rotation and args.reuse_stride < 2
 
     fixed_tok = [0]   # sink + window tokens attended (timed steps)
 
@@ -201,9 +205,12 @@ def run_ours(args, rank, world):
         eng.decode_step(tok, q_all[i], k_all[i], v_all[i], metrics=False)
         if timing["i"] is not None:
             fixed_tok[0] += eng.T * (C2["page_size"] * C2["sink_pages"] + sum(eng._win_fills))
-        # library kernels per step: append, search, paged attention, dense append,
-        # dense attention (+ the rotation insert kernel)
-        launches[0] += 5 + (1 if rot else 0)
+        # library kernels per step: window append, search + paged attention
+        # (reuse: anchor search, pages_from_tokens, paged attention), dense
+        # append, dense attention, + the rotation insert kernel; a fused
+        # rotation step is one launch for rotation + append + search + attention
+        base = 4 if args.reuse_stride < 2 else 6
+        launches[0] += 3 if (rot and fused_rot) else base + (1 if rot else 0)
         return rot
 
     for i in range(W):
@@ -217,6 +224,7 @@ def run_ours(args, rank, world):
     stats0 = eng.stats.sum(0).cpu().numpy().copy()
     launches[0] = 0
     rotations = 0
+    rot_steps = set()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -225,7 +233,10 @@ def run_ours(args, rank, world):
         e0.record(cur)
         for j in range(K):
             timing["i"] = j
-            rotations += step(W + j)
+            r = step(W + j)
+            rotations += r
+            if r:
+                rot_steps.add(j)
         timing["i"] = None
         e1.record(cur)
         torch.cuda.synchronize()
@@ -236,8 +247,11 @@ def run_ours(args, rank, world):
     stats1 = eng.stats.sum(0).cpu().numpy().copy()
     f.check()
     ms_max = rank_max(ms, dev, world)
-    q_ms = [ev_q0[j].elapsed_time(ev_q1[j]) for j in range(K)]
-    a_ms = [ev_q1[j].elapsed_time(ev_a1[j]) for j in range(K)]
+    # the search + attention launch of plain steps (a fused rotation step's
+    # launch also carries that step's inserts and is not a roofline sample)
+    timed = [j for j in range(K) if ev_q1[j].query() and ev_q0[j].query() and j not in rot_steps]
+    q_ms = [ev_q0[j].elapsed_time(ev_q1[j]) for j in timed]
+    a_ms = [ev_q1[j].elapsed_time(ev_a1[j]) for j in timed]
     # algorithmic bytes of the search kernel: 4(d+1) U + 4 E per tree-step
     rows = sum(b["rows_read"] - a["rows_read"] for a, b in zip(info0, info1))
     rere = sum(b["owner_rereads"] - a["owner_rereads"] for a, b in zip(info0, info1))

@@ -120,6 +120,21 @@ int icb_query_attend(icb_forest *f, const int32_t *trees, int32_t n, int32_t G, 
                      int32_t *out_counts, int32_t *out_pages, int32_t pages_cap, int32_t *out_npages,
                      float *attn_out, int64_t *attn_stats, int32_t scalar_bytes, void *stream);
 
+/* One whole decode step of a stage of indexed trees in one launch
+ * (Engine.decode_step, engine.py:412-475, with _rotate_layer, :516-534):
+ * each tree's CTA first rotates its oldest window page into the tree when
+ * `rotate` (as icb_rotate_window; rot_stats dev [n][2] or NULL), then appends
+ * the decode token (as icb_append_window_dev: token_dev, win_keys dev
+ * [n][dim], win_values dev [n][dim_v]), then runs icb_query_attend.  Results
+ * are identical to those four calls in sequence; the step's slowest rotation
+ * no longer holds back every tree's search. */
+int icb_step_attend(icb_forest *f, const int32_t *trees, int32_t n, int32_t G, const float *queries,
+                    int32_t k, int64_t beam, int64_t visit_cap, int32_t *out_ids, int32_t k_out,
+                    int32_t *out_counts, int32_t *out_pages, int32_t pages_cap, int32_t *out_npages,
+                    float *attn_out, int64_t *attn_stats, int32_t scalar_bytes, int32_t rotate,
+                    int64_t *rot_stats, const int32_t *token_dev, const float *win_keys,
+                    const float *win_values, void *stream);
+
 /* Sequential inserts of m points per tree (trees in parallel).  levels dev
  * [n][m] or NULL (draw from the tree's stream); out_levels dev or NULL. */
 int icb_insert(icb_forest *f, const int32_t *trees, int32_t n, int32_t m, const int32_t *tokens,

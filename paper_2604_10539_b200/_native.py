@@ -72,6 +72,8 @@ EXPORTS = {
     "icb_node_query": ([P, I32, I32, P, I32, I64, P, P, P], ctypes.c_int),
     "icb_attended_mask": ([P, P, I32, P, I32, P, P, P], ctypes.c_int),
     "icb_query_attend": ([P, P, I32, I32, P, I32, I64, I64, P, I32, P, P, I32, P, P, P, I32, P], ctypes.c_int),
+    "icb_step_attend": ([P, P, I32, I32, P, I32, I64, I64, P, I32, P, P, I32, P, P, P, I32, I32, P, P, P, P, P],
+                        ctypes.c_int),
     "icb_sparse_attention": ([P, P, I32, I32, P, P, I32, P, P, P, I32, I32, P], ctypes.c_int),
     "icb_dense_attention": ([I32, I32, I32, I32, I32, P, P, P, I64, I32, P, I32, P], ctypes.c_int),
     "icb_tree_info": ([P, I32, P], ctypes.c_int),

@@ -12,15 +12,35 @@ constexpr int kAttnThreads = 256;
 // kernels are instantiated for G in {1,2,4,8}; other GQA ratios run padded
 inline int padded_g(int G) { return G <= 2 ? G : G <= 4 ? 4 : 8; }
 
-template <typename KT>
+// K/V loads: NC = true reads through the non-coherent path (ld.global.nc;
+// the pages are read-only for the kernel).  NC = false (the fused decode
+// step, whose rotation and window append write pages earlier in the same
+// kernel) uses coherent L2 loads (ld.global.cg).
+template <bool NC, typename T>
+__device__ __forceinline__ T ldkv(const T* p) {
+  if constexpr (NC) return __ldg(p);
+  else return __ldcg(p);
+}
+template <typename KT, bool NC = true>
 __device__ __forceinline__ float4 load4(const KT* p);
 template <>
-__device__ __forceinline__ float4 load4<float>(const float* p) {
-  return __ldg(reinterpret_cast<const float4*>(p));
+__device__ __forceinline__ float4 load4<float, true>(const float* p) {
+  return ldkv<true>(reinterpret_cast<const float4*>(p));
 }
 template <>
-__device__ __forceinline__ float4 load4<__nv_bfloat16>(const __nv_bfloat16* p) {
-  uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+__device__ __forceinline__ float4 load4<float, false>(const float* p) {
+  return ldkv<false>(reinterpret_cast<const float4*>(p));
+}
+template <>
+__device__ __forceinline__ float4 load4<__nv_bfloat16, true>(const __nv_bfloat16* p) {
+  uint2 u = ldkv<true>(reinterpret_cast<const uint2*>(p));
+  float2 a = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.x));
+  float2 b = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+template <>
+__device__ __forceinline__ float4 load4<__nv_bfloat16, false>(const __nv_bfloat16* p) {
+  uint2 u = ldkv<false>(reinterpret_cast<const uint2*>(p));
   float2 a = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.x));
   float2 b = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.y));
   return make_float4(a.x, a.y, b.x, b.y);
@@ -65,14 +85,16 @@ struct Raw4;
 template <>
 struct Raw4<float> {
   using T = float4;
-  static __device__ __forceinline__ T load(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+  template <bool NC>
+  static __device__ __forceinline__ T load(const float* p) { return ldkv<NC>(reinterpret_cast<const float4*>(p)); }
   static __device__ __forceinline__ float4 cvt(T r) { return r; }
   static __device__ __forceinline__ T zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 };
 template <>
 struct Raw4<__nv_bfloat16> {
   using T = uint2;
-  static __device__ __forceinline__ T load(const __nv_bfloat16* p) { return __ldg(reinterpret_cast<const uint2*>(p)); }
+  template <bool NC>
+  static __device__ __forceinline__ T load(const __nv_bfloat16* p) { return ldkv<NC>(reinterpret_cast<const uint2*>(p)); }
   static __device__ __forceinline__ float4 cvt(T u) {
     float2 a = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.x));
     float2 b = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.y));
@@ -117,17 +139,17 @@ __device__ __forceinline__ void attend_vals(HeadAcc (&h)[G], const float4 (&qv)[
   }
 }
 
-template <typename KT, int G>
+template <typename KT, int G, bool NC = true>
 __device__ __forceinline__ void attend_row(HeadAcc (&h)[G], const float4 (&qv)[G], const KT* krow, const KT* vrow,
                                            int lane, int dim, int dim_v, float scale_log2) {
-  float4 k = lane * 4 < dim ? load4<KT>(krow + lane * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
-  float4 v = lane * 4 < dim_v ? load4<KT>(vrow + lane * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 k = lane * 4 < dim ? load4<KT, NC>(krow + lane * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 v = lane * 4 < dim_v ? load4<KT, NC>(vrow + lane * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
   attend_vals<KT, G>(h, qv, k, v, lane, scale_log2);
 }
 
 // A chunk of CH rows starting at row index `r0` of a [rows][ld] K/V pair:
 // all loads first, then the rows' online-softmax updates in order.
-template <typename KT, int G, int CH>
+template <typename KT, int G, int CH, bool NC = true>
 __device__ __forceinline__ void attend_chunk(HeadAcc (&h)[G], const float4 (&qv)[G], const KT* K, const KT* V,
                                              size_t r0, int nrow, int ldk, int ldv, int lane, int dim, int dim_v,
                                              float scale_log2) {
@@ -135,8 +157,8 @@ __device__ __forceinline__ void attend_chunk(HeadAcc (&h)[G], const float4 (&qv)
   typename R::T kr[CH], vr[CH];
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
-    kr[c] = (c < nrow && lane * 4 < dim) ? R::load(K + (r0 + c) * ldk + lane * 4) : R::zero();
-    vr[c] = (c < nrow && lane * 4 < dim_v) ? R::load(V + (r0 + c) * ldv + lane * 4) : R::zero();
+    kr[c] = (c < nrow && lane * 4 < dim) ? R::template load<NC>(K + (r0 + c) * ldk + lane * 4) : R::zero();
+    vr[c] = (c < nrow && lane * 4 < dim_v) ? R::template load<NC>(V + (r0 + c) * ldv + lane * 4) : R::zero();
   }
 #pragma unroll
   for (int c = 0; c < CH; ++c)
@@ -156,7 +178,7 @@ struct G4State {
   float4 acc[4];       // dims 4l..4l+3 of every head
 };
 
-template <typename KT>
+template <typename KT, bool NC = true>
 __device__ __forceinline__ void attend_chunk8_g4(G4State& st, const unsigned long long (&q2)[2][4], const KT* K,
                                                  const KT* V, size_t r0, int nrow, int ldk, int ldv, int lane,
                                                  int dim, int dim_v, float scale_log2) {
@@ -166,8 +188,8 @@ __device__ __forceinline__ void attend_chunk8_g4(G4State& st, const unsigned lon
 #pragma unroll
   for (int jj = 0; jj < 8; ++jj) {
     const int rk = jj ^ pi;
-    kr[jj] = (rk < nrow && lane * 4 < dim) ? R::load(K + (r0 + rk) * ldk + lane * 4) : R::zero();
-    vr[jj] = (jj < nrow && lane * 4 < dim_v) ? R::load(V + (r0 + jj) * ldv + lane * 4) : R::zero();
+    kr[jj] = (rk < nrow && lane * 4 < dim) ? R::template load<NC>(K + (r0 + rk) * ldk + lane * 4) : R::zero();
+    vr[jj] = (jj < nrow && lane * 4 < dim_v) ? R::template load<NC>(V + (r0 + jj) * ldv + lane * 4) : R::zero();
   }
   unsigned long long v2[8][2];
 #pragma unroll
@@ -240,7 +262,7 @@ __device__ __forceinline__ void attend_chunk8_g4(G4State& st, const unsigned lon
 // take pages round-robin; their online-softmax states are combined in shared
 // memory (no split-K).  Residency accounting as attn_kernel's split 0
 // (pagestore.py:169-215).  smem: >= NT/32 * G * (2 * 4 + 32 * 16) bytes.
-template <typename KT, int G, int NT>
+template <typename KT, int G, int NT, bool NC = true>
 __device__ void attend_tree_paged(const ForestView& F, int t, int GA, const float* q /*[GA][dim]*/,
                                   const int32_t* sel, int nsel, float* out /*[GA][dim_v]*/, int64_t* stats,
                                   int scalar_bytes, float scale_log2, unsigned char* smem) {
@@ -285,11 +307,11 @@ __device__ void attend_tree_paged(const ForestView& F, int t, int GA, const floa
     const size_t base = F.pg(t, p) * F.s;
     if constexpr (G == 4) {
       for (int r0 = 0; r0 < fill; r0 += 8)
-        attend_chunk8_g4<KT>(g4, q2, K, V, base + r0, min(8, fill - r0), F.dkp, F.dvp, lane, F.dim, F.dim_v,
+        attend_chunk8_g4<KT, NC>(g4, q2, K, V, base + r0, min(8, fill - r0), F.dkp, F.dvp, lane, F.dim, F.dim_v,
                              scale_log2);
     } else {
       for (int r0 = 0; r0 < fill; r0 += CH)
-        attend_chunk<KT, G, CH>(h, qv, K, V, base + r0, min(CH, fill - r0), F.dkp, F.dvp, lane, F.dim, F.dim_v,
+        attend_chunk<KT, G, CH, NC>(h, qv, K, V, base + r0, min(CH, fill - r0), F.dkp, F.dvp, lane, F.dim, F.dim_v,
                                 scale_log2);
     }
   }

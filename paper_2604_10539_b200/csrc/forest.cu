@@ -217,6 +217,20 @@ int icb_query_attend(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, 
                         scalar_bytes);
 }
 
+int icb_step_attend(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, const float* queries, int32_t k,
+                    int64_t beam, int64_t visit_cap, int32_t* out_ids, int32_t k_out, int32_t* out_counts,
+                    int32_t* out_pages, int32_t pages_cap, int32_t* out_npages, float* attn_out,
+                    int64_t* attn_stats, int32_t scalar_bytes, int32_t rotate, int64_t* rot_stats,
+                    const int32_t* token_dev, const float* win_keys, const float* win_values, void* stream) {
+  if (k < 1) { icb_set_error(ICB_E_INPUT, "k must be >= 1"); return ICB_E_INPUT; }
+  if (beam < k || visit_cap < k) { icb_set_error(ICB_E_CONFIG, "beam and visit_cap must be >= k"); return ICB_E_CONFIG; }
+  if (!attn_out || !out_pages || !out_npages) { icb_set_error(ICB_E_INPUT, "null output"); return ICB_E_INPUT; }
+  StepOpts step{rotate, rot_stats, token_dev, win_keys, win_values};
+  return icb_query_impl(f, trees, n, G, queries, 0, k, beam, visit_cap, ICB_SENTINEL_LEVEL, out_ids, k_out,
+                        out_counts, out_pages, pages_cap, out_npages, S_(stream), attn_out, attn_stats,
+                        scalar_bytes, &step);
+}
+
 int icb_insert(icb_forest* f, const int32_t* trees, int32_t n, int32_t m, const int32_t* tokens, const float* keys,
                const float* values, const int32_t* levels, int32_t* out_levels, void* stream) {
   return icb_insert_impl(f, trees, n, m, tokens, keys, values, levels, out_levels, 0, 4, nullptr, S_(stream));

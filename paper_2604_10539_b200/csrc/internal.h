@@ -93,11 +93,19 @@ int icb_resident_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t ro
 
 int icb_build_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t n_points, const int32_t* tokens,
                    const float* keys, const float* values, const double* scales, cudaStream_t st);
+// Fused decode-step prologue of the query kernel (icb_step_attend).
+struct StepOpts {
+  int rotate;                  // rotate the oldest window page into the tree first
+  int64_t* rot_stats;          // [n][2] or null
+  const int32_t* token_dev;    // the decode position (device memory)
+  const float* keys;           // [n][dim] window keys of this token
+  const float* values;         // [n][dim_v]
+};
 int icb_query_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, const float* queries,
                    int32_t lifted_input, int32_t k, int64_t beam, int64_t visit_cap, int32_t target_level,
                    int32_t* out_ids, int32_t k_out, int32_t* out_counts, int32_t* out_pages,
                    int32_t pages_cap, int32_t* out_npages, cudaStream_t st, float* attn_out = nullptr,
-                   int64_t* attn_stats = nullptr, int32_t scalar_bytes = 4);
+                   int64_t* attn_stats = nullptr, int32_t scalar_bytes = 4, const StepOpts* step = nullptr);
 int icb_insert_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t m, const int32_t* tokens,
                     const float* keys, const float* values, const int32_t* levels, int32_t* out_levels,
                     int from_window, int32_t scalar_bytes, int64_t* stats, cudaStream_t st);

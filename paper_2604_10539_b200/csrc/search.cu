@@ -2,6 +2,7 @@
 // gqa_union fused into the epilogue (dci.py:318-364, pagestore.py:111-113,
 // attention.py:96-103, engine.py:436-447).
 #include "search.cuh"
+#include "insert.cuh"
 #include "attend.cuh"
 #include "internal.h"
 
@@ -25,6 +26,16 @@ struct QueryArgs {
   int64_t* attn_stats;   // [n][5] or null
   int scalar_bytes;
   float scale_log2;
+  // fused decode-step prologue (icb_step_attend, the STEP kernel variant):
+  // rotate the oldest window page into the tree (if rotate), then append the
+  // decode token to the window, then search + attend
+  int rotate;
+  char* rot_scratch;          // insert slot scratch (ensure_insert_scratch)
+  SlotLayout rot_SL;
+  int64_t* rot_stats;         // [n][2] offload bytes, transactions (or null)
+  const int32_t* app_token_dev;
+  const float* app_keys;      // [n][dim]
+  const float* app_values;    // [n][dim_v]
 };
 
 // Lift raw query g (geometry.py:89-98): fp64 norm in pairwise order, fp32 q/|q|.
@@ -46,16 +57,33 @@ __device__ bool lift_query(SearchSmem& S, const ForestView& F, const float* q, i
   return nrm != 0.0;
 }
 
-template <int NT, int GP>
+template <int NT, int GP, bool STEP = false>
 __global__ void __launch_bounds__(NT, 512 / NT) query_kernel(ForestView F, QueryArgs A, char* scratch, SlotLayout SL) {
   __shared__ SearchSmem S;
   extern __shared__ __align__(128) unsigned char dsm[];
   GroupSmem* GSA = reinterpret_cast<GroupSmem*>(dsm);
+  const int b = blockIdx.x;
+  const int t = A.trees[b];
+  if constexpr (STEP) {
+    // this tree's rotation and window append, in Engine.decode_step order,
+    // before its search: the step's slowest rotation no longer gates every
+    // tree's search (shared memory is re-initialised for the search below)
+    if (A.rotate) {
+      const RingView RG1 = ring_view(dsm, 1);
+      if (threadIdx.x == 0) S.sortbuf = reinterpret_cast<unsigned long long*>(RG1.ring);
+      ring_init(RG1);
+      double* dt1;
+      unsigned* pb1;
+      SearchScratch SS1 = slot_scratch(A.rot_scratch + (size_t)b * A.rot_SL.total, A.rot_SL, F.tok_cap, &dt1, &pb1);
+      rotate_tree<NT>(S, GSA, RG1, F, SS1, t, dt1, A.rot_stats ? A.rot_stats + (size_t)b * 2 : nullptr,
+                      A.scalar_bytes, nullptr);
+    }
+    append_tree(F, t, *A.app_token_dev, A.app_keys + (size_t)b * F.dim, A.app_values + (size_t)b * F.dim_v);
+    __syncthreads();
+  }
   const RingView RG = ring_view(dsm, GP);
   if (threadIdx.x == 0) S.sortbuf = reinterpret_cast<unsigned long long*>(RG.ring);
   ring_init(RG);
-  const int b = blockIdx.x;
-  const int t = A.trees[b];
   const int G = A.G;
   const long long tk0 = clock64();
   double* dirs_tmp;
@@ -167,9 +195,9 @@ __global__ void __launch_bounds__(NT, 512 / NT) query_kernel(ForestView F, Query
     int64_t* stb = A.attn_stats ? A.attn_stats + (size_t)b * 5 : nullptr;
     const long long ta = clock64();
     if (F.kv_bf16)
-      attend_tree_paged<__nv_bfloat16, GP, NT>(F, t, G, qb, sel, nsel, ob, stb, A.scalar_bytes, A.scale_log2, sm);
+      attend_tree_paged<__nv_bfloat16, GP, NT, !STEP>(F, t, G, qb, sel, nsel, ob, stb, A.scalar_bytes, A.scale_log2, sm);
     else
-      attend_tree_paged<float, GP, NT>(F, t, G, qb, sel, nsel, ob, stb, A.scalar_bytes, A.scale_log2, sm);
+      attend_tree_paged<float, GP, NT, !STEP>(F, t, G, qb, sel, nsel, ob, stb, A.scalar_bytes, A.scale_log2, sm);
     if (A.P.prof && threadIdx.x == 0) atomicAdd(A.P.prof + 8, (unsigned long long)(clock64() - ta));
   }
 }
@@ -218,12 +246,18 @@ int ensure_query_scratch(icb_forest* f, int n, int G, cudaStream_t st, char** ou
   return ICB_OK;
 }
 
+int ensure_insert_scratch(icb_forest* f, int n, char** out, SlotLayout* lay);   // insert.cu
+
 int icb_query_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, const float* queries,
                    int32_t lifted_input, int32_t k, int64_t beam, int64_t visit_cap, int32_t target_level,
                    int32_t* out_ids, int32_t k_out, int32_t* out_counts, int32_t* out_pages,
                    int32_t pages_cap, int32_t* out_npages, cudaStream_t st, float* attn_out,
-                   int64_t* attn_stats, int32_t scalar_bytes) {
+                   int64_t* attn_stats, int32_t scalar_bytes, const StepOpts* step) {
   if (n <= 0) return ICB_OK;
+  if (step && (!attn_out || !step->token_dev || !step->keys || !step->values)) {
+    icb_set_error(ICB_E_INPUT, "decode step needs attention outputs, a device token and window K/V");
+    return ICB_E_INPUT;
+  }
   if (attn_out && (lifted_input || !out_pages)) {
     icb_set_error(ICB_E_INPUT, "fused attention needs raw queries and page outputs");
     return ICB_E_INPUT;
@@ -245,15 +279,28 @@ int icb_query_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, co
   A.pages_cap = pages_cap; A.out_npages = out_npages;
   A.attn_out = attn_out; A.attn_stats = attn_stats; A.scalar_bytes = scalar_bytes;
   A.scale_log2 = (float)(1.4426950408889634 / sqrt((double)f->cfg.dim));
+  if (step) {
+    A.rotate = step->rotate;
+    if (step->rotate && (rc = ensure_insert_scratch(f, n, &A.rot_scratch, &A.rot_SL))) return rc;
+    A.rot_stats = step->rot_stats;
+    A.app_token_dev = step->token_dev;
+    A.app_keys = step->keys;
+    A.app_values = step->values;
+  }
   const int GP = G <= 1 ? 1 : G <= 2 ? 2 : G <= 4 ? 4 : 8;
   size_t dsm = search_dsm_bytes(GP);
-  if (const char* e = getenv("ICB_QUERY_DSM_EXTRA")) dsm += (size_t)atol(e);   // debug knob: occupancy
   switch (GP) {
 #define ICB_LAUNCH_Q(gp)                                                                                  \
   case gp:                                                                                                \
-    ICB_CUDA(cudaFuncSetAttribute(query_kernel<kSearchThreads, gp>,                                       \
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));                \
-    query_kernel<kSearchThreads, gp><<<n, kSearchThreads, dsm, st>>>(f->view, A, scratch, SL);            \
+    if (step) {                                                                                           \
+      ICB_CUDA(cudaFuncSetAttribute(query_kernel<kSearchThreads, gp, true>,                               \
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));              \
+      query_kernel<kSearchThreads, gp, true><<<n, kSearchThreads, dsm, st>>>(f->view, A, scratch, SL);    \
+    } else {                                                                                              \
+      ICB_CUDA(cudaFuncSetAttribute(query_kernel<kSearchThreads, gp>,                                     \
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));              \
+      query_kernel<kSearchThreads, gp><<<n, kSearchThreads, dsm, st>>>(f->view, A, scratch, SL);          \
+    }                                                                                                     \
     break;
     ICB_LAUNCH_Q(1)
     ICB_LAUNCH_Q(2)

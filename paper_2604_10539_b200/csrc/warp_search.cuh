@@ -43,7 +43,7 @@ __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v)
 // q: lifted query (smem, ICB_DPAD floats), qt its tail.  On success returns
 // true with *parent (-1 if the floor level had no candidate) and adds the
 // distance evaluations to *evals (lane 0's copy is authoritative).
-__device__ bool warp_parent_search(const ForestView& F, int t, const float* q, float qt, int target,
+__device__ inline bool warp_parent_search(const ForestView& F, int t, const float* q, float qt, int target,
                                    WarpSearchBuf& W, int* parent, unsigned long long* evals) {
   const int lane = threadIdx.x & 31;
   const TreeMeta& mt = F.meta[t];

@@ -54,6 +54,11 @@ class EngineConfig:
     layer_serial: bool = False
     overlap_dense: bool = True     # skip layers' dense attention on a side stream, concurrent with the search
     cuda_graph: bool = False       # replay captured decode steps (metrics=False steps)
+    # rotation steps as one launch (icb_step_attend: rotate + append + search +
+    # attend per tree).  Off: measured slower at C2 (1.38 vs 1.15 ms per
+    # rotation step), the inserts lose issue slots to co-resident
+    # search CTAs
+    fuse_rotation: bool = False
 
     def __post_init__(self) -> None:
         if min(self.layers, self.kv_heads, self.query_heads_per_group, self.d, self.d_prime) < 1:
@@ -516,6 +521,24 @@ class Engine:
         groups = [(0, T)] if not cfg.layer_serial else [(l * H, (l + 1) * H) for l in range(T // H)]
         for a, b in groups:
             trees = self.trees_dev[a:b]
+            fused_step = rotate and cfg.fuse_rotation and cfg.reuse_stride < 2
+            if fused_step:
+                # rotation, window append, search and attention of each tree in
+                # one CTA (icb_step_attend): the slowest tree's rotation no
+                # longer holds back every other tree's search
+                if before_query is not None:
+                    before_query()
+                    before_query = None
+                o = f.step_attend(trees, qi[a:b], k, self.beam, self.visit_cap,
+                                  out=(self.ids[a:b], self.counts[a:b], self.pages[a:b], self.npages[a:b]),
+                                  attn_out=self._attn_out[a:b], token_dev=self._tok_dev, keys=ki[a:b],
+                                  values=vi[a:b], rotate=True, rot_stats=self.rot_stats[a:b],
+                                  stats=self.stats[a:b], scalar_bytes=cfg.scalar_bytes)
+                if after_query is not None:
+                    after_query()
+                    after_query = None
+                out[s0 + a // H: s0 + b // H] = o.reshape((b - a) // H, H * G, cfg.d_prime)
+                continue
             if rotate:
                 f.rotate_window(trees, cfg.scalar_bytes, self.rot_stats[a:b])
             f.append_window(trees, self._tok_dev, ki[a:b], vi[a:b])

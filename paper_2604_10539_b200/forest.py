@@ -199,6 +199,24 @@ class DeviceForest:
                                          scalar_bytes, _stream()))
         return attn_out
 
+    def step_attend(self, trees, queries, k, beam, visit_cap, *, out, attn_out, token_dev, keys, values,
+                    rotate=False, rot_stats=None, stats=None, scalar_bytes=4):
+        """A whole decode step of these trees in one launch (icb_step_attend):
+        per tree, rotate_window (if `rotate`), append_window(token_dev, keys,
+        values), then query_attend.  Same results as those calls in sequence."""
+        tr = self._trees(trees)
+        n = tr.numel()
+        q = self._f32(queries).reshape(n, -1, self.dim).contiguous()
+        G = q.shape[1]
+        ids, counts, pages, npages = out
+        kk, vv = self._f32(keys, (n, self.dim)), self._f32(values, (n, self.dim_v))
+        N.check(N.lib().icb_step_attend(self.h, _ptr(tr), n, G, _ptr(q), int(min(k, 2**30)), int(min(beam, 2**62)),
+                                        int(min(visit_cap, 2**62)), _ptr(ids), ids.shape[2], _ptr(counts),
+                                        _ptr(pages), pages.shape[1], _ptr(npages), _ptr(attn_out), _ptr(stats),
+                                        scalar_bytes, int(bool(rotate)), _ptr(rot_stats), _ptr(token_dev),
+                                        _ptr(kk), _ptr(vv), _stream()))
+        return attn_out
+
     def insert(self, trees, tokens, keys, values=None, levels=None):
         tr = self._trees(trees)
         n = tr.numel()

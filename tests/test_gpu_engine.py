@@ -115,6 +115,39 @@ def test_cuda_graph_replay_matches_eager(cuda_ok):
     assert set(graph._graphs) == {False, True}   # both variants captured and replayed
 
 
+def test_fused_rotation_step_matches_separate_launches(cuda_ok):
+    """icb_step_attend (rotation + window append + search + attention in one
+    CTA per tree) gives the outputs, selections, step metrics and final tree
+    structure of the separate rotate / append / query_attend launches."""
+    import torch
+    from paper_2604_10539_b200.engine import Engine, EngineConfig
+    from oracle.workload import Spec, generate
+    sk = dict(n_tokens=2048 + 70, d=64, d_prime=64, clusters=16, layers=4, kv_heads=2,
+              query_heads_per_group=4, seed=5)
+    keys, values, queries, _ = generate(Spec(kind="clustered", **sk))
+    shape = dict(layers=4, kv_heads=2, query_heads_per_group=4, d=64, d_prime=64, seed=5)
+    cfg = dict(token_budget=32, skip_layers=1, kv_dtype="bf16", max_tokens=2048 + 70)
+    sep = Engine(EngineConfig(**shape, **cfg, fuse_rotation=False)).prefill(keys, values, 2048)
+    fus = Engine(EngineConfig(**shape, **cfg, fuse_rotation=True)).prefill(keys, values, 2048)
+    q = torch.as_tensor(queries, device="cuda")
+    k = torch.as_tensor(keys, device="cuda")
+    v = torch.as_tensor(values, device="cuda")
+    for t in range(64):
+        tok = 2048 + t
+        o1, m1 = sep.decode_step(tok, q[tok], k[tok], v[tok])
+        o2, m2 = fus.decode_step(tok, q[tok], k[tok], v[tok])
+        assert torch.equal(o1, o2), t
+        assert m1 == m2, t
+        (i1, c1, p1, n1), (i2, c2, p2, n2) = sep.selected(), fus.selected()
+        assert (c1 == c2).all() and (n1 == n2).all(), t
+        for tr in range(c1.shape[0]):
+            assert list(p1[tr, :n1[tr]]) == list(p2[tr, :n2[tr]]), t
+    for tr in range(sep.T):
+        e1, e2 = sep.forest.export(tr), fus.forest.export(tr)
+        assert e1["nodes"] == e2["nodes"] and e1["pages"] == e2["pages"], tr
+        assert e1["info"] == e2["info"], tr
+
+
 @pytest.mark.parametrize("name", ["eval", "eval_reuse"])
 def test_engine_evaluation_metrics(cuda_ok, name):
     """evaluate=True (engine.py:536-566) on the device: recall@k, page hit rate,
