@@ -69,6 +69,14 @@ typedef struct {
   int32_t own_cap;     /* owned-node list entries per tree */
   int32_t dirs_cap;    /* cached P-DCI direction sets per tree */
   double promotion_ratio; /* r */
+  /* KV offload (BASELINE config 3; TierStore, pagestore.py:117-215): when
+   * kv_host != 0 all page K/V live in pinned, device-mapped host memory and
+   * each fused decode step (icb_query_attend / icb_step_attend) gathers the
+   * pages it attends -- sink, window and selected -- into a per-tree HBM pool
+   * of pool_pages slots (pages already resident are kept, the rest are
+   * evicted).  pool_pages must cover sink + window + the largest selection. */
+  int32_t kv_host;
+  int32_t pool_pages;
 } icb_forest_config;
 
 const char *icb_last_error(void);
@@ -237,6 +245,9 @@ int icb_read_meta_c(icb_forest *f, int32_t tree, double *c);
 /* KeyScale c of an empty tree that grows by inserts only (DciTree(dim, scale,
  * ...), dci.py:164-176; geometry.py:47-56).  A build sets c itself. */
 int icb_set_scale(icb_forest *f, int32_t tree, double c);
+/* KV offload: out host [n_trees][2] = bytes gathered host -> HBM pool so far,
+ * pages resident in the pool now (ICB_E_CONFIG when kv_host = 0). */
+int icb_pool_stats(icb_forest *f, int64_t *out);
 /* Host-side restatement check: n PCG64 doubles of SeedSequence(words, spawn). */
 int icb_host_pcg_doubles(const uint32_t *words, int32_t n_words, const uint32_t *spawn,
                          int32_t n_spawn, int32_t n, double *out);

@@ -45,7 +45,8 @@ class icb_forest_config(ctypes.Structure):
                 ("tok_cap", ctypes.c_int32), ("node_cap", ctypes.c_int32),
                 ("page_cap", ctypes.c_int32), ("member_cap", ctypes.c_int32),
                 ("own_cap", ctypes.c_int32), ("dirs_cap", ctypes.c_int32),
-                ("promotion_ratio", ctypes.c_double)]
+                ("promotion_ratio", ctypes.c_double), ("kv_host", ctypes.c_int32),
+                ("pool_pages", ctypes.c_int32)]
 
 
 _lib = None
@@ -84,6 +85,7 @@ EXPORTS = {
     "icb_read_meta_c": ([P, I32, P], ctypes.c_int),
     "icb_set_scale": ([P, I32, ctypes.c_double], ctypes.c_int),
     "icb_host_pcg_doubles": ([P, I32, P, I32, I32, P], ctypes.c_int),
+    "icb_pool_stats": ([P, P], ctypes.c_int),
     "icb_host_pcg_jump_doubles": ([P, I32, P, I32, ctypes.c_int64, I32, P], ctypes.c_int),
 }
 

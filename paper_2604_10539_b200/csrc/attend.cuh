@@ -262,6 +262,102 @@ __device__ __forceinline__ void attend_chunk8_g4(G4State& st, const unsigned lon
 // take pages round-robin; their online-softmax states are combined in shared
 // memory (no split-K).  Residency accounting as attn_kernel's split 0
 // (pagestore.py:169-215).  smem: >= NT/32 * G * (2 * 4 + 32 * 16) bytes.
+// KV offload (F.kv_host): make tree t's pool hold exactly the pages this step
+// attends -- sink, window and the `nsel` selected pages (hot = selected U
+// pinned, pagestore.py:169-215).  Resident pages outside that set are evicted,
+// missing ones claim the freed slots and their filled rows are copied from the
+// pinned host store (mapped; 16-byte loads, 8 in flight per thread, all of the
+// tree's pages at once).  rbits: a zeroed page bitmap (page_cap bits) of
+// scratch, returned zeroed.  Returns the bytes copied.
+template <typename KT, int NT>
+__device__ long long gather_pages(const ForestView& F, int t, const int32_t* sel, int nsel, unsigned* rbits) {
+  const TreeMeta* m = F.meta + t;
+  const int nsink = m->n_sink, nfix = nsink + m->n_window, total = nfix + nsel;
+  int* page_slot = F.page_slot + (size_t)t * F.page_cap;
+  int* slot_page = F.slot_page + (size_t)t * F.pool_cap;
+  int* freel = F.pool_tmp + (size_t)t * 2 * F.pool_cap;
+  int* copyl = freel + F.pool_cap;
+  __shared__ int s_nfree, s_ncopy;
+  auto page_at = [&](int i) { return i < nsink ? m->sink[i] : i < nfix ? m->win[i - nsink] : sel[i - nfix]; };
+  for (int i = threadIdx.x; i < total; i += NT) {
+    const int p = page_at(i);
+    atomicOr(rbits + (p >> 5), 1u << (p & 31));
+  }
+  if (threadIdx.x == 0) { s_nfree = 0; s_ncopy = 0; }
+  __syncthreads();
+  for (int s = threadIdx.x; s < F.pool_cap; s += NT) {   // evict, collect free slots
+    int p = slot_page[s];
+    if (p >= 0 && !((rbits[p >> 5] >> (p & 31)) & 1u)) {
+      page_slot[p] = -1;
+      slot_page[s] = -1;
+      p = -1;
+    }
+    if (p < 0) freel[atomicAdd(&s_nfree, 1)] = s;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < total; i += NT) {        // claim slots for missing pages
+    const int p = page_at(i);
+    if (page_slot[p] < 0) {
+      const int k = atomicAdd(&s_ncopy, 1);
+      if (k < s_nfree) {
+        const int s = freel[k];
+        page_slot[p] = s;
+        slot_page[s] = p;
+        copyl[k] = p;
+      } else {
+        set_err(F.meta + t, ICB_ERR_CAP_SCRATCH);   // pool smaller than the step's pages
+      }
+    }
+  }
+  __syncthreads();
+  // copy the filled rows: items (page, row, 16-byte chunk), K chunks then V
+  const int nc = min(s_ncopy, s_nfree);
+  const int ck = F.dkp * (int)sizeof(KT) / 16, cv = F.dvp * (int)sizeof(KT) / 16, cr = ck + cv;
+  const long long items = (long long)nc * F.s * cr;
+  const char* hk = (const char*)F.page_k;
+  const char* hv = (const char*)F.page_v;
+  char* pk = (char*)F.pool_k;
+  char* pv = (char*)F.pool_v;
+  long long bytes = 0;
+  constexpr int B = 8;
+  for (long long x0 = threadIdx.x; x0 < items; x0 += (long long)NT * B) {
+    uint4 v[B];
+    size_t dst[B];
+    bool isk[B], on[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const long long x = x0 + (long long)u * NT;
+      on[u] = false;
+      if (x < items) {
+        const int k = (int)(x / (F.s * cr));
+        const int rem = (int)(x - (long long)k * F.s * cr);
+        const int r = rem / cr, c = rem - r * cr;
+        const int p = copyl[k];
+        if (r < F.page_fill[F.pg(t, p)]) {
+          isk[u] = c < ck;
+          const size_t row_src = F.pg(t, p) * F.s + r;
+          const size_t row_dst = ((size_t)t * F.pool_cap + page_slot[p]) * F.s + r;
+          const size_t rb = (size_t)(isk[u] ? F.dkp : F.dvp) * sizeof(KT);
+          const int cc = isk[u] ? c : c - ck;
+          v[u] = *reinterpret_cast<const uint4*>((isk[u] ? hk : hv) + row_src * rb + (size_t)cc * 16);
+          dst[u] = row_dst * rb + (size_t)cc * 16;
+          on[u] = true;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u)
+      if (on[u]) {
+        *reinterpret_cast<uint4*>((isk[u] ? pk : pv) + dst[u]) = v[u];
+        bytes += 16;
+      }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < total; i += NT) rbits[page_at(i) >> 5] = 0u;
+  __syncthreads();
+  return bytes;
+}
+
 template <typename KT, int G, int NT, bool NC = true>
 __device__ void attend_tree_paged(const ForestView& F, int t, int GA, const float* q /*[GA][dim]*/,
                                   const int32_t* sel, int nsel, float* out /*[GA][dim_v]*/, int64_t* stats,
@@ -297,14 +393,15 @@ __device__ void attend_tree_paged(const ForestView& F, int t, int GA, const floa
       q2[hp][3] = pack_f2(qv[2 * hp].w, qv[2 * hp + 1].w);
     }
   }
-  const KT* K = (const KT*)F.page_k;
-  const KT* V = (const KT*)F.page_v;
+  // pages are read from the HBM pool under KV offload (gathered by the caller)
+  const KT* K = (const KT*)(F.kv_host ? F.pool_k : F.page_k);
+  const KT* V = (const KT*)(F.kv_host ? F.pool_v : F.page_v);
   const int nsink = m->n_sink, nfix = nsink + m->n_window, total = nfix + nsel;
   constexpr int CH = (sizeof(KT) == 2 ? 16 : 8) / (G >= 4 ? 2 : 1) / (G >= 8 ? 2 : 1);
   for (int i = warp; i < total; i += NW) {
     const int p = i < nsink ? m->sink[i] : i < nfix ? m->win[i - nsink] : sel[i - nfix];
     const int fill = F.page_fill[F.pg(t, p)];
-    const size_t base = F.pg(t, p) * F.s;
+    const size_t base = F.kv_host ? ((size_t)t * F.pool_cap + F.page_slot[F.pg(t, p)]) * F.s : F.pg(t, p) * F.s;
     if constexpr (G == 4) {
       for (int r0 = 0; r0 < fill; r0 += 8)
         attend_chunk8_g4<KT, NC>(g4, q2, K, V, base + r0, min(8, fill - r0), F.dkp, F.dvp, lane, F.dim, F.dim_v,

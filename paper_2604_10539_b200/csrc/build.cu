@@ -304,7 +304,8 @@ __global__ void __launch_bounds__(256) nn_parent_kernel(ForestView F, BuildArgs 
                                                         const int* pts, const int* pts_off,
                                                         const int* cands, const int* cand_off,
                                                         const double* cand64, const double* cand_sq,
-                                                        int stride, int* parent_pos) {
+                                                        int stride, int* parent_pos, const int* ovf_cnt = nullptr,
+                                                        int ovf_cap = 0) {
   extern __shared__ double smem[];
   double* sp = smem;                              // [NN_BM][dim+1 padded]
   const int D1 = F.dim + 1;
@@ -323,6 +324,16 @@ __global__ void __launch_bounds__(256) nn_parent_kernel(ForestView F, BuildArgs 
   const int e1 = min(npts, e0 + NN_BM);
   const double c = F.meta[t].c;
   const int tid = threadIdx.x;
+  if (ovf_cnt) {
+    // after the filter: only blocks holding a point whose window overflowed
+    __shared__ int s_any;
+    if (tid == 0) s_any = 0;
+    __syncthreads();
+    for (int e = e0 + tid; e < e1; e += blockDim.x)
+      if (ovf_cnt[(size_t)b * A.n_points + e] > ovf_cap) s_any = 1;
+    __syncthreads();
+    if (!s_any) return;
+  }
   // levels of block entries
   for (int e = e0 + tid; e < e1; e += blockDim.x) {
     int lv = 1;
@@ -515,8 +526,8 @@ __global__ void __launch_bounds__(128) nn_verify_kernel(ForestView F, BuildArgs 
   const int c0 = cand_off[(size_t)b * 64 + lv];
   const int nc = cand_off[(size_t)b * 64 + lv + 1] - c0;
   const int c = cnt[(size_t)b * A.n_points + e];
-  const bool all = c > NF_CAP;
-  const int m = all ? nc : c;
+  const bool all = c > NF_CAP;   // overflowed windows: nn_parent_kernel's shared tiles do those points
+  const int m = all ? 0 : c;
   const double* c64base = cand64 + ((size_t)b * stride + c0) * (ICB_DPAD + 1);
   const IdxT* lst = list + ((size_t)b * A.n_points + e) * NF_CAP;
   if (prof && lane == 0) {
@@ -1050,6 +1061,13 @@ int icb_build_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t n_poi
       ICB_CUDA(cudaFuncSetAttribute(nn_verify_kernel<IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize, nv_sm));
       nn_verify_kernel<IdxT><<<dim3((P + 3) / 4, n), 128, nv_sm, st>>>(
           F, A, pts, pts_off, cands, cand_off, p64, cand64, cand_sq, stride, list, nf_cnt, parent_pos, prof);
+      // points whose window held more than NF_CAP candidates: the brute-force
+      // tiled kernel, restricted to blocks that contain one
+      const int D1 = F.dim + 1, PS = D1 | 1;
+      const size_t psm = sizeof(double) * (NN_BM * PS + NN_BN * (NN_KC + 1));
+      ICB_CUDA(cudaFuncSetAttribute(nn_parent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
+      nn_parent_kernel<<<dim3((P + NN_BM - 1) / NN_BM, n), 256, psm, st>>>(
+          F, A, nsq, pts, pts_off, cands, cand_off, cand64, cand_sq, stride, parent_pos, nf_cnt, NF_CAP);
       return ICB_OK;
     };
     int rc;

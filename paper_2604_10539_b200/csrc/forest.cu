@@ -123,13 +123,40 @@ int icb_forest_create(const icb_forest_config* cfg, icb_forest** out) {
   F.upper_cap = c.tok_cap / 4 + 64;   // ~r = 10% of points expected; overflow only disables the start shortcut
   AL(F.upper, T * F.upper_cap, 0);
 #undef AL
-  if (rc == ICB_OK) {
+  F.kv_host = c.kv_host != 0;
+  F.pool_cap = F.kv_host ? c.pool_pages : 0;
+  if (F.kv_host && c.pool_pages < 4) { icb_set_error(ICB_E_CONFIG, "kv_host needs pool_pages >= 4"); rc = ICB_E_CONFIG; }
+  if (rc == ICB_OK && !F.kv_host) {
     char* pk = nullptr;
     char* pv = nullptr;
     rc = falloc(f, &pk, T * c.page_cap * c.page_size * F.dkp * kvb, 0);
     if (rc == ICB_OK) rc = falloc(f, &pv, T * c.page_cap * c.page_size * F.dvp * kvb, 0);
     F.page_k = pk;
     F.page_v = pv;
+  } else if (rc == ICB_OK) {
+    // the host store: pinned, mapped into the device address space
+    const size_t nk = T * c.page_cap * c.page_size * F.dkp * kvb, nv = T * c.page_cap * c.page_size * F.dvp * kvb;
+    for (int i = 0; i < 2 && rc == ICB_OK; ++i) {
+      void* h = nullptr;
+      cudaError_t e = cudaHostAlloc(&h, i ? nv : nk, cudaHostAllocMapped | cudaHostAllocPortable);
+      if (e != cudaSuccess) { icb_set_error(ICB_E_CUDA, cudaGetErrorString(e)); rc = ICB_E_CUDA; break; }
+      f->host_allocs.push_back(h);
+      memset(h, 0, i ? nv : nk);
+      void* d = nullptr;
+      e = cudaHostGetDevicePointer(&d, h, 0);
+      if (e != cudaSuccess) { icb_set_error(ICB_E_CUDA, cudaGetErrorString(e)); rc = ICB_E_CUDA; break; }
+      (i ? F.page_v : F.page_k) = d;
+    }
+    char* qk = nullptr;
+    char* qv = nullptr;
+    if (rc == ICB_OK) rc = falloc(f, &qk, T * F.pool_cap * c.page_size * F.dkp * kvb, 0);
+    if (rc == ICB_OK) rc = falloc(f, &qv, T * F.pool_cap * c.page_size * F.dvp * kvb, 0);
+    F.pool_k = qk;
+    F.pool_v = qv;
+    if (rc == ICB_OK) rc = falloc(f, &F.page_slot, T * c.page_cap, 0xff);
+    if (rc == ICB_OK) rc = falloc(f, &F.slot_page, T * F.pool_cap, 0xff);
+    if (rc == ICB_OK) rc = falloc(f, &F.pool_tmp, T * 2 * F.pool_cap, 0);
+    if (rc == ICB_OK) rc = falloc(f, &F.pool_bytes, T, 0);
   }
   if (rc != ICB_OK) {
     icb_forest_destroy(f);
@@ -143,6 +170,7 @@ int icb_forest_destroy(icb_forest* f) {
   if (!f) return ICB_OK;
   cudaDeviceSynchronize();
   for (void* p : f->allocs) cudaFree(p);
+  for (void* p : f->host_allocs) cudaFreeHost(p);
   if (f->qscratch) cudaFree(f->qscratch);
   if (f->iscratch) cudaFree(f->iscratch);
   if (f->ascratch) cudaFree(f->ascratch);
@@ -442,6 +470,22 @@ int icb_host_pcg_doubles(const uint32_t* words, int32_t n_words, const uint32_t*
   icb_seedseq_u64x4(words, n_words, spawn, n_spawn, st);
   Pcg64 g = icb_pcg_seed(st);
   for (int i = 0; i < n; ++i) out[i] = icb_pcg_double(g);
+  return ICB_OK;
+}
+
+int icb_pool_stats(icb_forest* f, int64_t* out) {
+  if (!f->view.kv_host) { icb_set_error(ICB_E_CONFIG, "the forest keeps its KV in HBM (kv_host = 0)"); return ICB_E_CONFIG; }
+  const int T = f->cfg.n_trees;
+  std::vector<int> slot_page((size_t)T * f->view.pool_cap);
+  std::vector<long long> bytes(T);
+  ICB_CUDA(cudaMemcpy(bytes.data(), f->view.pool_bytes, sizeof(long long) * T, cudaMemcpyDeviceToHost));
+  ICB_CUDA(cudaMemcpy(slot_page.data(), f->view.slot_page, sizeof(int) * slot_page.size(), cudaMemcpyDeviceToHost));
+  for (int t = 0; t < T; ++t) {
+    long long res = 0;
+    for (int s = 0; s < f->view.pool_cap; ++s) res += slot_page[(size_t)t * f->view.pool_cap + s] >= 0;
+    out[2 * t] = bytes[t];
+    out[2 * t + 1] = res;
+  }
   return ICB_OK;
 }
 

@@ -122,6 +122,16 @@ struct ForestView {
   uint32_t* prev_sel; // [T][page_cap/32 + 1] residency: previous step's selection
   int* upper;         // [T][upper_cap] points with top level >= 2
   int upper_cap;
+  // KV offload (icb_forest_config.kv_host): page_k / page_v are the pinned,
+  // mapped host store; pages a step attends are gathered into a per-tree HBM
+  // pool of pool_cap page slots (pagestore.py:169-215 backload / evict)
+  int kv_host, pool_cap;
+  void* pool_k;       // [T][pool_cap][s][dkp]
+  void* pool_v;       // [T][pool_cap][s][dvp]
+  int* page_slot;     // [T][page_cap] pool slot of a resident page, -1 if not resident
+  int* slot_page;     // [T][pool_cap] page held by a slot, -1 if free
+  int* pool_tmp;      // [T][2 * pool_cap] gather scratch (free slots, pages to copy)
+  long long* pool_bytes; // [T] bytes gathered host -> pool so far
 
   __device__ __forceinline__ size_t tk(int t, int tok) const { return (size_t)t * tok_cap + tok; }
   __device__ __forceinline__ size_t nd(int t, int n) const { return (size_t)t * node_cap + n; }

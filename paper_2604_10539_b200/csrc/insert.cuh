@@ -93,6 +93,14 @@ __device__ __forceinline__ void set_own(const ForestView& F, int t, int tok, int
   F.own_list[(size_t)t * F.own_cap + F.own_base[F.tk(t, tok)] + lv - 1] = node;
 }
 
+// KV offload: the HBM pool row mirroring page `page` row `slot` when the page
+// is resident in the pool (writes go to the host store and to that copy).
+__device__ __forceinline__ size_t pool_dst(const ForestView& F, int t, int page, int slot) {
+  if (!F.kv_host) return ~(size_t)0;
+  const int sl = F.page_slot[F.pg(t, page)];
+  return sl < 0 ? ~(size_t)0 : ((size_t)t * F.pool_cap + sl) * F.s + slot;
+}
+
 // Copy one entry into a page slot (one warp; lane l owns dims 4l..4l+3).
 // K/V come either from fp32 arrays or from another page slot of the same
 // forest (window rotation).  Every source element is loaded before any store
@@ -123,6 +131,11 @@ __device__ inline void write_slot(const ForestView& F, int t, int page, int slot
     }
     if (j0 < F.dkp) *reinterpret_cast<uint2*>(K + dst * F.dkp + j0) = kw;
     if (j0 < F.dvp) *reinterpret_cast<uint2*>(V + dst * F.dvp + j0) = vw;
+    const size_t pd = pool_dst(F, t, page, slot);
+    if (pd != ~(size_t)0) {
+      if (j0 < F.dkp) *reinterpret_cast<uint2*>((__nv_bfloat16*)F.pool_k + pd * F.dkp + j0) = kw;
+      if (j0 < F.dvp) *reinterpret_cast<uint2*>((__nv_bfloat16*)F.pool_v + pd * F.dvp + j0) = vw;
+    }
   } else {
     float* K = (float*)F.page_k;
     float* V = (float*)F.page_v;
@@ -142,6 +155,11 @@ __device__ inline void write_slot(const ForestView& F, int t, int page, int slot
     }
     if (j0 < F.dkp) *reinterpret_cast<float4*>(K + dst * F.dkp + j0) = kw;
     if (j0 < F.dvp) *reinterpret_cast<float4*>(V + dst * F.dvp + j0) = vw;
+    const size_t pd = pool_dst(F, t, page, slot);
+    if (pd != ~(size_t)0) {
+      if (j0 < F.dkp) *reinterpret_cast<float4*>((float*)F.pool_k + pd * F.dkp + j0) = kw;
+      if (j0 < F.dvp) *reinterpret_cast<float4*>((float*)F.pool_v + pd * F.dvp + j0) = vw;
+    }
   }
 }
 
@@ -556,6 +574,13 @@ __device__ void rotate_tree(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
   if (threadIdx.x == 0) {
     // release (pagestore.py:157-162) then a fresh window page
     F.page_role[F.pg(t, old)] = 0;
+    if (F.kv_host) {   // its pool slot, if resident, is free again
+      const int sl = F.page_slot[F.pg(t, old)];
+      if (sl >= 0) {
+        F.slot_page[(size_t)t * F.pool_cap + sl] = -1;
+        F.page_slot[F.pg(t, old)] = -1;
+      }
+    }
     for (int i = 0; i + 1 < m->n_window; ++i) m->win[i] = m->win[i + 1];
     int np = m->next_page;
     if (np >= F.page_cap) { set_err(m, ICB_ERR_CAP_PAGES); }

@@ -32,6 +32,7 @@ struct icb_forest {
   icb_forest_config cfg;
   ForestView view;
   std::vector<void*> allocs;
+  std::vector<void*> host_allocs;   // pinned, mapped host store (kv_host)
   // persistent scratch for queries / inserts (grown on demand)
   void* qscratch = nullptr;
   size_t qscratch_bytes = 0;

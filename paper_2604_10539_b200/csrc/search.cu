@@ -194,10 +194,27 @@ __global__ void __launch_bounds__(NT, 512 / NT) query_kernel(ForestView F, Query
     float* ob = A.attn_out + (size_t)b * G * F.dim_v;
     int64_t* stb = A.attn_stats ? A.attn_stats + (size_t)b * 5 : nullptr;
     const long long ta = clock64();
-    if (F.kv_bf16)
+    if (F.kv_host) {
+      // KV offload: gather this step's pages into the tree's HBM pool, then
+      // attend from the pool (written by this CTA: coherent loads)
+      const long long moved = F.kv_bf16 ? gather_pages<__nv_bfloat16, NT>(F, t, sel, nsel, pbits)
+                                        : gather_pages<float, NT>(F, t, sel, nsel, pbits);
+      __shared__ unsigned long long s_moved;
+      if (threadIdx.x == 0) s_moved = 0;
+      __syncthreads();
+      atomicAdd(&s_moved, (unsigned long long)moved);
+      __syncthreads();
+      if (threadIdx.x == 0) F.pool_bytes[t] += (long long)s_moved;
+      if (F.kv_bf16)
+        attend_tree_paged<__nv_bfloat16, GP, NT, false>(F, t, G, qb, sel, nsel, ob, stb, A.scalar_bytes,
+                                                        A.scale_log2, sm);
+      else
+        attend_tree_paged<float, GP, NT, false>(F, t, G, qb, sel, nsel, ob, stb, A.scalar_bytes, A.scale_log2, sm);
+    } else if (F.kv_bf16) {
       attend_tree_paged<__nv_bfloat16, GP, NT, !STEP>(F, t, G, qb, sel, nsel, ob, stb, A.scalar_bytes, A.scale_log2, sm);
-    else
+    } else {
       attend_tree_paged<float, GP, NT, !STEP>(F, t, G, qb, sel, nsel, ob, stb, A.scalar_bytes, A.scale_log2, sm);
+    }
     if (A.P.prof && threadIdx.x == 0) atomicAdd(A.P.prof + 8, (unsigned long long)(clock64() - ta));
   }
 }

@@ -59,6 +59,10 @@ class EngineConfig:
     # rotation step), the inserts lose issue slots to co-resident
     # search CTAs
     fuse_rotation: bool = False
+    # BASELINE config 3: indexed layers' page K/V in pinned host memory, each
+    # step's pages gathered into a per-tree HBM pool (TierStore,
+    # pagestore.py:117-215); sink / window / skip layers stay resident
+    kv_offload: bool = False
 
     def __post_init__(self) -> None:
         if min(self.layers, self.kv_heads, self.query_heads_per_group, self.d, self.d_prime) < 1:
@@ -81,6 +85,9 @@ class EngineConfig:
             raise ConfigError("scalar_bytes must be >= 1")
         if self.kv_dtype not in ("fp32", "bf16"):
             raise ConfigError("kv_dtype must be fp32 or bf16")
+        if self.kv_offload and self.fuse_rotation:
+            raise ConfigError("kv_offload does not combine with fuse_rotation (the fused step would read host "
+                              "rows it wrote in the same launch)")
         if self.compare_baseline:
             raise ConfigError("compare_baseline (TokenOrderBaseline, engine.py:148-182) is outside the device path")
 
@@ -195,9 +202,13 @@ class Engine:
         H = cfg.kv_heads
         T = Li * H
         self.T = T
+        # KV offload: the pool holds a step's sink, window and largest selection
+        pool = (cfg.query_heads_per_group * min(cfg.token_budget, self.max_tokens) + cfg.sink_pages
+                + cfg.window_pages + 2)
         self.forest = DeviceForest(T, cfg.d, cfg.d_prime, tok_cap=self.max_tokens,
                                    promotion_ratio=cfg.promotion_ratio, page_size=s,
-                                   kv_dtype=cfg.kv_dtype, device=dev,
+                                   kv_dtype=cfg.kv_dtype, device=dev, kv_host=cfg.kv_offload,
+                                   pool_pages=pool if cfg.kv_offload else 0,
                                    caps=ForestCaps.for_tokens(self.max_tokens, cfg.promotion_ratio, s,
                                                               extra_pages=cfg.sink_pages + 4 * cfg.window_pages
                                                               + self.max_tokens // s))

@@ -71,7 +71,10 @@ class DeviceForest:
 
     def __init__(self, n_trees: int, dim: int, dim_v: int, *, tok_cap: int, promotion_ratio: float = 0.1,
                  page_size: int = 16, kv_dtype: str = "fp32", caps: ForestCaps | None = None,
-                 device=None):
+                 device=None, kv_host: bool = False, pool_pages: int = 0):
+        """kv_host: page K/V live in pinned, device-mapped host memory; each fused
+        decode step gathers the pages it attends into a per-tree HBM pool of
+        `pool_pages` slots (TierStore backload / evict, pagestore.py:117-215)."""
         if not torch.cuda.is_available():
             raise RuntimeError("DeviceForest needs a CUDA device (B200); there is no CPU path")
         if dim > DPAD or dim_v > DPAD:
@@ -85,11 +88,19 @@ class DeviceForest:
                                 N.KV_BF16 if kv_dtype == "bf16" else N.KV_F32,
                                 self.caps.tok_cap, self.caps.node_cap, self.caps.page_cap,
                                 self.caps.member_cap, self.caps.own_cap, self.caps.dirs_cap,
-                                promotion_ratio)
+                                promotion_ratio, int(bool(kv_host)), int(pool_pages))
+        self.kv_host = bool(kv_host)
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             N.check(N.lib().icb_forest_create(ctypes.byref(c), ctypes.byref(h)))
         self.h = h
+
+    def pool_stats(self) -> np.ndarray:
+        """KV offload: [n_trees, 2] = bytes gathered host -> HBM pool so far, pages
+        resident in the pool now."""
+        out = np.zeros((self.n_trees, 2), dtype=np.int64)
+        N.check(N.lib().icb_pool_stats(self.h, out.ctypes.data_as(ctypes.c_void_p)))
+        return out
 
     def close(self):
         if getattr(self, "h", None):

@@ -177,3 +177,41 @@ def test_engine_evaluation_metrics(cuda_ok, name):
         ref = z["outputs"][t]
         o = out.cpu().numpy()
         assert (np.linalg.norm(o - ref, axis=-1) / np.linalg.norm(ref, axis=-1)).max() < 1e-3
+
+
+@pytest.mark.parametrize("kv", ["bf16", "fp32"])
+def test_kv_offload_matches_resident(cuda_ok, kv):
+    """BASELINE config 3: page K/V in pinned host memory, each step's sink,
+    window and selected pages gathered into the HBM pool (TierStore backload /
+    evict, pagestore.py:169-215).  Outputs, selections and step metrics equal
+    the all-resident engine bit for bit; the pool holds exactly the last step's
+    pages; the gathered bytes cover the reference's backload."""
+    import torch
+    from paper_2604_10539_b200.engine import Engine, EngineConfig
+    from oracle.workload import Spec, generate
+    sk = dict(n_tokens=2048 + 70, d=64, d_prime=64, clusters=16, layers=4, kv_heads=2,
+              query_heads_per_group=4, seed=3)
+    keys, values, queries, _ = generate(Spec(kind="clustered", **sk))
+    shape = dict(layers=4, kv_heads=2, query_heads_per_group=4, d=64, d_prime=64, seed=3)
+    cfg = dict(token_budget=32, skip_layers=1, kv_dtype=kv, max_tokens=2048 + 70)
+    res = Engine(EngineConfig(**shape, **cfg)).prefill(keys, values, 2048)
+    off = Engine(EngineConfig(**shape, **cfg, kv_offload=True)).prefill(keys, values, 2048)
+    assert off.forest.kv_host and not res.forest.kv_host
+    q = torch.as_tensor(queries, device="cuda")
+    k = torch.as_tensor(keys, device="cuda")
+    v = torch.as_tensor(values, device="cuda")
+    moved = 0
+    for t in range(64):
+        tok = 2048 + t
+        o1, m1 = res.decode_step(tok, q[tok], k[tok], v[tok])
+        o2, m2 = off.decode_step(tok, q[tok], k[tok], v[tok])
+        assert torch.equal(o1, o2), t
+        assert m1 == m2, t
+        moved += m2.bytes_moved
+        (i1, c1, p1, n1), (i2, c2, p2, n2) = res.selected(), off.selected()
+        assert (c1 == c2).all() and (n1 == n2).all(), t
+    ps = off.forest.pool_stats()
+    n_sel = np.asarray(n2)
+    fixed = off.cfg.sink_pages + off.cfg.window_pages
+    assert (ps[:, 1] == n_sel + fixed).all()
+    assert ps[:, 0].sum() > 0
