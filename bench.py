@@ -59,6 +59,9 @@ def parse():
                     help="selection reuse (anchor layers, engine.py:321-363); 0 = the reference default (off)")
     ap.add_argument("--kv-offload", action="store_true",
                     help="BASELINE config 3: page K/V in pinned host memory, per-step HBM page pool")
+    ap.add_argument("--seqs-per-gpu", type=int, default=1,
+                    help="BASELINE config 4: S independent sequences per GPU, decoded in lockstep in the same "
+                         "launches (their trees side by side: kv_heads x S)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
     return ap.parse_args()
@@ -145,9 +148,13 @@ def run_ours(args, rank, world):
     W = max(W, 40) if graph else W
     n0 = args.ctx
     total_steps = W + K + E2E_WARM + E2E_SEGMENTS * E2E_STEPS + 1
-    stream = clustered_stream(n0, total_steps, C2["layers"], C2["kv_heads"], C2["query_heads_per_group"],
-                              C2["d"], C2["d_prime"], seed=args.seed + rank, device=dev)
-    cfg = EngineConfig(**C2, seed=args.seed + rank, kv_dtype=args.kv, max_tokens=n0 + total_steps + 1,
+    S = args.seqs_per_gpu
+    # S sequences of equal length: per (layer, kv head) trees are independent and
+    # rotate in lockstep, so the batch is the model with kv_heads x S
+    cS = dict(C2, kv_heads=C2["kv_heads"] * S)
+    stream = clustered_stream(n0, total_steps, cS["layers"], cS["kv_heads"], cS["query_heads_per_group"],
+                              cS["d"], cS["d_prime"], seed=args.seed + rank, device=dev)
+    cfg = EngineConfig(**cS, seed=args.seed + rank, kv_dtype=args.kv, max_tokens=n0 + total_steps + 1,
                        layer_serial=args.layer_serial, cuda_graph=graph, reuse_stride=args.reuse_stride,
                        fuse_rotation=args.fuse_rotation, kv_offload=args.kv_offload)
     t0 = time.time()
@@ -270,12 +277,12 @@ def run_ours(args, rank, world):
     search_s = statistics.mean(q_ms) / 1e3
     peak, peak_kind = peaks()
     achieved = launch_bytes / search_s / 1e9
-    tokens_per_s = world * K / (ms_max / 1e3)
+    tokens_per_s = world * S * K / (ms_max / 1e3)
     heads = eng.T * C2["query_heads_per_group"]
 
     # ---- e2e: the next steps through the public API with host (pinned) inputs/outputs
     f.query, f.attention = orig_query, orig_attn
-    e2e_val = run_e2e(eng, stream, n0, W + K, E2E_STEPS, dev, world, E2E_SEGMENTS)
+    e2e_val = run_e2e(eng, stream, n0, W + K, E2E_STEPS, dev, world, E2E_SEGMENTS, seqs=S)
 
     traffic = read_ncu_traffic()
     offload = None
@@ -309,7 +316,7 @@ def run_ours(args, rank, world):
         "config": {"workload": "C2: Llama-3.1-8B-shaped decode, 32 layers (2 dense skip + 30 DCI-indexed), "
                                "GQA 32q/8kv, d=128, 32k ctx, budget 256, page 16",
                    "context": n0, "budget": 256, "beam": 512, "visit_cap": 1024, "page_size": 16,
-                   "layers": 32, "kv_heads": 8, "q_heads": 32, "sequences_per_gpu": 1,
+                   "layers": 32, "kv_heads": 8, "q_heads": 32, "sequences_per_gpu": S,
                    "parallelism": f"sequence-parallel x{world} (no collective)",
                    "layer_mode": "layer-serial" if args.layer_serial else "layers batched per step",
                    "step_execution": "timed region: eager launches; e2e: CUDA-graph replays (plain / rotating "
@@ -348,7 +355,7 @@ def rank_max(x, dev, world):
     return float(t.item())
 
 
-def run_e2e(eng, stream, n0, start, K2, dev, world, segments=1):
+def run_e2e(eng, stream, n0, start, K2, dev, world, segments=1, seqs=1):
     """Same metric through Engine.decode_step with pinned host inputs (H2D)
     and the step's outputs read back to pinned host memory (D2H) inside the
     timed region; whole-job tokens over the slowest rank's wall time.  The
@@ -382,7 +389,7 @@ def run_e2e(eng, stream, n0, start, K2, dev, world, segments=1):
                 eng.decode_step(tok, qh[i], kh[i], vh[i], metrics=False, out=outh[i])
             torch.cuda.synchronize()
             dt = rank_max(time.perf_counter() - t0, dev, world)
-            vals.append(world * K2 / dt)
+            vals.append(world * seqs * K2 / dt)
     finally:
         gc.enable()
     h2d = (qh[0].numel() + kh[0].numel() + vh[0].numel()) * 4
