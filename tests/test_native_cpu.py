@@ -134,6 +134,24 @@ def test_engine_config_validation_mirrors_reference():
             EngineConfig(**bad)
     c = EngineConfig(token_budget=256)
     assert c.budget() == (256, 512, 1024) and c.n_query_heads == c.kv_heads
+    # device-path options: KV offload and the fused rotation step do not combine
+    assert not c.kv_offload and not c.fuse_rotation
+    EngineConfig(kv_offload=True)
+    EngineConfig(fuse_rotation=True)
+    with pytest.raises(ConfigError):
+        EngineConfig(kv_offload=True, fuse_rotation=True)
+
+
+def test_forest_config_struct_matches_header():
+    """icb_forest_config as ctypes sees it: field order and offsets of the C
+    struct (include/icecache_b200.h), including the KV-offload fields."""
+    from paper_2604_10539_b200 import _native as N
+    hdr = open(os.path.join(ROOT, "include", "icecache_b200.h")).read()
+    body = hdr[hdr.index("typedef struct {", hdr.index("typedef struct icb_forest icb_forest;")):]
+    body = body[:body.index("} icb_forest_config;")]
+    names = re.findall(r"^\s*(?:int32_t|double)\s+(\w+);", body, flags=re.M)
+    assert [f for f, _ in N.icb_forest_config._fields_] == names
+    assert N.icb_forest_config.kv_host.offset == 56 and ctypes.sizeof(N.icb_forest_config) == 64
 
 
 def test_sequence_sharding():
