@@ -275,6 +275,11 @@ int icb_query_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, co
     icb_set_error(ICB_E_INPUT, "decode step needs attention outputs, a device token and window K/V");
     return ICB_E_INPUT;
   }
+  if (step && f->view.kv_host) {
+    // the step's append would write host rows its own gather reads in the same launch
+    icb_set_error(ICB_E_CONFIG, "icb_step_attend does not support kv_host forests; use the separate launches");
+    return ICB_E_CONFIG;
+  }
   if (attn_out && (lifted_input || !out_pages)) {
     icb_set_error(ICB_E_INPUT, "fused attention needs raw queries and page outputs");
     return ICB_E_INPUT;
