@@ -155,9 +155,27 @@ def make_engine_goldens(only=None):
         print("engine", name, rows[0], rows[-1])
 
 
+def make_trace_golden():
+    """An ICET trace written by the reference's save_trace (workload.py:175-192)
+    and the arrays its load_trace (:195-224) returns."""
+    from icecache.workload import WorkloadSpec, generate_workload, load_trace, save_trace
+    spec = WorkloadSpec(kind="clustered", n_tokens=40, d=12, d_prime=6, clusters=4, layers=3, kv_heads=2,
+                        query_heads_per_group=2, seed=11)
+    path = os.path.join(OUT, "trace_small.icet")
+    save_trace(generate_workload(spec), path)
+    back = load_trace(path)
+    np.savez_compressed(os.path.join(OUT, "trace_small.npz"), keys=back.keys, values=back.values,
+                        queries=back.queries, shape=np.array([back.spec.layers, back.spec.kv_heads,
+                                                              back.spec.query_heads_per_group, back.spec.d,
+                                                              back.spec.d_prime, back.spec.n_tokens]))
+    print("trace", os.path.getsize(path), "bytes")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["tree", "engine"]
+    which = sys.argv[1:] or ["tree", "engine", "trace"]
     if "tree" in which:
         make_tree_goldens()
+    if "trace" in which:
+        make_trace_golden()
     if "engine" in which:
-        make_engine_goldens([w for w in which if w not in ("tree", "engine")] or None)
+        make_engine_goldens([w for w in which if w not in ("tree", "engine", "trace")] or None)
