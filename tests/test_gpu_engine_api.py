@@ -97,3 +97,33 @@ def test_gqa_groups_share_the_union(cuda_ok):
         for g in range(ids.shape[1]):
             per_head |= set(int(t2p[t]) for t in ids[tr, g, :counts[tr, g]])
         assert per_head == set(int(p) for p in pages[tr, :npages[tr]])
+
+
+def test_page_bound_fuzz(cuda_ok):
+    """Acceptance test 05 (test_acceptance.py:107-132): 10,000 random queries
+    with random k in [1, 64] against one tree; every selection has at most k
+    pages, and the tokens loaded with them fit in pages x page size.  Batched
+    by k: the same tree repeated along the launch, one query per row."""
+    import torch
+    from paper_2604_10539_b200.dci import SearchBudget
+    Engine, cfg, k, v, q = _small(seed=105, n_tokens=2049, layers=3, kv_heads=1, d=16, d_prime=8, token_budget=64)
+    eng = Engine(cfg).prefill(k, v, 2048)
+    f, tree = eng.forest, eng.T - 1                  # layer 2, head 0
+    pages_of = {p: len(toks) for p, (role, toks) in f.export(tree)["pages"].items()}
+    rng = np.random.default_rng(1055)
+    qs = rng.normal(size=(10_000, 16)).astype(np.float32)
+    ks = rng.integers(1, 65, size=10_000)
+    s = cfg.page_size
+    violations = 0
+    for kk in np.unique(ks):
+        rows = np.nonzero(ks == kk)[0]
+        b = SearchBudget.for_k(int(kk))
+        _, _, pages, npages = f.query(torch.full((len(rows),), tree, dtype=torch.int32), qs[rows][:, None, :],
+                                      b.k, b.beam, b.visit_cap)
+        pages, npages = pages.cpu().numpy(), npages.cpu().numpy()
+        for i in range(len(rows)):
+            sel = pages[i, :npages[i]]
+            loaded = sum(pages_of[int(p)] for p in sel)
+            if loaded > len(sel) * s or len(sel) > kk:
+                violations += 1
+    assert violations == 0
