@@ -910,16 +910,30 @@ __global__ void build_pages_kernel(ForestView F, BuildArgs A, int max_nodes, con
     const float* kin = A.keys + ((size_t)b * P + pos) * F.dim;
     const float* vin = A.values ? A.values + ((size_t)b * P + pos) * F.dim_v : nullptr;
     size_t kslot = (F.pg(t, page) * F.s + slot);
+    // lane l writes dims 4l..4l+3 (row strides are multiples of 4; padding
+    // stays zero): one 8- or 16-byte store per lane, one contiguous row per
+    // warp store -- few, large writes also when the store is host memory
+    const int j0 = lane * 4;
+    float k4[4], v4[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      k4[u] = j0 + u < F.dim ? kin[j0 + u] : 0.f;
+      v4[u] = (vin && j0 + u < F.dim_v) ? vin[j0 + u] : 0.f;
+    }
     if (F.kv_bf16) {
       __nv_bfloat16* K = (__nv_bfloat16*)F.page_k + kslot * F.dkp;
       __nv_bfloat16* V = (__nv_bfloat16*)F.page_v + kslot * F.dvp;
-      for (int j = lane; j < F.dim; j += 32) K[j] = __float2bfloat16_rn(kin[j]);
-      for (int j = lane; j < F.dim_v; j += 32) V[j] = __float2bfloat16_rn(vin ? vin[j] : 0.f);
+      __nv_bfloat162 k01 = __floats2bfloat162_rn(k4[0], k4[1]), k23 = __floats2bfloat162_rn(k4[2], k4[3]);
+      __nv_bfloat162 v01 = __floats2bfloat162_rn(v4[0], v4[1]), v23 = __floats2bfloat162_rn(v4[2], v4[3]);
+      if (j0 < F.dkp)
+        *reinterpret_cast<uint2*>(K + j0) = make_uint2(*reinterpret_cast<unsigned*>(&k01), *reinterpret_cast<unsigned*>(&k23));
+      if (j0 < F.dvp)
+        *reinterpret_cast<uint2*>(V + j0) = make_uint2(*reinterpret_cast<unsigned*>(&v01), *reinterpret_cast<unsigned*>(&v23));
     } else {
       float* K = (float*)F.page_k + kslot * F.dkp;
       float* V = (float*)F.page_v + kslot * F.dvp;
-      for (int j = lane; j < F.dim; j += 32) K[j] = kin[j];
-      for (int j = lane; j < F.dim_v; j += 32) V[j] = vin ? vin[j] : 0.f;
+      if (j0 < F.dkp) *reinterpret_cast<float4*>(K + j0) = make_float4(k4[0], k4[1], k4[2], k4[3]);
+      if (j0 < F.dvp) *reinterpret_cast<float4*>(V + j0) = make_float4(v4[0], v4[1], v4[2], v4[3]);
     }
   }
   (void)leaf_total;

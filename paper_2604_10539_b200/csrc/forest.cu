@@ -141,7 +141,8 @@ int icb_forest_create(const icb_forest_config* cfg, icb_forest** out) {
       cudaError_t e = cudaHostAlloc(&h, i ? nv : nk, cudaHostAllocMapped | cudaHostAllocPortable);
       if (e != cudaSuccess) { icb_set_error(ICB_E_CUDA, cudaGetErrorString(e)); rc = ICB_E_CUDA; break; }
       f->host_allocs.push_back(h);
-      memset(h, 0, i ? nv : nk);
+      // no memset: freshly pinned pages are zero, and every row is written at
+      // full padded width (build scatter, write_slot) before anything reads it
       void* d = nullptr;
       e = cudaHostGetDevicePointer(&d, h, 0);
       if (e != cudaSuccess) { icb_set_error(ICB_E_CUDA, cudaGetErrorString(e)); rc = ICB_E_CUDA; break; }

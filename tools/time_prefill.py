@@ -34,7 +34,7 @@ for rep in range(2):
     times.clear()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    eng = Engine(EngineConfig(**C2, kv_dtype="bf16", max_tokens=ctx + 8)).prefill(st.keys, st.values, ctx)
+    eng = Engine(EngineConfig(**C2, kv_dtype="bf16", max_tokens=ctx + 8, kv_offload=bool(os.environ.get("KVOFF")))).prefill(st.keys, st.values, ctx)
     torch.cuda.synchronize()
     total = time.perf_counter() - t0
     print(f"prefill {total:.3f}s  device build {times.get('build', 0):.3f}s  other {total - times.get('build', 0):.3f}s")
@@ -44,7 +44,7 @@ for rep in range(2):
 if os.environ.get("KPROF"):
     from torch.profiler import profile, ProfilerActivity
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-        eng = Engine(EngineConfig(**C2, kv_dtype="bf16", max_tokens=ctx + 8)).prefill(st.keys, st.values, ctx)
+        eng = Engine(EngineConfig(**C2, kv_dtype="bf16", max_tokens=ctx + 8, kv_offload=bool(os.environ.get("KVOFF")))).prefill(st.keys, st.values, ctx)
         torch.cuda.synchronize()
     print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=15, max_name_column_width=50))
 
