@@ -171,8 +171,10 @@ int icb_sparse_attention(icb_forest *f, const int32_t *trees, int32_t n, int32_t
                          int32_t scalar_bytes, int32_t splits, void *stream);
 
 /* Dense decode attention (skip layers / fallback): n heads-groups, G query
- * heads each, over n_tokens contiguous K/V rows.  k, v dev [n][ld][dim]
- * (kv_dtype), q dev [n][G][dim], out dev [n][G][dim_v]. */
+ * heads each, over n_tokens contiguous K/V rows.  k dev [n][ld][ceil4(dim)],
+ * v dev [n][ld][ceil4(dim_v)] (kv_dtype; rows padded to 4 elements, as
+ * icb_dense_append writes them), q dev [n][G][dim], out dev [n][G][dim_v].
+ * Logits are scaled by 1/sqrt(dim) (attention.py:70, d = q.size). */
 int icb_dense_attention(int32_t n, int32_t G, int32_t dim, int32_t dim_v, int32_t kv_dtype,
                         const float *q, const void *k, const void *v, int64_t ld,
                         int32_t n_tokens, float *out, int32_t splits, void *stream);
@@ -214,6 +216,35 @@ int icb_dense_attention_dev(int32_t n, int32_t G, int32_t dim, int32_t dim_v, in
 int icb_dense_append(int32_t n, int32_t dim, int32_t dim_v, int32_t kv_dtype, const float *k,
                      const float *v, void *dense_k, void *dense_v, int64_t ld,
                      const int32_t *token_dev, void *stream);
+
+/* Reference-shaped attention outputs (AttentionOutput.weights,
+ * attention.py:26-93).  The decode hot path computes only value_out; these
+ * serve the API around it.
+ *
+ * icb_exact_attention: full_attention (attention.py:55-74) of one query over
+ * n_rows key/value rows, all fp64: logits k.q / sqrt(dim), max-subtracted
+ * softmax, weights @ V.  q dev [dim], k dev [n_rows][dim], v dev
+ * [n_rows][dim_v] (double); weights dev [n_rows], out dev [dim_v] (double).
+ *
+ * icb_attention_weights: for each tree trees[b] and query head g, the tokens
+ * of its attended set in entry order -- sink pages, window pages, selected
+ * pages (pages dev [n][pages_cap], npages dev [n]) each in append order
+ * (engine.py:454-461) -- and their softmax weights, logits in fp64 from the
+ * stored K (kv dtype) and the fp32 query (q dev [n][G][dim]).  out_tokens dev
+ * [n][cap] int32, out_weights dev [n][G][cap] double, out_count dev [n]
+ * (attended tokens; entries past cap are dropped).
+ *
+ * icb_dense_weights: the same over dense planes (skip layers / fallback,
+ * engine.py:418-422): rows [0, n_tokens) of k dev [n][ld][ceil4(dim)];
+ * out_weights dev [n][G][n_tokens]. */
+int icb_exact_attention(int32_t n_rows, int32_t dim, int32_t dim_v, const double *q, const double *k,
+                        const double *v, double *weights, double *out, void *stream);
+int icb_attention_weights(icb_forest *f, const int32_t *trees, int32_t n, int32_t G, const float *queries,
+                          const int32_t *pages, int32_t pages_cap, const int32_t *npages,
+                          int32_t *out_tokens, double *out_weights, int32_t cap, int32_t *out_count,
+                          void *stream);
+int icb_dense_weights(int32_t n, int32_t G, int32_t dim, int32_t kv_dtype, const float *q, const void *k,
+                      int64_t ld, int32_t n_tokens, double *out_weights, void *stream);
 
 /* Per-tree summary (host out[16]): levels, top_node, n_nodes, next_page,
  * n_points, err, n_window, n_sink, query_count, distance_evals, scale_clamps,

@@ -9,7 +9,11 @@ sparse paged attention run as sm_100a kernels behind a C ABI
 from .errors import (ConfigError, ConsistencyError, DegenerateQueryError, IceCacheError, InputError,
                      InvariantViolation, PolicyError, ScaleViolationError)
 from .forest import DeviceForest, ForestCaps, dense_attention, entropy_words
+from .attention import AttentionOutput, HeadGroup, full_attention, gqa_union, sparse_attention
 from .dci import (PARENT_BUDGET, SENTINEL_LEVEL, DciTree, KeyScale, SearchBudget, assign_level, dci_indexing,
-                  gqa_union, query_raw, transform_query)
+                  query_raw, transform_query)
+from .engine import Engine, EngineConfig, StepMetrics, prefill
+from .pagestore import Page, PageTable, TierStore, TransferStats, TreePageTable, find_page_index
+from .workload import DecodeStep, Workload, WorkloadSpec, generate_workload
 
 __version__ = "0.1.0"

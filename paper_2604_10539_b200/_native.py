@@ -77,6 +77,9 @@ EXPORTS = {
                         ctypes.c_int),
     "icb_sparse_attention": ([P, P, I32, I32, P, P, I32, P, P, P, I32, I32, P], ctypes.c_int),
     "icb_dense_attention": ([I32, I32, I32, I32, I32, P, P, P, I64, I32, P, I32, P], ctypes.c_int),
+    "icb_exact_attention": ([I32, I32, I32, P, P, P, P, P, P], ctypes.c_int),
+    "icb_attention_weights": ([P, P, I32, I32, P, P, I32, P, P, P, I32, P, P], ctypes.c_int),
+    "icb_dense_weights": ([I32, I32, I32, I32, P, P, I64, I32, P, P], ctypes.c_int),
     "icb_tree_info": ([P, I32, P], ctypes.c_int),
     "icb_export_tree": ([P, I32] + [P] * 18, ctypes.c_int),
     "icb_read_pages": ([P, I32, P, I32, P, P], ctypes.c_int),

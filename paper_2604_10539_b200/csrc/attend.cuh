@@ -400,8 +400,13 @@ __device__ void attend_tree_paged(const ForestView& F, int t, int GA, const floa
   constexpr int CH = (sizeof(KT) == 2 ? 16 : 8) / (G >= 4 ? 2 : 1) / (G >= 8 ? 2 : 1);
   for (int i = warp; i < total; i += NW) {
     const int p = i < nsink ? m->sink[i] : i < nfix ? m->win[i - nsink] : sel[i - nfix];
+    int slot = 0;
+    if (F.kv_host) {
+      slot = F.page_slot[F.pg(t, p)];
+      if (slot < 0) continue;   // pool overflow (ICB_ERR_CAP_SCRATCH is set): never read outside the pool
+    }
     const int fill = F.page_fill[F.pg(t, p)];
-    const size_t base = F.kv_host ? ((size_t)t * F.pool_cap + F.page_slot[F.pg(t, p)]) * F.s : F.pg(t, p) * F.s;
+    const size_t base = F.kv_host ? ((size_t)t * F.pool_cap + slot) * F.s : F.pg(t, p) * F.s;
     if constexpr (G == 4) {
       for (int r0 = 0; r0 < fill; r0 += 8)
         attend_chunk8_g4<KT, NC>(g4, q2, K, V, base + r0, min(8, fill - r0), F.dkp, F.dvp, lane, F.dim, F.dim_v,

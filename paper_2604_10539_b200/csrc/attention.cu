@@ -23,6 +23,7 @@ struct AttnArgs {
   const void* k;
   const void* v;
   long long ld;
+  int ldk, ldv;                // dense mode row strides: ceil4(dim), ceil4(dim_v)
   int n_tokens;
   const int32_t* token_dev;    // dense mode: rows [0, *token_dev + 1) when set (CUDA-graph replays)
   float* out;                  // [n][G][dim_v]
@@ -40,7 +41,6 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attn_kernel(ForestView F, Att
   const int b = blockIdx.x, sp = blockIdx.y, S = A.splits;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = kAttnThreads / 32;
   __shared__ int s_pages[1024];
-  __shared__ int s_np;
   __shared__ float s_red[kAttnThreads / 32][G][2];
   __shared__ float4 s_acc[kAttnThreads / 32][G][32];
   __shared__ bool s_last;
@@ -80,32 +80,36 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attn_kernel(ForestView F, Att
     const int nfix = m->n_sink + m->n_window;
     const int total = nfix + nsel;
     const int p0 = (int)((long long)total * sp / S), p1 = (int)((long long)total * (sp + 1) / S);
-    if (threadIdx.x == 0) s_np = min(p1 - p0, 1024);
-    for (int i = threadIdx.x; i < p1 - p0 && i < 1024; i += kAttnThreads) {
-      int gi = p0 + i;
-      int p;
-      if (gi < m->n_sink) p = m->sink[gi];
-      else if (gi < nfix) p = m->win[gi - m->n_sink];
-      else p = A.pages[(size_t)b * A.pages_cap + gi - nfix];
-      s_pages[i] = p;
-    }
-    __syncthreads();
     const KT* K = (const KT*)F.page_k;
     const KT* V = (const KT*)F.page_v;
     // rows per chunk, loaded together (register budget: 2 CTAs / SM)
     constexpr int CH = (sizeof(KT) == 2 ? 16 : 8) / (G >= 4 ? 2 : 1) / (G >= 8 ? 2 : 1);
-    for (int i = warp; i < s_np; i += NW) {
-      const int p = s_pages[i];
-      const int fill = F.page_fill[F.pg(t, p)];
-      const size_t base = F.pg(t, p) * F.s;
-      if constexpr (G == 4) {
-        for (int r0 = 0; r0 < fill; r0 += 8)
-          attend_chunk8_g4<KT>(g4, q2, K, V, base + r0, min(8, fill - r0), F.dkp, F.dvp, lane, A.dim, A.dim_v,
-                               A.scale_log2);
-      } else {
-        for (int r0 = 0; r0 < fill; r0 += CH)
-          attend_chunk<KT, G, CH>(h, qv, K, V, base + r0, min(CH, fill - r0), F.dkp, F.dvp, lane, A.dim, A.dim_v,
-                                  A.scale_log2);
+    // the split's page list is staged 1024 ids at a time
+    for (int c0 = p0; c0 < p1; c0 += 1024) {
+      const int cn = min(p1 - c0, 1024);
+      __syncthreads();   // previous chunk consumed
+      for (int i = threadIdx.x; i < cn; i += kAttnThreads) {
+        int gi = c0 + i;
+        int p;
+        if (gi < m->n_sink) p = m->sink[gi];
+        else if (gi < nfix) p = m->win[gi - m->n_sink];
+        else p = A.pages[(size_t)b * A.pages_cap + gi - nfix];
+        s_pages[i] = p;
+      }
+      __syncthreads();
+      for (int i = warp; i < cn; i += NW) {
+        const int p = s_pages[i];
+        const int fill = F.page_fill[F.pg(t, p)];
+        const size_t base = F.pg(t, p) * F.s;
+        if constexpr (G == 4) {
+          for (int r0 = 0; r0 < fill; r0 += 8)
+            attend_chunk8_g4<KT>(g4, q2, K, V, base + r0, min(8, fill - r0), F.dkp, F.dvp, lane, A.dim, A.dim_v,
+                                 A.scale_log2);
+        } else {
+          for (int r0 = 0; r0 < fill; r0 += CH)
+            attend_chunk<KT, G, CH>(h, qv, K, V, base + r0, min(CH, fill - r0), F.dkp, F.dvp, lane, A.dim,
+                                    A.dim_v, A.scale_log2);
+        }
       }
     }
     // residency accounting (pagestore.py:169-215) by split 0
@@ -141,17 +145,17 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attn_kernel(ForestView F, Att
       }
     }
   } else {
-    const KT* K = (const KT*)A.k + (size_t)b * A.ld * A.dim;
-    const KT* V = (const KT*)A.v + (size_t)b * A.ld * A.dim_v;
+    const KT* K = (const KT*)A.k + (size_t)b * A.ld * A.ldk;
+    const KT* V = (const KT*)A.v + (size_t)b * A.ld * A.ldv;
     const int ntok = A.token_dev ? *A.token_dev + 1 : A.n_tokens;
     const int r0 = (int)((long long)ntok * sp / S), r1 = (int)((long long)ntok * (sp + 1) / S);
     constexpr int CH = G == 4 ? 8 : (sizeof(KT) == 2 ? 16 : 8) / (G >= 4 ? 2 : 1) / (G >= 8 ? 2 : 1);
     for (int r = r0 + warp * CH; r < r1; r += NW * CH) {
       if constexpr (G == 4)
-        attend_chunk8_g4<KT>(g4, q2, K, V, (size_t)r, min(CH, r1 - r), A.dim, A.dim_v, lane, A.dim, A.dim_v,
+        attend_chunk8_g4<KT>(g4, q2, K, V, (size_t)r, min(CH, r1 - r), A.ldk, A.ldv, lane, A.dim, A.dim_v,
                              A.scale_log2);
       else
-        attend_chunk<KT, G, CH>(h, qv, K, V, (size_t)r, min(CH, r1 - r), A.dim, A.dim_v, lane, A.dim, A.dim_v,
+        attend_chunk<KT, G, CH>(h, qv, K, V, (size_t)r, min(CH, r1 - r), A.ldk, A.ldv, lane, A.dim, A.dim_v,
                                 A.scale_log2);
     }
   }
@@ -185,7 +189,11 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attn_kernel(ForestView F, Att
     }
     float* pg = part + (size_t)g * (2 + A.dim_v);
     if (ln == 0) { pg[0] = mx; pg[1] = l; }
-    if (ln * 4 < A.dim_v) { pg[2 + ln * 4] = acc.x; pg[3 + ln * 4] = acc.y; pg[4 + ln * 4] = acc.z; pg[5 + ln * 4] = acc.w; }
+    const int j0 = ln * 4;
+    if (j0 < A.dim_v) pg[2 + j0] = acc.x;
+    if (j0 + 1 < A.dim_v) pg[3 + j0] = acc.y;
+    if (j0 + 2 < A.dim_v) pg[4 + j0] = acc.z;
+    if (j0 + 3 < A.dim_v) pg[5 + j0] = acc.w;
   }
   // last CTA of this tree combines the splits
   __threadfence();
@@ -284,6 +292,8 @@ int icb_dense_attention_impl(int32_t n, int32_t G, int32_t dim, int32_t dim_v, i
   AttnArgs A{};
   A.n = n; A.G = G; A.dim = dim; A.dim_v = dim_v; A.splits = splits; A.q = q; A.k = k; A.v = v; A.ld = ld;
   A.n_tokens = n_tokens; A.token_dev = token_dev; A.out = out;
+  A.ldk = (dim + 3) & ~3; A.ldv = (dim_v + 3) & ~3;
+  // logits / sqrt(q.size) with the unpadded dimension (attention.py:70)
   A.scale_log2 = (float)(1.4426950408889634 / sqrt((double)dim));
   int rc = ensure_attn_scratch(nullptr, (size_t)n * splits * padded_g(G) * (2 + dim_v), n, &A.part, &A.counter);
   if (rc) return rc;

@@ -234,6 +234,15 @@ int icb_query(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, const f
                         out_counts, out_pages, pages_cap, out_npages, S_(stream));
 }
 
+static int check_pool(icb_forest* f, int32_t pages_cap) {
+  // KV offload: the pool must hold a step's sink + window + largest selection
+  if (f && f->view.kv_host && f->view.pool_cap < pages_cap + 2) {
+    icb_set_error(ICB_E_CONFIG, "pool_pages must cover sink + window + pages_cap (the largest selection)");
+    return ICB_E_CONFIG;
+  }
+  return ICB_OK;
+}
+
 int icb_query_attend(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, const float* queries, int32_t k,
                      int64_t beam, int64_t visit_cap, int32_t* out_ids, int32_t k_out, int32_t* out_counts,
                      int32_t* out_pages, int32_t pages_cap, int32_t* out_npages, float* attn_out,
@@ -241,6 +250,7 @@ int icb_query_attend(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, 
   if (k < 1) { icb_set_error(ICB_E_INPUT, "k must be >= 1"); return ICB_E_INPUT; }
   if (beam < k || visit_cap < k) { icb_set_error(ICB_E_CONFIG, "beam and visit_cap must be >= k"); return ICB_E_CONFIG; }
   if (!attn_out || !out_pages || !out_npages) { icb_set_error(ICB_E_INPUT, "null output"); return ICB_E_INPUT; }
+  if (int rc = check_pool(f, pages_cap)) return rc;
   return icb_query_impl(f, trees, n, G, queries, 0, k, beam, visit_cap, ICB_SENTINEL_LEVEL, out_ids, k_out,
                         out_counts, out_pages, pages_cap, out_npages, S_(stream), attn_out, attn_stats,
                         scalar_bytes);
@@ -254,6 +264,7 @@ int icb_step_attend(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, c
   if (k < 1) { icb_set_error(ICB_E_INPUT, "k must be >= 1"); return ICB_E_INPUT; }
   if (beam < k || visit_cap < k) { icb_set_error(ICB_E_CONFIG, "beam and visit_cap must be >= k"); return ICB_E_CONFIG; }
   if (!attn_out || !out_pages || !out_npages) { icb_set_error(ICB_E_INPUT, "null output"); return ICB_E_INPUT; }
+  if (int rc = check_pool(f, pages_cap)) return rc;
   StepOpts step{rotate, rot_stats, token_dev, win_keys, win_values};
   return icb_query_impl(f, trees, n, G, queries, 0, k, beam, visit_cap, ICB_SENTINEL_LEVEL, out_ids, k_out,
                         out_counts, out_pages, pages_cap, out_npages, S_(stream), attn_out, attn_stats,
@@ -299,7 +310,7 @@ int icb_sparse_attention(icb_forest* f, const int32_t* trees, int32_t n, int32_t
 int icb_dense_attention(int32_t n, int32_t G, int32_t dim, int32_t dim_v, int32_t kv_dtype, const float* q,
                         const void* k, const void* v, int64_t ld, int32_t n_tokens, float* out, int32_t splits,
                         void* stream) {
-  if (dim % 4 || dim_v % 4) { icb_set_error(ICB_E_CONFIG, "dense attention needs dims divisible by 4"); return ICB_E_CONFIG; }
+  if (dim < 1 || dim > 128 || dim_v < 1 || dim_v > 128) { icb_set_error(ICB_E_CONFIG, "dense attention supports 1 <= d, d' <= 128"); return ICB_E_CONFIG; }
   if (n_tokens < 1) { icb_set_error(ICB_E_INPUT, "empty key set"); return ICB_E_INPUT; }
   return icb_dense_attention_impl(n, G, dim, dim_v, kv_dtype, q, k, v, ld, n_tokens, nullptr, out, splits,
                                   S_(stream));
@@ -308,7 +319,7 @@ int icb_dense_attention(int32_t n, int32_t G, int32_t dim, int32_t dim_v, int32_
 int icb_dense_attention_dev(int32_t n, int32_t G, int32_t dim, int32_t dim_v, int32_t kv_dtype, const float* q,
                             const void* k, const void* v, int64_t ld, const int32_t* token_dev, float* out,
                             int32_t splits, void* stream) {
-  if (dim % 4 || dim_v % 4) { icb_set_error(ICB_E_CONFIG, "dense attention needs dims divisible by 4"); return ICB_E_CONFIG; }
+  if (dim < 1 || dim > 128 || dim_v < 1 || dim_v > 128) { icb_set_error(ICB_E_CONFIG, "dense attention supports 1 <= d, d' <= 128"); return ICB_E_CONFIG; }
   if (!token_dev || ld < 1) { icb_set_error(ICB_E_INPUT, "null device token / empty capacity"); return ICB_E_INPUT; }
   // splits sized for the full capacity; each CTA clips its rows to *token_dev + 1
   return icb_dense_attention_impl(n, G, dim, dim_v, kv_dtype, q, k, v, ld, (int32_t)ld, token_dev, out, splits,

@@ -19,8 +19,10 @@ import numpy as np
 import torch
 
 from . import _native as N
+from .attention import gqa_union  # noqa: F401  (re-exported: attention.py:96-103)
 from .errors import ConfigError, InputError
 from .forest import DeviceForest, ForestCaps
+from .pagestore import INDEXED, PageTable
 
 SENTINEL_LEVEL = -1            # dci.py:35
 ROOT_OWNER = -1                # dci.py:38
@@ -129,20 +131,44 @@ class DciTree:
         self.scale = scale
         self.promotion_ratio = promotion_ratio
         self.page_size = page_size
-        self.store, self.table = store, table
+        # store / table (dci.py:176-177): the device tree's pages are mirrored
+        # into them as the reference's _place_entry writes them (dci.py:368-381)
+        self.store = store
+        self.table = table if table is not None else (PageTable() if store is not None else None)
+        self._dev2store: dict[int, int] = {}
         self.parent_budget = parent_budget
         self.capacity = int(capacity)
         self.forest = DeviceForest(1, dim, self.dim_v, tok_cap=self.capacity, promotion_ratio=promotion_ratio,
                                    page_size=page_size, kv_dtype="fp32", device=device,
                                    caps=ForestCaps.for_tokens(self.capacity, promotion_ratio, page_size))
+        self._t = 0
         self.forest.seed([0], [seed])
         if scale is not None:
             N.check(N.lib().icb_set_scale(self.forest.h, 0, float(scale.c)))
         self._export = None
 
+    @classmethod
+    def bound(cls, forest: DeviceForest, tree: int, scale: float, promotion_ratio: float, page_size: int,
+              capacity: int) -> "DciTree":
+        """A view of tree `tree` of an existing forest (the Engine's trees):
+        the same read / query / insert API, no store mirror."""
+        self = cls.__new__(cls)
+        self.dim, self.dim_v = forest.dim, forest.dim_v
+        self.scale = KeyScale(float(scale))
+        self.promotion_ratio, self.page_size = promotion_ratio, page_size
+        self.store, self.table = None, None
+        self._dev2store = {}
+        self.parent_budget = PARENT_BUDGET
+        self.capacity = int(capacity)
+        self.forest = forest
+        self._t = int(tree)
+        self._export = None
+        self._live = True    # the engine mutates the tree between calls: never cache its export
+        return self
+
     # -- counters / structure (host mirror) ------------------------------------------
     def _info(self):
-        return self.forest.info(0)
+        return self.forest.info(self._t)
 
     def __len__(self) -> int:
         return self._info()["n_points"]
@@ -164,8 +190,8 @@ class DciTree:
         return self._info()["scale_clamps"]
 
     def export(self) -> dict:
-        if self._export is None:
-            self._export = self.forest.export(0)
+        if self._export is None or getattr(self, "_live", False):
+            self._export = self.forest.export(self._t)
         return self._export
 
     @property
@@ -184,17 +210,49 @@ class DciTree:
     def nodes(self) -> dict[int, DciNode]:
         ex = self.export()
         top = ex["info"]["top_node"]
-        return {i: DciNode(i, lv, None if i == top else par, own, list(mem), list(ex["leaf_pages"].get(i, [])))
+        pid = (lambda p: self._dev2store[p]) if self.store is not None else (lambda p: p)   # noqa: E731
+        return {i: DciNode(i, lv, None if i == top else par, own, list(mem),
+                           [pid(p) for p in ex["leaf_pages"].get(i, [])])
                 for i, lv, par, own, mem in ex["nodes"]}
 
     def lifted(self, point_id: int) -> np.ndarray:
         """The stored lifted key [dim + 1] (fp32 rows, returned as fp64)."""
-        ex = self.forest.export(0, with_rows=True)
+        ex = self.forest.export(self._t, with_rows=True)
         return np.concatenate([ex["lift"][point_id, : self.dim].astype(np.float64),
                                [float(ex["tail"][point_id])]])
 
     def page_fill(self, page_id: int) -> int:
         return len(self.export()["pages"][int(page_id)][1])
+
+    # -- store / table mirror (dci.py:368-381) -----------------------------------------
+    def _mirror_page(self, dev_page: int, leaf: int):
+        sp = self._dev2store.get(dev_page)
+        if sp is None:
+            page = self.store.allocate_page(self.page_size, INDEXED, resident=False)
+            sp = self._dev2store[dev_page] = page.page_id
+            self.table.assign_page(leaf, sp)
+        return self.store.page(sp)
+
+    def _mirror_build(self, ids, keys, values):
+        """Write the built tree's pages into the store in device page order
+        (leaves in node-id order, members in order: the reference's order)."""
+        ex = self.export()
+        row = {int(p): i for i, p in enumerate(ids)}
+        leaf_of = {p: leaf for leaf, pages in ex["leaf_pages"].items() for p in pages}
+        for dp in sorted(p for p, (role, _) in ex["pages"].items() if role == N.ROLE_INDEXED):
+            page = self._mirror_page(dp, leaf_of[dp])
+            for tok in ex["pages"][dp][1]:
+                r = row[tok]
+                page.append(tok, keys[r], values[r] if values is not None else np.zeros(self.store.d_prime))
+                self.table.map_token(tok, page.page_id)
+
+    def _mirror_insert(self, point_id: int, key, value):
+        ex = self.export()
+        dp = int(ex["tok2page"][point_id])
+        leaf = next(i for i, lv, _, _, mem in ex["nodes"] if lv == 1 and point_id in mem)
+        page = self._mirror_page(dp, leaf)
+        page.append(point_id, key, value if value is not None else np.zeros(self.store.d_prime))
+        self.table.map_token(point_id, page.page_id)
 
     # -- search --------------------------------------------------------------------
     def query(self, q_vec, target_level: int, k: int, budget: SearchBudget | None = None) -> list[int]:
@@ -208,7 +266,7 @@ class DciTree:
         return self._query(torch.as_tensor(q.astype(np.float32)), target_level, k, budget, lifted=True)
 
     def _query(self, q, target_level, k, budget, lifted):
-        ids, counts, _, _ = self.forest.query([0], q.reshape(1, 1, -1), k, budget.beam, budget.visit_cap,
+        ids, counts, _, _ = self.forest.query([self._t], q.reshape(1, 1, -1), k, budget.beam, budget.visit_cap,
                                               target_level, lifted=lifted, want_pages=False)
         self.forest.check()
         return [int(x) for x in ids[0, 0, : int(counts[0, 0])].cpu().tolist()]
@@ -228,7 +286,7 @@ class DciTree:
         qd = torch.as_tensor(q.astype(np.float32), device=dev)
         ids = torch.empty(max(1, min(int(k), self.capacity)), dtype=torch.int32, device=dev)
         cnt = torch.zeros(1, dtype=torch.int32, device=dev)
-        N.check(N.lib().icb_node_query(self.forest.h, 0, node_id, _ptr(qd), int(min(k, ids.numel())),
+        N.check(N.lib().icb_node_query(self.forest.h, self._t, node_id, _ptr(qd), int(min(k, ids.numel())),
                                        int(min(budget.visit_cap, 2**62)), _ptr(ids), _ptr(cnt), _stream()))
         self.forest.check()
         return [int(x) for x in ids[: int(cnt.item())].cpu().tolist()]
@@ -250,17 +308,19 @@ class DciTree:
             raise ConfigError("an empty tree needs a KeyScale before its first insert")
         val = np.zeros(self.dim_v) if value is None else np.asarray(value, dtype=float).reshape(self.dim_v)
         lv = None if level is None else np.array([[int(level)]], dtype=np.int32)
-        out = self.forest.insert([0], np.array([[point_id]], dtype=np.int32), key.reshape(1, 1, -1),
+        out = self.forest.insert([self._t], np.array([[point_id]], dtype=np.int32), key.reshape(1, 1, -1),
                                  val.reshape(1, 1, -1), levels=lv)
         self._export = None
         self.forest.check()
+        if self.store is not None:
+            self._mirror_insert(point_id, key, None if value is None else np.asarray(value, dtype=float))
         return int(out[0, 0])
 
     # -- integrity -----------------------------------------------------------------
     def check_invariants(self) -> None:
         """dci.py:453-476 on the exported device structure (AssertionError on
         violation)."""
-        ex = self.forest.export(0)
+        ex = self.forest.export(self._t)
         levels, top = ex["info"]["levels"], ex["info"]["top_node"]
         nodes = {n[0]: n for n in ex["nodes"]}
         assert levels >= 1 and top >= 0
@@ -308,6 +368,8 @@ def dci_indexing(keys, promotion_ratio: float, seed: int | tuple = 0, *, values=
     tree.forest.check()
     if tree.scale is None:
         tree.scale = KeyScale(tree.forest.scale(0))
+    if store is not None:
+        tree._mirror_build(ids, mat, vals)
     return tree
 
 
@@ -319,11 +381,3 @@ def query_raw(tree: DciTree, q, target_level: int, k: int, budget: SearchBudget 
     if q.shape != (tree.dim,):
         raise InputError(f"query must have shape ({tree.dim},), got {q.shape}")
     return tree._query(torch.as_tensor(q.astype(np.float32)), target_level, k, budget, lifted=False)
-
-
-def gqa_union(page_sets) -> set[int]:
-    """attention.py:96-103: union of the heads' page lists."""
-    out: set[int] = set()
-    for s in page_sets:
-        out.update(int(p) for p in s)
-    return out

@@ -22,7 +22,7 @@ import torch
 
 from . import _native as N
 from .errors import ConfigError, InputError
-from .forest import DeviceForest, ForestCaps, dense_append, dense_attention
+from .forest import DeviceForest, ForestCaps, _ptr, _stream, dense_append, dense_attention
 
 
 @dataclass
@@ -96,9 +96,15 @@ class EngineConfig:
         return self.kv_heads * self.query_heads_per_group
 
     def budget(self):
-        k = self.token_budget
-        return (k, self.beam if self.beam is not None else 2 * k,
-                self.visit_cap if self.visit_cap is not None else 4 * k)
+        """engine.py:97-98: the decode SearchBudget."""
+        from .dci import SearchBudget
+        return SearchBudget.for_k(self.token_budget, self.beam, self.visit_cap)
+
+    def head_groups(self):
+        """engine.py:100-103."""
+        from .attention import HeadGroup
+        g = self.query_heads_per_group
+        return [HeadGroup(h, tuple(range(h * g, (h + 1) * g))) for h in range(self.kv_heads)]
 
 
 @dataclass
@@ -124,6 +130,13 @@ def _dev(x, device, dtype=torch.float32):
     return torch.as_tensor(x, dtype=dtype, device=device)
 
 
+def _budget_tuple(b):
+    """A SearchBudget (dci.py:50-74) or a (k, beam, visit_cap) tuple."""
+    if hasattr(b, "visit_cap"):
+        return int(b.k), int(b.beam), int(b.visit_cap)
+    return tuple(int(x) for x in b)
+
+
 class Engine:
     def __init__(self, cfg: EngineConfig, device=None):
         self.cfg = cfg
@@ -144,13 +157,29 @@ class Engine:
         self._warmed = set()
         self._gbuf = None
         self._io = None
+        self._cum_stats = None     # [T, 5] host: residency counters summed over metric steps
+        self._anchor_tokens: dict[int, list[int]] = {}
 
     # -- prefill ---------------------------------------------------------------
-    def prefill(self, keys, values, n_prefill: int) -> "Engine":
-        """keys [n, L, H, d], values [n, L, H, d'] (numpy or tensors; only the
-        first n_prefill tokens are read)."""
+    def prefill(self, workload, n_prefill, *more) -> "Engine":
+        """engine.py:226-301.  Reference form: prefill(workload, n_prefill) with
+        a Workload (this package's or the reference's: anything with `spec`
+        and `prefill_view`).  Array form: prefill(keys [n, L, H, d],
+        values [n, L, H, d'], n_prefill) (numpy or tensors; only the first
+        n_prefill tokens are read)."""
         if self.prefilled:
             raise ConfigError("engine already prefilled")
+        if hasattr(workload, "prefill_view"):
+            if more:
+                raise InputError("prefill(workload, n_prefill) takes no further arguments")
+            self._check_workload(workload)
+            if n_prefill < 1:
+                raise ConfigError("prefill needs at least one token")
+            keys, values = workload.prefill_view(n_prefill)
+        else:
+            if len(more) != 1:
+                raise InputError("prefill(keys, values, n_prefill) or prefill(workload, n_prefill)")
+            keys, values, n_prefill = workload, n_prefill, more[0]
         if n_prefill < 1:
             raise ConfigError("prefill needs at least one token")
         cfg = self.cfg
@@ -180,7 +209,7 @@ class Engine:
             self._mk[:, :, :n_prefill] = keys.permute(1, 2, 0, 3)
             self._mv[:, :, :n_prefill] = values.permute(1, 2, 0, 3)
             self._indexed_mask = torch.zeros(self.max_tokens, dtype=torch.bool, device=dev)
-        self._dense_res = torch.empty((max(nd, 1), cfg.query_heads_per_group, dvpad), dtype=torch.float32,
+        self._dense_res = torch.empty((max(nd, 1), cfg.query_heads_per_group, cfg.d_prime), dtype=torch.float32,
                                       device=dev)   # dense attention output (nd planes)
         self.dense_k = torch.zeros((max(nd, 1), self.max_tokens, dpad), dtype=kvt, device=dev)
         self.dense_v = torch.zeros((max(nd, 1), self.max_tokens, dvpad), dtype=kvt, device=dev)
@@ -233,7 +262,7 @@ class Engine:
             f.build(self.trees_dev[c0:c1], tok[sink_end:win_start].expand(c1 - c0, -1),
                     ki[c0:c1, sink_end:win_start], vi[c0:c1, sink_end:win_start])
         f.check()
-        k, beam, cap = cfg.budget()
+        k, beam, cap = _budget_tuple(cfg.budget())
         self.k_eff = int(min(k, self.max_tokens))
         self.beam, self.visit_cap = int(min(beam, 2**62)), int(min(cap, 2**62))
         G = cfg.query_heads_per_group
@@ -243,6 +272,15 @@ class Engine:
         self._alloc_step_buffers()
         self.prefilled = True
         return self
+
+    def _check_workload(self, workload) -> None:
+        """engine.py:216-224."""
+        spec, cfg = workload.spec, self.cfg
+        if (spec.layers, spec.kv_heads, spec.query_heads_per_group) != \
+                (cfg.layers, cfg.kv_heads, cfg.query_heads_per_group):
+            raise ConfigError("workload head/layer shape does not match the engine config")
+        if (spec.d, spec.d_prime) != (cfg.d, cfg.d_prime):
+            raise ConfigError("workload dims do not match the engine config")
 
     def _alloc_step_buffers(self):
         cfg, dev, T = self.cfg, self.device, self.T
@@ -293,19 +331,32 @@ class Engine:
         return self.T * G
 
     def page_select(self, q, layer: int, kv_head: int, budget=None) -> list[int]:
-        """Pages holding the tree's top-budget tokens for one query (engine.py:305-310)."""
-        tokens = self.select_tokens(q, layer, kv_head, budget)
-        ex_t2p = self.forest.export(self._tree(layer, kv_head))["tok2page"]
-        return sorted({int(ex_t2p[t]) for t in tokens})
+        """Pages holding the tree's top-budget tokens for one query
+        (engine.py:305-310): the search kernel's page epilogue
+        (find_page_index on the device)."""
+        return self._select(q, layer, kv_head, budget)[1]
 
     def select_tokens(self, q, layer: int, kv_head: int, budget=None) -> list[int]:
+        """engine.py:312-319 (_select_tokens): the ranked top-k token ids."""
+        return self._select(q, layer, kv_head, budget)[0]
+
+    _select_tokens = select_tokens
+
+    def _select(self, q, layer, kv_head, budget):
         t = self._tree(layer, kv_head)
-        k, beam, cap = budget if budget is not None else self.cfg.budget()
+        k, beam, cap = _budget_tuple(budget if budget is not None else self.cfg.budget())
         self.selection_queries += 1
         q = _dev(q, self.device).reshape(1, 1, self.cfg.d)
-        ids, counts, _, _ = self.forest.query([t], q, k, beam, cap, want_pages=False)
+        k_out = int(min(k, self.forest.caps.tok_cap))
+        ids, counts, pages, npages = self.forest.query([t], q, k, beam, cap, k_out=k_out, pages_cap=k_out)
         self.forest.check()
-        return [int(x) for x in ids[0, 0, : int(counts[0, 0])].cpu().tolist()]
+        return ([int(x) for x in ids[0, 0, : int(counts[0, 0])].cpu().tolist()],
+                [int(x) for x in pages[0, : int(npages[0])].cpu().tolist()])
+
+    def token_census(self, layer: int, kv_head: int) -> int:
+        """engine.py:568-575: tokens across the tree's sink, window and indexed pages."""
+        ex = self.forest.export(self._tree(layer, kv_head))
+        return sum(len(toks) for _, toks in ex["pages"].values())
 
     def _tree(self, layer, kv_head):
         if self.fallback or layer < self.cfg.skip_layers or layer >= self.cfg.layers:
@@ -317,8 +368,15 @@ class Engine:
         """engine.py:408-411: newest window page at fill >= s - 1."""
         return (not self.fallback) and self._win_fills[-1] >= self.cfg.page_size - 1
 
-    def decode_step(self, token_id: int, queries, keys, values, *, metrics: bool = True, out=None):
+    def decode_step(self, token_id, queries=None, keys=None, values=None, *, metrics: bool = True, out=None):
         """One decode token through every layer (engine.py:383-514).
+
+        Reference form: decode_step(step) with a DecodeStep (anything with
+        token_id / queries / keys / values) returns (outputs, StepMetrics)
+        with outputs[layer][query head] an AttentionOutput (weights over the
+        attended tokens in entry order, value_out) as the reference does.
+
+        Array form: decode_step(token_id, queries, keys, values).
         queries [L, Hq, d], keys [L, H, d], values [L, H, d'] (device tensors,
         or host tensors: staged through a copy stream, overlapping the previous
         step's compute).  Returns (outputs [L, Hq, d'] fp32, StepMetrics |
@@ -328,6 +386,8 @@ class Engine:
         device tensor receives a copy; a host (pinned) tensor is filled
         asynchronously on the copy stream (synchronize before reading it) and
         is returned."""
+        if queries is None and hasattr(token_id, "token_id"):
+            return self._decode_reference(token_id)
         if not self.prefilled:
             raise ConfigError("decode_step before prefill")
         cfg = self.cfg
@@ -391,6 +451,56 @@ class Engine:
                 rec, hit, mass, rel = self._evaluate(token, q, res)
                 m.recall_at_k, m.page_hit_rate, m.covered_attention_mass, m.approx_rel_error = rec, hit, mass, rel
         return res, m
+
+    def _decode_reference(self, step):
+        """decode_step(DecodeStep) -> (list[list[AttentionOutput]], StepMetrics):
+        the device step, then every query head's output with its weights
+        (icb_attention_weights over the attended set in entry order;
+        icb_dense_weights over all tokens for dense layers)."""
+        from .attention import AttentionOutput
+        if not self.prefilled:
+            raise ConfigError("decode_step before prefill")
+        cfg, dev = self.cfg, self.device
+        L, H, G = cfg.layers, cfg.kv_heads, cfg.query_heads_per_group
+        q = _dev(np.asarray(step.queries, dtype=np.float64), dev).reshape(L, H * G, cfg.d)
+        res, m = self.decode_step(int(step.token_id), q, np.asarray(step.keys, dtype=np.float64),
+                                  np.asarray(step.values, dtype=np.float64))
+        token = int(step.token_id)
+        vals = res.double().cpu().numpy()
+        outs: list[list] = [[None] * (H * G) for _ in range(L)]
+        nd = self.n_dense
+        if nd:
+            ntok = token + 1
+            w = torch.empty((nd * H, G, ntok), dtype=torch.float64, device=dev)
+            qd = q[:nd].reshape(nd * H, G, cfg.d).contiguous()
+            kvd = N.KV_BF16 if self.dense_k.dtype == torch.bfloat16 else N.KV_F32
+            N.check(N.lib().icb_dense_weights(nd * H, G, cfg.d, kvd, _ptr(qd), _ptr(self.dense_k),
+                                              self.dense_k.shape[1], ntok, _ptr(w), _stream()))
+            wn = w.cpu().numpy()
+            for layer in range(nd):
+                for qh in range(H * G):
+                    row = wn[layer * H + qh // G, qh % G]
+                    outs[layer][qh] = AttentionOutput(dict(enumerate(row.tolist())), vals[layer, qh])
+        if not self.fallback:
+            s0, T = cfg.skip_layers, self.T
+            f = self.forest
+            cap = (cfg.sink_pages + cfg.window_pages + self.pages.shape[1]) * cfg.page_size
+            toks = torch.empty((T, cap), dtype=torch.int32, device=dev)
+            w = torch.empty((T, G, cap), dtype=torch.float64, device=dev)
+            cnt = torch.empty((T,), dtype=torch.int32, device=dev)
+            qi = q[s0:].reshape(T, G, cfg.d).contiguous()
+            N.check(N.lib().icb_attention_weights(f.h, _ptr(self.trees_dev), T, G, _ptr(qi), _ptr(self.pages),
+                                                  self.pages.shape[1], _ptr(self.npages), _ptr(toks), _ptr(w), cap,
+                                                  _ptr(cnt), _stream()))
+            toks, w, cnt = toks.cpu().numpy(), w.cpu().numpy(), cnt.cpu().numpy()
+            for t in range(T):
+                layer, h = s0 + t // H, t % H
+                n = min(int(cnt[t]), cap)
+                ids = toks[t, :n].tolist()
+                for g in range(G):
+                    outs[layer][h * G + g] = AttentionOutput(dict(zip(ids, w[t, g, :n].tolist())),
+                                                             vals[layer, h * G + g])
+        return outs, m
 
     def _device_step(self, q, kk, vv, rotate, out):
         """All device work of one step (capturable: the position comes from
@@ -515,11 +625,10 @@ class Engine:
         dense_append(kk[:nd].reshape(nd * H, cfg.d), vv[:nd].reshape(nd * H, cfg.d_prime), self.dense_k,
                      self.dense_v, self._tok_dev)
         qd = q[:nd].reshape(nd * H, G, cfg.d)
-        if cfg.d % 4:
-            qd = torch.nn.functional.pad(qd, (0, (4 - cfg.d % 4) % 4))
+        # logits scaled by 1/sqrt(d) with the unpadded d (attention.py:70)
         res = dense_attention(qd.contiguous(), self.dense_k, self.dense_v, self._tok_dev, splits=splits,
-                              out=self._dense_res[: nd * H])
-        out[:nd] = res[:, :, : cfg.d_prime].reshape(nd, H * G, cfg.d_prime)
+                              out=self._dense_res[: nd * H], dim_v=cfg.d_prime)
+        out[:nd] = res.reshape(nd, H * G, cfg.d_prime)
 
     def _indexed_part(self, q, kk, vv, rotate, out, after_query=None, before_query=None):
         cfg, f = self.cfg, self.forest
@@ -619,13 +728,15 @@ class Engine:
             ref = torch.einsum("hgn,hnv->hgv", w, V)
             order_idx = torch.sort(-scores.masked_fill(~idx_mask, float("-inf")), dim=-1, stable=True).indices
             order_all = torch.sort(-scores, dim=-1, stable=True).indices[..., :k_all]
-            # each head's selected tokens (reuse layers: the anchor's union, engine.py:358-361)
+            # each head's selected tokens (reuse mode: the anchor's group union, engine.py:358-361)
             src = li if cfg.reuse_stride < 2 else (li // cfg.reuse_stride) * cfg.reuse_stride
             sel = torch.zeros((H, G, n + 1), dtype=torch.bool, device=dev)   # column n: padding slots
             ids = self.ids[src * H:(src + 1) * H].long()
             cnt = self.counts[src * H:(src + 1) * H]
             valid = torch.arange(ids.shape[-1], device=dev)[None, None, :] < cnt[..., None]
-            if cfg.reuse_stride >= 2 and li != src:
+            if cfg.reuse_stride >= 2:
+                # under reuse every layer, anchors included, scores the group's
+                # token union (engine.py:346-352, 431-433)
                 ids = ids.reshape(H, 1, -1).expand(H, G, -1)
                 valid = valid.reshape(H, 1, -1).expand(H, G, -1)
             ok = valid & (ids >= 0) & (ids < n)
@@ -647,12 +758,58 @@ class Engine:
             dq = 0
         else:
             self.forest.check()
-            st = self.stats.sum(0).tolist()
+            per_tree = self.stats.cpu().numpy()
+            self._cum_stats = per_tree.copy() if self._cum_stats is None else self._cum_stats + per_tree
+            st = per_tree.sum(0).tolist()
             dq = self._queries_per_step()
         return StepMetrics(step=self.steps_done - 1, token_id=token, recall_at_k=1.0, page_hit_rate=1.0,
                            covered_attention_mass=1.0, approx_rel_error=0.0, pages_selected=int(st[0]),
                            pages_loaded=int(st[2]), tokens_loaded=int(st[1]), bytes_moved=int(st[3]),
                            transactions=int(st[4]), dci_queries=dq)
+
+    # -- reference-shaped views ------------------------------------------------------
+    @property
+    def heads(self) -> dict:
+        """engine.py:206 (Engine.heads): (layer, kv head) -> a read-only view of
+        that tree's device state (tree, table, store snapshot, sink / window
+        pages).  Empty before prefill and in fallback mode."""
+        if not self.prefilled or self.fallback:
+            return {}
+        cfg = self.cfg
+        return {(cfg.skip_layers + t // cfg.kv_heads, t % cfg.kv_heads): _HeadView(self, t) for t in range(self.T)}
+
+    def select_with_reuse(self, layer: int, layer_queries):
+        """engine.py:331-363 for one layer: anchors search every query head of
+        each group and record the group's token union; other layers map the
+        last anchor's tokens through their own page table.  Returns
+        ({kv head: pages}, {kv head: token set})."""
+        if self.cfg.reuse_stride < 2:
+            raise ConfigError("selection reuse is disabled")
+        cfg, dev, f = self.cfg, self.device, self.forest
+        H, G = cfg.kv_heads, cfg.query_heads_per_group
+        trees = [self._tree(layer, h) for h in range(H)]
+        pages_by_head, tokens_by_head = {}, {}
+        if self.is_anchor_layer(layer):
+            k, beam, cap = _budget_tuple(cfg.budget())
+            q = _dev(np.asarray(layer_queries, dtype=np.float64), dev).reshape(H, G, cfg.d)
+            ids, counts, pages, npages = f.query(trees, q, k, beam, cap, k_out=self.k_eff, pages_cap=self.pages_cap)
+            f.check()
+            self.selection_queries += H * G
+            ids, counts, pages, npages = (x.cpu().numpy() for x in (ids, counts, pages, npages))
+            for h in range(H):
+                toks = sorted({int(x) for g in range(G) for x in ids[h, g, : counts[h, g]]})
+                self._anchor_tokens[h] = toks
+                pages_by_head[h] = [int(p) for p in pages[h, : npages[h]]]
+                tokens_by_head[h] = set(toks)
+        else:
+            from .pagestore import TreePageTable, find_page_index
+            for h, t in enumerate(trees):
+                if h not in self._anchor_tokens:
+                    raise ConfigError(f"no anchor selection recorded yet for head {h}")
+                toks = self._anchor_tokens[h]
+                pages_by_head[h] = find_page_index(toks, TreePageTable(f, t))
+                tokens_by_head[h] = set(toks)
+        return pages_by_head, tokens_by_head
 
     def selected(self):
         """Last step's per-tree (ranked ids per head, union pages) on the host."""
@@ -664,3 +821,73 @@ class Engine:
 
     def config_dict(self):
         return asdict(self.cfg)
+
+
+def prefill(workload, cfg: EngineConfig, n_prefill: int | None = None, device=None) -> Engine:
+    """engine.py:578-583: build an engine and prefill it from the stream's head."""
+    if n_prefill is None:
+        n_prefill = workload.n_tokens
+    return Engine(cfg, device=device).prefill(workload, n_prefill)
+
+
+class _HeadView:
+    """One (layer, kv head) tree of the engine, shaped like the reference's
+    _HeadState (engine.py:185-194): `tree` (a DciTree view), `table` (its
+    token -> page table, queried on the device), `store` (a TierStore
+    snapshot: pages with their entries, hot / pinned sets, cumulative
+    TransferStats), `sink` / `window` (Page lists, oldest window first)."""
+
+    def __init__(self, eng: Engine, t: int):
+        self._eng, self._t = eng, t
+
+    @property
+    def tree(self):
+        from .dci import DciTree
+        e = self._eng
+        f = e.forest
+        return DciTree.bound(f, self._t, f.scale(self._t), e.cfg.promotion_ratio, e.cfg.page_size, f.caps.tok_cap)
+
+    @property
+    def table(self):
+        from .pagestore import TreePageTable
+        return TreePageTable(self._eng.forest, self._t)
+
+    @property
+    def store(self):
+        from .pagestore import INDEXED, SINK, WINDOW, TierStore, TransferStats
+        e, t = self._eng, self._t
+        cfg, f = e.cfg, e.forest
+        ex = f.export(t)
+        st = TierStore(cfg.d, cfg.d_prime, cfg.scalar_bytes)
+        role = {N.ROLE_SINK: SINK, N.ROLE_WINDOW: WINDOW, N.ROLE_INDEXED: INDEXED}
+        pids = sorted(ex["pages"])
+        k, v = f.read_pages(t, pids) if pids else (None, None)
+        for i, p in enumerate(pids):
+            r, toks = ex["pages"][p]
+            st._next_page_id = p
+            page = st.allocate_page(cfg.page_size, role[r], resident=r != N.ROLE_INDEXED,
+                                    pinned=r != N.ROLE_INDEXED)
+            for j, tok in enumerate(toks):
+                page.append(tok, k[i, j].astype(np.float64), v[i, j].astype(np.float64))
+        st._next_page_id = ex["info"]["next_page"]
+        if e.steps_done and e.pages is not None:
+            n = int(e.npages[t])
+            st.hot |= {int(p) for p in e.pages[t, :n].cpu().tolist()}
+        cum = e._cum_stats[t] if e._cum_stats is not None else np.zeros(5, np.int64)
+        rot = e.rot_stats[t].cpu().numpy()
+        st.stats = TransferStats(transactions=int(cum[4] + rot[1]), bytes_moved=int(cum[3] + rot[0]),
+                                 pages_backloaded=int(cum[2]), pages_filtered_resident=int(cum[0] - cum[2]),
+                                 pages_offloaded=int(rot[1]))
+        return st
+
+    def _pages(self, ids):
+        st = self.store
+        return [st.page(p) for p in ids]
+
+    @property
+    def sink(self):
+        return self._pages(self._eng.forest.export(self._t)["sink"])
+
+    @property
+    def window(self):
+        return self._pages(self._eng.forest.export(self._t)["win"])

@@ -363,13 +363,18 @@ class DeviceForest:
         return k, v
 
 
-def dense_attention(q, k, v, n_tokens=None, *, splits=0, out=None):
+def dense_attention(q, k, v, n_tokens=None, *, splits=0, out=None, dim_v=None):
     """full_attention (attention.py:55-74) over the first n_tokens rows of
-    contiguous K/V on the device.  q [n,G,d] fp32; k [n,T,d], v [n,T,d'] fp32
-    or bf16 (same dtype, contiguous).  `n_tokens` may be an int32 device
-    tensor holding the decode position p (rows [0, p + 1) are attended)."""
+    contiguous K/V on the device.  q [n,G,d] fp32; k [n,T,ceil4(d)],
+    v [n,T,ceil4(d')] fp32 or bf16 (same dtype, contiguous; rows padded to 4
+    elements as dense_append writes them); d' = dim_v (default v's width).
+    Logits are scaled by 1/sqrt(d), d = q.shape[-1].  `n_tokens` may be an
+    int32 device tensor holding the decode position p (rows [0, p + 1) are
+    attended)."""
     n, G, d = q.shape
-    dv = v.shape[-1]
+    dv = int(dim_v) if dim_v is not None else v.shape[-1]
+    if k.shape[-1] != (d + 3) // 4 * 4 or v.shape[-1] != (dv + 3) // 4 * 4:
+        raise ConfigError("dense K/V rows must be padded to ceil4(d) / ceil4(d')")
     if n_tokens is None:
         n_tokens = k.shape[1]
     if out is None:

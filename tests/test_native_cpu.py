@@ -133,7 +133,8 @@ def test_engine_config_validation_mirrors_reference():
         with pytest.raises(ConfigError):
             EngineConfig(**bad)
     c = EngineConfig(token_budget=256)
-    assert c.budget() == (256, 512, 1024) and c.n_query_heads == c.kv_heads
+    b = c.budget()
+    assert (b.k, b.beam, b.visit_cap) == (256, 512, 1024) and c.n_query_heads == c.kv_heads
     # device-path options: KV offload and the fused rotation step do not combine
     assert not c.kv_offload and not c.fuse_rotation
     EngineConfig(kv_offload=True)
