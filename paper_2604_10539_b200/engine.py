@@ -423,6 +423,8 @@ class Engine:
                 self._mk[:, :, token] = kk
                 self._mv[:, :, token] = vv
             self._device_step(q, kk, vv, rotate, res)
+            if not self.fallback:
+                self._warmed.add(bool(rotate))
         if host_in:
             self._io["in_free"][slot].record(torch.cuda.current_stream(dev))
         if host_out:
@@ -588,7 +590,7 @@ class Engine:
         io["out_done"][slot].record(cs)
         return out_host
 
-    def _graph_step(self, rotate, queries, keys, values):
+    def _graph_buffers(self):
         cfg, dev = self.cfg, self.device
         L, H, G = cfg.layers, cfg.kv_heads, cfg.query_heads_per_group
         if self._gbuf is None:
@@ -596,7 +598,32 @@ class Engine:
                               k=torch.empty((L, H, cfg.d), dtype=torch.float32, device=dev),
                               v=torch.empty((L, H, cfg.d_prime), dtype=torch.float32, device=dev),
                               out=torch.empty((L, H * G, cfg.d_prime), dtype=torch.float32, device=dev))
-        b = self._gbuf
+        return self._gbuf
+
+    def _capture(self, key):
+        b = self._graph_buffers()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._device_step(b["q"], b["k"], b["v"], key, b["out"])
+        self._graphs[key] = g
+
+    def capture_graphs(self) -> None:
+        """Capture both decode-step variants (plain, rotating) as CUDA graphs
+        without running them, so no later step pays a capture.  Each variant
+        must have run once (eagerly or replayed) so every lazily allocated
+        scratch exists."""
+        if not self.cfg.cuda_graph:
+            raise ConfigError("capture_graphs needs EngineConfig.cuda_graph")
+        if self.fallback:
+            raise ConfigError("fallback engines run no graph-captured step")
+        if {False, True} - self._warmed:
+            raise ConfigError("run a plain and a rotating step before capture_graphs()")
+        for key in (False, True):
+            if key not in self._graphs:
+                self._capture(key)
+
+    def _graph_step(self, rotate, queries, keys, values):
+        b = self._graph_buffers()
         b["q"].copy_(torch.as_tensor(queries), non_blocking=True)
         b["k"].copy_(torch.as_tensor(keys), non_blocking=True)
         b["v"].copy_(torch.as_tensor(values), non_blocking=True)
@@ -605,10 +632,8 @@ class Engine:
         if g is None and key in self._warmed:
             # second occurrence of this step variant: every lazily allocated
             # scratch exists (first occurrence ran eagerly) -> capture
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                self._device_step(b["q"], b["k"], b["v"], rotate, b["out"])
-            self._graphs[key] = g
+            self._capture(key)
+            g = self._graphs[key]
         if g is None:
             self._warmed.add(key)
             self._device_step(b["q"], b["k"], b["v"], rotate, b["out"])

@@ -22,14 +22,15 @@ def _worker(rank, world, port, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_2604_10539_b200.dist import aggregate_throughput, max_over_ranks, shard_sequences
-    mine = shard_sequences(64, world, rank)
+    from paper_2604_10539_b200.dist import aggregate_throughput, max_over_ranks, plan_rank
+    plan = plan_rank(64, world, rank, base_seed=3)     # what bench.py's rank decodes (C4: 64 sequences)
+    mine = list(plan.sequences)
     seconds = 1.0 + rank          # rank 1 is the slow one
     tmax = max_over_ranks(seconds)
     gathered = [None] * world
-    dist.all_gather_object(gathered, mine)
+    dist.all_gather_object(gathered, (mine, plan.seed, plan.per_gpu))
     if rank == 0:
-        out.put((tmax, aggregate_throughput(len(mine), world, tmax), gathered))
+        out.put((tmax, aggregate_throughput(plan.per_gpu, world, tmax), gathered))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -47,5 +48,15 @@ def test_two_rank_sequence_parallel():
         assert p.exitcode == 0
     assert tmax == 2.0
     assert thr == 32 * 2 / 2.0
-    assert sorted(gathered[0] + gathered[1]) == list(range(64))
-    assert not set(gathered[0]) & set(gathered[1])
+    (s0, seed0, n0), (s1, seed1, n1) = gathered
+    assert sorted(s0 + s1) == list(range(64)) and not set(s0) & set(s1)
+    assert n0 == n1 == 32 and seed0 != seed1
+
+
+def test_uneven_sequence_split_is_rejected():
+    import pytest
+    from paper_2604_10539_b200.dist import plan_rank
+    with pytest.raises(ValueError):
+        plan_rank(63, 2, 0)
+    with pytest.raises(ValueError):
+        plan_rank(1, 2, 0)
