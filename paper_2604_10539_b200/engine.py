@@ -234,34 +234,18 @@ class Engine:
         # KV offload: the pool holds a step's sink, window and largest selection
         pool = (cfg.query_heads_per_group * min(cfg.token_budget, self.max_tokens) + cfg.sink_pages
                 + cfg.window_pages + 2)
-        self.forest = DeviceForest(T, cfg.d, cfg.d_prime, tok_cap=self.max_tokens,
-                                   promotion_ratio=cfg.promotion_ratio, page_size=s,
-                                   kv_dtype=cfg.kv_dtype, device=dev, kv_host=cfg.kv_offload,
-                                   pool_pages=pool if cfg.kv_offload else 0,
-                                   caps=ForestCaps.for_tokens(self.max_tokens, cfg.promotion_ratio, s,
-                                                              extra_pages=cfg.sink_pages + 4 * cfg.window_pages
-                                                              + self.max_tokens // s))
-        f = self.forest
-        trees = list(range(T))
-        f.seed(trees, [(cfg.seed, cfg.skip_layers + t // H, t % H) for t in trees])
         self.trees_dev = torch.arange(T, dtype=torch.int32, device=dev)
-        ki = keys[:, cfg.skip_layers:].permute(1, 2, 0, 3).reshape(T, n_prefill, cfg.d)
-        vi = values[:, cfg.skip_layers:].permute(1, 2, 0, 3).reshape(T, n_prefill, cfg.d_prime)
-        tok = torch.arange(n_prefill, dtype=torch.int32, device=dev)
-        # pages: sink ids 0.., window next, then indexed (engine.py:263-281)
-        f.alloc_resident(self.trees_dev, N.ROLE_SINK, cfg.sink_pages,
-                         tok[:sink_end].expand(T, -1), ki[:, :sink_end], vi[:, :sink_end])
-        wn = n_prefill - win_start
-        f.alloc_resident(self.trees_dev, N.ROLE_WINDOW, cfg.window_pages,
-                         tok[win_start:].expand(T, -1), ki[:, win_start:], vi[:, win_start:])
-        self._win_fills = [min(s, max(0, wn - i * s)) for i in range(cfg.window_pages)]
+        self._win_fills = [min(s, max(0, (n_prefill - win_start) - i * s)) for i in range(cfg.window_pages)]
         self._win_start = [win_start + i * s for i in range(cfg.window_pages)]
-        chunk = max(1, min(T, (2 << 30) // max(1, (win_start - sink_end) * 1200)))
-        for c0 in range(0, T, chunk):
-            c1 = min(T, c0 + chunk)
-            f.build(self.trees_dev[c0:c1], tok[sink_end:win_start].expand(c1 - c0, -1),
-                    ki[c0:c1, sink_end:win_start], vi[c0:c1, sink_end:win_start])
-        f.check()
+        try:
+            self._build_forest(keys, values, n_prefill, sink_end, win_start, pool, tight=True)
+        except ConfigError as e:
+            if "page capacity" not in str(e):
+                raise
+            # the trees outgrew the tight page estimate: rebuild at the worst case
+            self.forest.close()
+            self._build_forest(keys, values, n_prefill, sink_end, win_start, pool, tight=False)
+        f = self.forest
         k, beam, cap = _budget_tuple(cfg.budget())
         self.k_eff = int(min(k, self.max_tokens))
         self.beam, self.visit_cap = int(min(beam, 2**62)), int(min(cap, 2**62))
@@ -272,6 +256,32 @@ class Engine:
         self._alloc_step_buffers()
         self.prefilled = True
         return self
+
+    def _build_forest(self, keys, values, n_prefill, sink_end, win_start, pool, tight):
+        cfg, dev, T, H, s = self.cfg, self.device, self.T, self.cfg.kv_heads, self.cfg.page_size
+        caps = ForestCaps.for_stream(win_start - sink_end, self.max_tokens - n_prefill, cfg.promotion_ratio, s,
+                                     cfg.sink_pages + cfg.window_pages, tight=tight)
+        caps.tok_cap = self.max_tokens
+        self.forest = f = DeviceForest(T, cfg.d, cfg.d_prime, tok_cap=self.max_tokens,
+                                       promotion_ratio=cfg.promotion_ratio, page_size=s, kv_dtype=cfg.kv_dtype,
+                                       device=dev, kv_host=cfg.kv_offload, pool_pages=pool if cfg.kv_offload else 0,
+                                       caps=caps)
+        trees = list(range(T))
+        f.seed(trees, [(cfg.seed, cfg.skip_layers + t // H, t % H) for t in trees])
+        ki = keys[:, cfg.skip_layers:].permute(1, 2, 0, 3).reshape(T, n_prefill, cfg.d)
+        vi = values[:, cfg.skip_layers:].permute(1, 2, 0, 3).reshape(T, n_prefill, cfg.d_prime)
+        tok = torch.arange(n_prefill, dtype=torch.int32, device=dev)
+        # pages: sink ids 0.., window next, then indexed (engine.py:263-281)
+        f.alloc_resident(self.trees_dev, N.ROLE_SINK, cfg.sink_pages,
+                         tok[:sink_end].expand(T, -1), ki[:, :sink_end], vi[:, :sink_end])
+        f.alloc_resident(self.trees_dev, N.ROLE_WINDOW, cfg.window_pages,
+                         tok[win_start:].expand(T, -1), ki[:, win_start:], vi[:, win_start:])
+        chunk = max(1, min(T, (2 << 30) // max(1, (win_start - sink_end) * 1200)))
+        for c0 in range(0, T, chunk):
+            c1 = min(T, c0 + chunk)
+            f.build(self.trees_dev[c0:c1], tok[sink_end:win_start].expand(c1 - c0, -1),
+                    ki[c0:c1, sink_end:win_start], vi[c0:c1, sink_end:win_start])
+        f.check()
 
     def _check_workload(self, workload) -> None:
         """engine.py:216-224."""

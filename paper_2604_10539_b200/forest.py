@@ -57,6 +57,31 @@ class ForestCaps:
     dirs_cap: int = 64
 
     @staticmethod
+    def for_stream(n_build: int, n_decode: int, r: float, page_size: int, resident_pages: int,
+                   tight: bool = True) -> "ForestCaps":
+        """Capacities for trees built over n_build points and then decoded for
+        n_decode tokens.  Page K/V dominate HBM (8 KB per page at d = 128,
+        bf16), so the page capacity is sized close to use:
+        - build: every leaf is owned by a point of level >= 2 (Binomial(n, r):
+          bounded at 8 standard deviations), and a leaf of m members takes
+          ceil(m / s) pages; `tight` budgets half a page of fill slack per s
+          points (C2: 4.2k pages used of a 4.8k estimate), the fallback
+          (tight=False) the worst case of for_tokens.  A build that outgrows the
+          tight estimate raises ConfigError and the Engine rebuilds with the
+          worst case.
+        - decode: each rotation inserts s points (at most one new page each)
+          and opens one window page: at most s + 1 pages per s - 1 tokens."""
+        tok_cap = n_build + n_decode
+        base = ForestCaps.for_tokens(tok_cap, r, page_size, extra_pages=resident_pages + n_decode // page_size)
+        if not tight:
+            return base
+        leaves = r * n_build + 8.0 * (n_build * r * (1.0 - r)) ** 0.5 + 16
+        build_pages = int(leaves + n_build / (2.0 * page_size)) + 1
+        decode_pages = (page_size + 1) * (n_decode // max(1, page_size - 1) + 2)
+        base.page_cap = min(base.page_cap, resident_pages + build_pages + decode_pages + 8)
+        return base
+
+    @staticmethod
     def for_tokens(tok_cap: int, r: float, page_size: int, extra_pages: int = 64) -> "ForestCaps":
         frac = r / (1.0 - r)
         node_cap = int(tok_cap * frac * 1.6) + 256
