@@ -88,8 +88,6 @@ class EngineConfig:
         if self.kv_offload and self.fuse_rotation:
             raise ConfigError("kv_offload does not combine with fuse_rotation (the fused step would read host "
                               "rows it wrote in the same launch)")
-        if self.compare_baseline:
-            raise ConfigError("compare_baseline (TokenOrderBaseline, engine.py:148-182) is outside the device path")
 
     @property
     def n_query_heads(self) -> int:
@@ -158,6 +156,7 @@ class Engine:
         self._gbuf = None
         self._io = None
         self._cum_stats = None     # [T, 5] host: residency counters summed over metric steps
+        self._baseline_hit = None  # TokenOrderBaseline hit rate of the last evaluated step
         self._anchor_tokens: dict[int, list[int]] = {}
 
     # -- prefill ---------------------------------------------------------------
@@ -462,6 +461,7 @@ class Engine:
             if cfg.evaluate and not self.fallback and not graph:
                 rec, hit, mass, rel = self._evaluate(token, q, res)
                 m.recall_at_k, m.page_hit_rate, m.covered_attention_mass, m.approx_rel_error = rec, hit, mass, rel
+                m.baseline_hit_rate = self._baseline_hit
         return res, m
 
     def _decode_reference(self, step):
@@ -752,7 +752,7 @@ class Engine:
         idx_mask = self._indexed_mask[:n]
         k_eff = min(cfg.token_budget, len(self.indexed_tokens))
         k_all = min(cfg.token_budget, n)
-        rec, hit, mass, rel = [], [], [], []
+        rec, hit, mass, rel, base = [], [], [], [], []
         for layer in range(cfg.skip_layers, cfg.layers):
             li = layer - cfg.skip_layers
             K = self._mk[layer, :, :n].double()
@@ -783,8 +783,42 @@ class Engine:
             mass.append((w * a).sum(-1))
             o = out[layer].double().reshape(H, G, -1)
             rel.append(torch.linalg.norm(o - ref, dim=-1) / torch.linalg.norm(ref, dim=-1).clamp_min(1e-300))
+            if cfg.compare_baseline:
+                base.append(self._token_order_hits(layer, li, ql, order_all, k_all, n))
         f = lambda xs: float(torch.cat([x.reshape(-1) for x in xs]).mean())   # noqa: E731
+        self._baseline_hit = f(base) if base else None
         return f(rec), f(hit), f(mass), f(rel)
+
+    def _token_order_hits(self, layer, li, ql, order_all, k_all, n):
+        """TokenOrderBaseline (engine.py:148-182) for one layer's heads, on the
+        device in fp64: indexed tokens in arrival order (prefill middle, then
+        each rotated window page) fill pages of s; a page's score for q is
+        sum_i max(q_i lo_i, q_i hi_i) over its coordinate envelope; the
+        top-n pages (n = the group's selected page count; ties to the older
+        page) plus sink and window tokens form the baseline's attended set;
+        returns the exact top-k's hit rate in it per head."""
+        cfg, dev = self.cfg, self.device
+        H, G, s = cfg.kv_heads, cfg.query_heads_per_group, cfg.page_size
+        order = torch.as_tensor(self.indexed_tokens, dtype=torch.long, device=dev)
+        P = (order.numel() + s - 1) // s
+        K = self._mk[layer][:, order].double()                                    # [H, m, d]
+        pad = P * s - order.numel()
+        lo = torch.cat([K, K[:, -1:].expand(H, pad, -1)], 1).reshape(H, P, s, -1).amin(2)
+        hi = torch.cat([K, K[:, -1:].expand(H, pad, -1)], 1).reshape(H, P, s, -1).amax(2)
+        sc = torch.maximum(lo[:, None] * ql[:, :, None], hi[:, None] * ql[:, :, None]).sum(-1)   # [H, G, P]
+        rank = torch.sort(-sc, dim=-1, stable=True).indices
+        npg = self.npages[li * H:(li + 1) * H].long()                              # group union sizes
+        keep = torch.arange(P, device=dev)[None, None, :] < npg[:, None, None]
+        chosen = torch.zeros((H, G, P), dtype=torch.bool, device=dev)
+        chosen.scatter_(-1, rank, keep.expand(H, G, P))
+        page_of = torch.arange(order.numel(), device=dev) // s
+        att = torch.zeros((H, G, n), dtype=torch.bool, device=dev)
+        att[:, :, order] = chosen[:, :, page_of]
+        fixed = list(self.sink_tokens)
+        for st0, fl in zip(self._win_start, self._win_fills):
+            fixed += range(st0, st0 + fl)
+        att[:, :, torch.as_tensor(fixed, dtype=torch.long, device=dev)] = True
+        return att.gather(-1, order_all).sum(-1).double() / k_all
 
     def _metrics(self, token) -> StepMetrics:
         cfg = self.cfg

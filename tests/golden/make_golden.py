@@ -117,6 +117,10 @@ def engine_cases():
         ("eval_reuse", dict(n_tokens=1024 + 40, d=32, d_prime=16, clusters=8, layers=8, kv_heads=2,
                             query_heads_per_group=2, seed=11),
          dict(token_budget=24, skip_layers=2, reuse_stride=3, evaluate=True), 1024, 20),
+        # acceptance 06 (tests/test_acceptance.py:135-153): TokenOrderBaseline hit rates
+        ("baseline", dict(n_tokens=10_100, d=64, d_prime=32, clusters=32, layers=3, kv_heads=1,
+                          query_heads_per_group=1, seed=106),
+         dict(token_budget=64, evaluate=True, compare_baseline=True), 10_000, 100),
     ]
 
 

@@ -171,7 +171,7 @@ def test_fused_rotation_step_matches_separate_launches(cuda_ok):
         assert e1["info"] == e2["info"], tr
 
 
-@pytest.mark.parametrize("name", ["eval", "eval_reuse"])
+@pytest.mark.parametrize("name", ["eval", "eval_reuse", "baseline"])
 def test_engine_evaluation_metrics(cuda_ok, name):
     """evaluate=True (engine.py:536-566) on the device: recall@k, page hit rate,
     covered attention mass and relative error against the reference's golden
@@ -187,6 +187,7 @@ def test_engine_evaluation_metrics(cuda_ok, name):
     eng = Engine(EngineConfig(**shape, **ck, kv_dtype="fp32", max_tokens=n0 + meta["steps"] + 1)).prefill(
         keys, values, n0)
     k = ck["token_budget"]
+    sem, base = [], []
     for t in range(meta["steps"]):
         tok = n0 + t
         out, m = eng.decode_step(tok, queries[tok], keys[tok], values[tok])
@@ -198,9 +199,19 @@ def test_engine_evaluation_metrics(cuda_ok, name):
         assert abs(m.page_hit_rate - row["page_hit_rate"]) <= 1.0 / k + 1e-9, (t, m.page_hit_rate)
         assert abs(m.covered_attention_mass - row["covered_attention_mass"]) < 1e-6, t
         assert abs(m.approx_rel_error - row["approx_rel_error"]) < 1e-4 * max(1.0, row["approx_rel_error"]), t
+        if row.get("baseline_hit_rate") is not None:
+            # TokenOrderBaseline (engine.py:148-182) on the device: same pages, same hits
+            assert abs(m.baseline_hit_rate - row["baseline_hit_rate"]) <= 1e-9, (t, m.baseline_hit_rate)
+            sem.append(m.page_hit_rate)
+            base.append(m.baseline_hit_rate)
+        else:
+            assert m.baseline_hit_rate is None
         ref = z["outputs"][t]
         o = out.cpu().numpy()
         assert (np.linalg.norm(o - ref, axis=-1) / np.linalg.norm(ref, axis=-1)).max() < 1e-3
+    if sem:
+        # acceptance 06 (tests/test_acceptance.py:135-153): semantic paging hits at least as often
+        assert np.mean(sem) >= np.mean(base)
 
 
 @pytest.mark.parametrize("kv,reuse", [("bf16", 0), ("fp32", 0), ("bf16", 3)])
