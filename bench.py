@@ -178,8 +178,11 @@ def run_ours(args, rank, world):
     # S sequences of equal length: per (layer, kv head) trees are independent and
     # rotate in lockstep, so the batch is the model with kv_heads x S
     cS = dict(C2, kv_heads=C2["kv_heads"] * S)
+    # several sequences per GPU: the prompt stream in bf16 (its K/V plus the forest
+    # must fit HBM together; the engine converts it per chunk of layers)
     stream = clustered_stream(n0, total_steps, cS["layers"], cS["kv_heads"], cS["query_heads_per_group"],
-                              cS["d"], cS["d_prime"], seed=plan.seed, device=dev)
+                              cS["d"], cS["d_prime"], seed=plan.seed, device=dev,
+                              dtype=torch.bfloat16 if S > 1 else torch.float32)
     cfg = EngineConfig(**cS, seed=plan.seed, kv_dtype=args.kv, max_tokens=n0 + total_steps + 1,
                        layer_serial=args.layer_serial, cuda_graph=False, reuse_stride=args.reuse_stride,
                        fuse_rotation=args.fuse_rotation, kv_offload=args.kv_offload)
@@ -324,7 +327,8 @@ def run_ours(args, rank, world):
         "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "fp32 search keys / bf16 KV / fp32 accum" if args.kv == "bf16" else "fp32",
-        "data": "synthetic clustered q/k/v (reference workload distribution), random init, drawn on device",
+        "data": "synthetic clustered q/k/v (reference workload distribution), random init, drawn on device" +
+                (" (prompt K/V bf16-representable: the multi-sequence stream is held in bf16)" if S > 1 else ""),
         "config": {"workload": workload_label(args), "context": n0, "budget": 256, "beam": 512, "visit_cap": 1024,
                    "page_size": 16, "layers": 32, "kv_heads": 8, "q_heads": 32, "kv_dtype": args.kv,
                    "sequences_per_gpu": S, "sequences": list(plan.sequences), "global_batch": S * world,
@@ -400,9 +404,9 @@ def run_e2e(eng, stream, n0, start, K2, dev, world, segments=1, seqs=1):
 
     from paper_2604_10539_b200.dist import max_over_ranks
     n = K2 * segments + E2E_WARM
-    qh = stream.queries[start:start + n].cpu().pin_memory()
-    kh = stream.keys[n0 + start:n0 + start + n].cpu().pin_memory()
-    vh = stream.values[n0 + start:n0 + start + n].cpu().pin_memory()
+    qh = stream.queries[start:start + n].float().cpu().pin_memory()
+    kh = stream.keys[n0 + start:n0 + start + n].float().cpu().pin_memory()
+    vh = stream.values[n0 + start:n0 + start + n].float().cpu().pin_memory()
     outh = torch.empty((n,) + (qh.shape[1], qh.shape[2], stream.values.shape[-1]), dtype=torch.float32).pin_memory()
     if eng.steps_done != start:
         return None

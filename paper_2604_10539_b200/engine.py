@@ -128,6 +128,14 @@ def _dev(x, device, dtype=torch.float32):
     return torch.as_tensor(x, dtype=dtype, device=device)
 
 
+def _on_device(x, device):
+    dev = torch.device(device)
+    if isinstance(x, torch.Tensor) and x.is_floating_point() and x.device.type == dev.type and \
+            (dev.index is None or x.device.index == dev.index):
+        return x
+    return torch.as_tensor(x, dtype=torch.float32, device=device)
+
+
 def _budget_tuple(b):
     """A SearchBudget (dci.py:50-74) or a (k, beam, visit_cap) tuple."""
     if hasattr(b, "visit_cap"):
@@ -183,8 +191,10 @@ class Engine:
             raise ConfigError("prefill needs at least one token")
         cfg = self.cfg
         dev = self.device
-        keys = _dev(keys[:n_prefill], dev)
-        values = _dev(values[:n_prefill], dev)
+        # device tensors keep their dtype (an fp32 / bf16 stream is converted per
+        # chunk of layers, never materialised whole in fp32); numpy / host -> fp32
+        keys = _on_device(keys[:n_prefill], dev)
+        values = _on_device(values[:n_prefill], dev)
         if tuple(keys.shape[1:]) != (cfg.layers, cfg.kv_heads, cfg.d) or \
                 tuple(values.shape[1:]) != (cfg.layers, cfg.kv_heads, cfg.d_prime):
             raise ConfigError("workload dims do not match the engine config")
@@ -205,8 +215,8 @@ class Engine:
             self._mk = torch.zeros((cfg.layers, cfg.kv_heads, self.max_tokens, cfg.d), dtype=torch.float32, device=dev)
             self._mv = torch.zeros((cfg.layers, cfg.kv_heads, self.max_tokens, cfg.d_prime), dtype=torch.float32,
                                    device=dev)
-            self._mk[:, :, :n_prefill] = keys.permute(1, 2, 0, 3)
-            self._mv[:, :, :n_prefill] = values.permute(1, 2, 0, 3)
+            self._mk[:, :, :n_prefill] = keys.permute(1, 2, 0, 3).float()
+            self._mv[:, :, :n_prefill] = values.permute(1, 2, 0, 3).float()
             self._indexed_mask = torch.zeros(self.max_tokens, dtype=torch.bool, device=dev)
         self._dense_res = torch.empty((max(nd, 1), cfg.query_heads_per_group, cfg.d_prime), dtype=torch.float32,
                                       device=dev)   # dense attention output (nd planes)
@@ -267,19 +277,26 @@ class Engine:
                                        caps=caps)
         trees = list(range(T))
         f.seed(trees, [(cfg.seed, cfg.skip_layers + t // H, t % H) for t in trees])
-        ki = keys[:, cfg.skip_layers:].permute(1, 2, 0, 3).reshape(T, n_prefill, cfg.d)
-        vi = values[:, cfg.skip_layers:].permute(1, 2, 0, 3).reshape(T, n_prefill, cfg.d_prime)
         tok = torch.arange(n_prefill, dtype=torch.int32, device=dev)
-        # pages: sink ids 0.., window next, then indexed (engine.py:263-281)
-        f.alloc_resident(self.trees_dev, N.ROLE_SINK, cfg.sink_pages,
-                         tok[:sink_end].expand(T, -1), ki[:, :sink_end], vi[:, :sink_end])
-        f.alloc_resident(self.trees_dev, N.ROLE_WINDOW, cfg.window_pages,
-                         tok[win_start:].expand(T, -1), ki[:, win_start:], vi[:, win_start:])
-        chunk = max(1, min(T, (2 << 30) // max(1, (win_start - sink_end) * 1200)))
-        for c0 in range(0, T, chunk):
-            c1 = min(T, c0 + chunk)
-            f.build(self.trees_dev[c0:c1], tok[sink_end:win_start].expand(c1 - c0, -1),
-                    ki[c0:c1, sink_end:win_start], vi[c0:c1, sink_end:win_start])
+        Li = T // H
+        # whole layers per chunk, ~2 GB of fp32 prefill keys + values at a time
+        per_layer = H * n_prefill * (cfg.d + cfg.d_prime) * 4
+        lchunk = max(1, min(Li, (2 << 30) // max(1, per_layer)))
+        for l0 in range(0, Li, lchunk):
+            l1 = min(Li, l0 + lchunk)
+            c0, c1 = l0 * H, l1 * H
+            trs = self.trees_dev[c0:c1]
+            sl = slice(cfg.skip_layers + l0, cfg.skip_layers + l1)
+            ki = keys[:, sl].permute(1, 2, 0, 3).reshape(c1 - c0, n_prefill, cfg.d)
+            vi = values[:, sl].permute(1, 2, 0, 3).reshape(c1 - c0, n_prefill, cfg.d_prime)
+            # pages: sink ids 0.., window next, then indexed (engine.py:263-281)
+            f.alloc_resident(trs, N.ROLE_SINK, cfg.sink_pages, tok[:sink_end].expand(c1 - c0, -1),
+                             ki[:, :sink_end], vi[:, :sink_end])
+            f.alloc_resident(trs, N.ROLE_WINDOW, cfg.window_pages, tok[win_start:].expand(c1 - c0, -1),
+                             ki[:, win_start:], vi[:, win_start:])
+            f.build(trs, tok[sink_end:win_start].expand(c1 - c0, -1), ki[:, sink_end:win_start],
+                    vi[:, sink_end:win_start])
+            del ki, vi
         f.check()
 
     def _check_workload(self, workload) -> None:

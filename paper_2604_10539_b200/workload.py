@@ -169,7 +169,10 @@ def _unit(x):
 
 def clustered_stream(n_prefill: int, steps: int, layers: int, kv_heads: int, G: int, d: int, d_prime: int, *,
                      clusters: int = 32, spread: float = 0.1, jitter: float = 0.1, seed: int = 0,
-                     device="cuda") -> DeviceStream:
+                     device="cuda", dtype=torch.float32) -> DeviceStream:
+    """Keys / values [n, L, H, d] in `dtype` (bf16 halves a multi-sequence
+    prompt's footprint: its values are then bf16-representable fp32 inputs),
+    queries [steps, L, H*G, d] fp32.  Generated layer by layer."""
     g = torch.Generator(device=device)
     g.manual_seed(seed)
     n = n_prefill + steps
@@ -183,10 +186,12 @@ def clustered_stream(n_prefill: int, steps: int, layers: int, kv_heads: int, G: 
     hidx = torch.arange(H, device=device)
     base = centers[hidx[None, :], cluster_of[:, None]]                       # [n, H, d]
     base = base + torch.randn(n, H, d, **kw) * sigma
-    keys = torch.empty((n, L, H, d), dtype=torch.float32, device=device)
+    keys = torch.empty((n, L, H, d), dtype=dtype, device=device)
+    values = torch.empty((n, L, H, d_prime), dtype=dtype, device=device)
     for layer in range(L):
         keys[:, layer] = base + torch.randn(n, H, d, **kw) * jit
-    values = torch.randn(n, L, H, d_prime, **kw) / math.sqrt(d_prime)
+    for layer in range(L):
+        values[:, layer] = torch.randn(n, H, d_prime, **kw) / math.sqrt(d_prime)
     qbase = centers[hidx[None, :], qcluster[:, None]]                        # [steps, H, d]
     qbase = qbase[:, :, None, :].expand(steps, H, G, d) + torch.randn(steps, H, G, d, **kw) * sigma
     queries = torch.empty((steps, L, H * G, d), dtype=torch.float32, device=device)
