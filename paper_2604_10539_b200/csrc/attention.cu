@@ -288,6 +288,15 @@ int icb_dense_attention_impl(int32_t n, int32_t G, int32_t dim, int32_t dim_v, i
                              int32_t splits, cudaStream_t st) {
   if (n <= 0) return ICB_OK;
   if (!valid_g(G)) { icb_set_error(ICB_E_CONFIG, "attention supports 1 <= G <= 8"); return ICB_E_CONFIG; }
+  if (icb_dense_flash_ok(G, dim, dim_v, kv_dtype)) {
+    // TMA + tensor-core flash-decoding kernel (dense.cu): two CTAs per SM, one wave
+    if (splits <= 0) splits = std::max(1, std::min((n_tokens + 1023) / 1024, (2 * 148) / n));
+    float* part;
+    unsigned* counter;
+    int rc = ensure_attn_scratch(nullptr, (size_t)n * splits * G * (2 + 128), n, &part, &counter);
+    if (rc) return rc;
+    return icb_dense_flash_impl(n, G, q, k, v, ld, n_tokens, token_dev, out, splits, part, counter, st);
+  }
   if (splits <= 0) splits = std::max(1, std::min((n_tokens + 255) / 256, (2 * 148) / n));   // one wave
   AttnArgs A{};
   A.n = n; A.G = G; A.dim = dim; A.dim_v = dim_v; A.splits = splits; A.q = q; A.k = k; A.v = v; A.ld = ld;

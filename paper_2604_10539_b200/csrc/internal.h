@@ -125,3 +125,7 @@ int icb_dense_append_impl(int32_t n, int32_t dim, int32_t dim_v, int32_t kv_dtyp
 int icb_dense_attention_impl(int32_t n, int32_t G, int32_t dim, int32_t dim_v, int32_t kv_dtype,
                              const float* q, const void* k, const void* v, int64_t ld, int32_t n_tokens,
                              const int32_t* token_dev, float* out, int32_t splits, cudaStream_t st);
+bool icb_dense_flash_ok(int G, int dim, int dim_v, int kv_dtype);
+int icb_dense_flash_impl(int32_t n, int32_t G, const float* q, const void* k, const void* v, int64_t ld,
+                         int32_t n_tokens, const int32_t* token_dev, float* out, int32_t splits, float* part,
+                         unsigned* counter, cudaStream_t st);

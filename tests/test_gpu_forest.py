@@ -218,3 +218,26 @@ def test_dense_attention(cuda_ok, kv, tol):
             _, ref = full_attention(q[b, g].cpu().double().numpy(), k[b, :4321].cpu().double().numpy(),
                                     v[b, :4321].cpu().double().numpy())
             assert np.linalg.norm(out[b, g] - ref) / np.linalg.norm(ref) < tol
+
+
+@pytest.mark.parametrize("G,ntok", [(4, 1), (4, 63), (4, 64), (4, 33000), (1, 777), (3, 5000), (8, 4097)])
+def test_dense_flash_attention(cuda_ok, G, ntok):
+    """The TMA + tensor-core dense kernel (bf16, d = d' = 128; csrc/dense.cu)
+    against fp64 over the bf16-stored K/V, and the device-position variant."""
+    import torch
+    from paper_2604_10539_b200 import dense_attention
+    rng = np.random.default_rng(ntok + G)
+    n, T, d = 3, 33024, 128
+    k = torch.tensor(rng.normal(size=(n, T, d)) / np.sqrt(d), dtype=torch.float32, device="cuda").bfloat16()
+    v = torch.tensor(rng.normal(size=(n, T, d)) / np.sqrt(d), dtype=torch.float32, device="cuda").bfloat16()
+    q = torch.tensor(rng.normal(size=(n, G, d)) * np.sqrt(d) * 0.3, dtype=torch.float32, device="cuda")
+    out = dense_attention(q, k, v, ntok).cpu().numpy()
+    pos = torch.tensor([ntok - 1], dtype=torch.int32, device="cuda")
+    out_dev = dense_attention(q, k, v, pos).cpu().numpy()
+    kd, vd = k.double().cpu().numpy(), v.double().cpu().numpy()
+    for b in range(n):
+        for g in range(G):
+            _, ref = full_attention(q[b, g].cpu().double().numpy(), kd[b, :ntok], vd[b, :ntok])
+            err = np.linalg.norm(out[b, g] - ref) / np.linalg.norm(ref)
+            assert err < 2e-3, (b, g, err)
+            assert np.linalg.norm(out_dev[b, g] - ref) / np.linalg.norm(ref) < 2e-3
