@@ -735,10 +735,42 @@ __device__ const double* pdci_dirs(const ForestView& F, int t, int node, double*
   return slot >= 0 ? F.dirs + ((size_t)t * F.dirs_cap + slot) * ICB_NPROJ * D1 : tmp;
 }
 
+// Block bitonic sort of n (a power of two) entries ascending by (k64, k32),
+// the payload `pl` travelling along; shared-memory arrays.
+template <int NT>
+__device__ void bitonic3(unsigned long long* k64, unsigned* k32, int* pl, int n) {
+  for (int size = 2; size <= n; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < (n >> 1); i += NT) {
+        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        const unsigned long long a = k64[lo], b = k64[hi];
+        const unsigned a2 = k32[lo], b2 = k32[hi];
+        const bool gt = a > b || (a == b && a2 > b2);
+        if (gt == ((lo & size) == 0)) {
+          k64[lo] = b; k64[hi] = a;
+          k32[lo] = b2; k32[hi] = a2;
+          const int t = pl[lo]; pl[lo] = pl[hi]; pl[hi] = t;
+        }
+      }
+      __syncthreads();
+    }
+}
+
+__device__ __forceinline__ unsigned long long orderable_f64(double x) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
 // Visit list of a large node (cap entries, ascending emission order) into
 // SS.vis; returns the count.  Emission key of a member = lexicographic max over
 // its 8 ladder entries of (gap, j, chain position) -- the pop order of the
 // reference's heap merge (see oracle/dci.py:visit_order for the equivalence).
+// The chain position of member i on ladder j is its rank in the node sorted by
+// (projection_j, id), and the ladder's start is the number of projections
+// below the query's.  Up to kPdciSort members: one bitonic sort per ladder and
+// one of the emission keys, in the idle row ring (S.sortbuf, 64 KB); larger
+// nodes rank by counting (O(m^2)).
+constexpr int kPdciSort = 4096;
 template <int NT>
 __device__ int pdci_visit(SearchSmem& S, const ForestView& F, const SearchScratch& SS, int t, int node,
                           int g, long long cap, double* dirs_tmp) {
@@ -764,6 +796,59 @@ __device__ int pdci_visit(SearchSmem& S, const ForestView& F, const SearchScratc
     SS.proj[(size_t)i * ICB_NPROJ + j] = acc;
   }
   __syncthreads();
+  const int cnt = (int)min((long long)m, cap);
+  if (m <= kPdciSort) {
+    int n2 = 1;
+    while (n2 < m) n2 <<= 1;
+    unsigned long long* k64 = S.sortbuf;                            // [n2]
+    unsigned* k32 = reinterpret_cast<unsigned*>(k64 + n2);          // [n2]
+    int* pl = reinterpret_cast<int*>(k32 + n2);                     // [n2]
+    for (int i = threadIdx.x; i < m; i += NT) { SS.ekey[2 * (size_t)i] = 0; SS.ekey[2 * (size_t)i + 1] = 0; }
+    for (int j = 0; j < ICB_NPROJ; ++j) {
+      // ladder j: members by (projection, id)
+      for (int i = threadIdx.x; i < n2; i += NT) {
+        const bool on = i < m;
+        k64[i] = on ? orderable_f64(SS.proj[(size_t)i * ICB_NPROJ + j]) : ~0ull;
+        k32[i] = on ? (unsigned)mem[i] : 0xffffffffu;
+        pl[i] = on ? i : -1;
+      }
+      __syncthreads();
+      bitonic3<NT>(k64, k32, pl, n2);
+      // start = #projections strictly below the query's (binary search)
+      const double qp = S.dirs_tmp[j];
+      const unsigned long long qk = orderable_f64(qp);
+      int lo = 0, hi = m;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (k64[mid] < qk) lo = mid + 1;
+        else hi = mid;
+      }
+      const int start = lo;
+      for (int pos = threadIdx.x; pos < m; pos += NT) {
+        const int i = pl[pos];
+        const double gap = fabs(__dsub_rn(SS.proj[(size_t)i * ICB_NPROJ + j], qp));
+        const unsigned long long h = (unsigned long long)__double_as_longlong(gap);
+        const unsigned long long sec = pos < start ? (unsigned long long)((1 << 23) - 1 - pos)
+                                                   : (unsigned long long)((1 << 23) + pos);
+        const unsigned long long l = ((unsigned long long)j << 24) | sec;
+        const unsigned long long bh = SS.ekey[2 * (size_t)i], bl = SS.ekey[2 * (size_t)i + 1];
+        if (h > bh || (h == bh && l > bl)) { SS.ekey[2 * (size_t)i] = h; SS.ekey[2 * (size_t)i + 1] = l; }
+      }
+      __syncthreads();
+    }
+    // the cnt smallest emission keys, ascending
+    for (int i = threadIdx.x; i < n2; i += NT) {
+      const bool on = i < m;
+      k64[i] = on ? SS.ekey[2 * (size_t)i] : ~0ull;
+      k32[i] = on ? (unsigned)SS.ekey[2 * (size_t)i + 1] : 0xffffffffu;
+      pl[i] = on ? mem[i] : -1;
+    }
+    __syncthreads();
+    bitonic3<NT>(k64, k32, pl, n2);
+    for (int r = threadIdx.x; r < cnt; r += NT) SS.vis[r] = pl[r];
+    __syncthreads();
+    return cnt;
+  }
   // emission keys
   for (int i = threadIdx.x; i < m; i += NT) {
     unsigned long long best_hi = 0, best_lo = 0;
@@ -789,7 +874,6 @@ __device__ int pdci_visit(SearchSmem& S, const ForestView& F, const SearchScratc
     SS.ekey[2 * (size_t)i + 1] = best_lo;
   }
   __syncthreads();
-  int cnt = (int)min((long long)m, cap);
   for (int i = threadIdx.x; i < m; i += NT) {
     unsigned long long hi = SS.ekey[2 * (size_t)i], lo = SS.ekey[2 * (size_t)i + 1];
     int rank = 0;

@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+ICB_PROF=1 timeout 600 python tools/time_rotation.py 32768 > gpurun_out/rot_c2.log 2>&1
+ICB_PROF=1 timeout 900 python tools/time_rotation.py 131072 > gpurun_out/rot_c3.log 2>&1

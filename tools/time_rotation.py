@@ -31,10 +31,26 @@ def timed(*a, **kw):
 
 
 f.rotate_window = timed
+qtimes = []
+orig_qa = f.query_attend
+
+
+def timed_qa(*a, **kw):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    r = orig_qa(*a, **kw)
+    e1.record()
+    qtimes.append((e0, e1, eng.rotation_due()))
+    return r
+
+
+f.query_attend = timed_qa
 for i in range(steps):
     eng.decode_step(ctx + i, st.queries[i], st.keys[ctx + i], st.values[ctx + i], metrics=False)
 torch.cuda.synchronize()
 ms = [a.elapsed_time(b) for a, b in times]
+qms = [(round(a.elapsed_time(b), 3)) for a, b, _ in qtimes]
+print("query_attend ms per step:", qms)
 print("rotations", len(ms), "ms each", [round(x, 3) for x in ms])
 print("mean rotation ms %.3f  -> %.1f us per decode step amortized" % (sum(ms[1:]) / max(1, len(ms) - 1),
                                                                     1e3 * sum(ms[1:]) / max(1, len(ms) - 1) / 16))
@@ -63,3 +79,13 @@ if os.environ.get("ICB_PROF"):
                                                       for t in order[:8]])
     print("mean fallbacks per tree-rotation %.2f; slowest-10%% trees %.2f" % (fb.mean() / len(ms),
                                                                           fb[order[:24]].mean() / len(ms)))
+
+# node sizes per level (largest nodes drive the P-DCI fallbacks)
+import numpy as np  # noqa: E402
+for tr in (0, eng.T // 2):
+    ex = f.export(tr)
+    by = {}
+    for i, lv, par, own, mem in ex["nodes"]:
+        by.setdefault(lv, []).append(len(mem))
+    print("tree", tr, {lv: (len(v), int(np.max(v)), int(np.sum(np.array(v) > 64))) for lv, v in sorted(by.items())},
+          "(level: nodes, max size, nodes > 64)")
