@@ -768,9 +768,11 @@ __device__ __forceinline__ unsigned long long orderable_f64(double x) {
 // The chain position of member i on ladder j is its rank in the node sorted by
 // (projection_j, id), and the ladder's start is the number of projections
 // below the query's.  Up to kPdciSort members: one bitonic sort per ladder and
-// one of the emission keys, in the idle row ring (S.sortbuf, 64 KB); larger
-// nodes rank by counting (O(m^2)).
+// one of the emission keys, in the idle row ring (S.sortbuf, 64 KB).  Smaller
+// nodes (the sorts' barrier chain costs more than counting there) and larger
+// ones rank by counting (O(m^2)).
 constexpr int kPdciSort = 4096;
+constexpr int kPdciSortMin = 384;
 template <int NT>
 __device__ int pdci_visit(SearchSmem& S, const ForestView& F, const SearchScratch& SS, int t, int node,
                           int g, long long cap, double* dirs_tmp) {
@@ -797,7 +799,7 @@ __device__ int pdci_visit(SearchSmem& S, const ForestView& F, const SearchScratc
   }
   __syncthreads();
   const int cnt = (int)min((long long)m, cap);
-  if (m <= kPdciSort) {
+  if (m > kPdciSortMin && m <= kPdciSort) {
     int n2 = 1;
     while (n2 < m) n2 <<= 1;
     unsigned long long* k64 = S.sortbuf;                            // [n2]
