@@ -122,6 +122,13 @@ int icb_forest_create(const icb_forest_config* cfg, icb_forest** out) {
   AL(F.prev_sel, T * (c.page_cap / 32 + 1), 0);
   F.upper_cap = c.tok_cap / 4 + 64;   // ~r = 10% of points expected; overflow only disables the start shortcut
   AL(F.upper, T * F.upper_cap, 0);
+  F.pc_cap = std::min(4096, c.tok_cap + 64);
+  AL(F.node_pc, T * c.node_cap, 0xff);
+  AL(F.node_pcm, T * c.node_cap, 0xff);
+  AL(F.node_pccap, T * c.node_cap, 0);
+  AL(F.pc_proj, T * F.pc_cap * ICB_NPROJ, 0);
+  AL(F.pc_ord, T * F.pc_cap * ICB_NPROJ, 0);
+  AL(F.pc_pos, T * F.pc_cap * ICB_NPROJ, 0);
 #undef AL
   F.kv_host = c.kv_host != 0;
   F.pool_cap = F.kv_host ? c.pool_pages : 0;

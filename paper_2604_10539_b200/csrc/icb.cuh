@@ -89,6 +89,7 @@ struct TreeMeta {
   int lvl_maxnode[ICB_LV_TRACK];
   int n_upper;
   int lv_ovf;
+  int pc_top;        // P-DCI ladder cache: bump pointer into the tree's arena (entries)
 };
 
 struct ForestView {
@@ -122,6 +123,17 @@ struct ForestView {
   uint32_t* prev_sel; // [T][page_cap/32 + 1] residency: previous step's selection
   int* upper;         // [T][upper_cap] points with top level >= 2
   int upper_cap;
+  // P-DCI ladder cache (query independent, per node of > 64 members): member
+  // projections on the node's 8 directions and, per direction, the members in
+  // (projection, id) order and each member's rank.  Valid while the node's
+  // size equals node_pcm (members are only ever appended).
+  int* node_pc;       // [T][node_cap] arena offset of the node's entries (-1: none)
+  int* node_pcm;      // [T][node_cap] member count the entries describe
+  int* node_pccap;    // [T][node_cap] entries reserved
+  double* pc_proj;    // [T][pc_cap][8] projection of member i on direction j
+  int* pc_ord;        // [T][pc_cap][8] entry (off + r, j): member index of rank r on direction j
+  int* pc_pos;        // [T][pc_cap][8] entry (off + i, j): rank of member i on direction j
+  int pc_cap;
   // KV offload (icb_forest_config.kv_host): page_k / page_v are the pinned,
   // mapped host store; pages a step attends are gathered into a per-tree HBM
   // pool of pool_cap page slots (pagestore.py:169-215 backload / evict)

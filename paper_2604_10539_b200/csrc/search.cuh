@@ -767,12 +767,76 @@ __device__ __forceinline__ unsigned long long orderable_f64(double x) {
 // reference's heap merge (see oracle/dci.py:visit_order for the equivalence).
 // The chain position of member i on ladder j is its rank in the node sorted by
 // (projection_j, id), and the ladder's start is the number of projections
-// below the query's.  Up to kPdciSort members: one bitonic sort per ladder and
-// one of the emission keys, in the idle row ring (S.sortbuf, 64 KB).  Smaller
-// nodes (the sorts' barrier chain costs more than counting there) and larger
-// ones rank by counting (O(m^2)).
+// below the query's.  Everything but the query's projections and gaps is
+// query independent: nodes of up to kPdciSort members keep their projections
+// and ladder ranks in the tree's P-DCI cache (built here with one bitonic sort
+// per ladder in the idle row ring, S.sortbuf, 64 KB; rebuilt when the node
+// has grown), and a visit is then O(8m) plus one sort of the emission keys.
+// Nodes the cache cannot hold rank by counting (O(m^2)).
 constexpr int kPdciSort = 4096;
-constexpr int kPdciSortMin = 384;
+
+// Orderable bits of a fp64 projection.
+__device__ __forceinline__ unsigned long long proj_key(double x) { return orderable_f64(x); }
+
+// Make (or confirm) node's cache entries; returns their offset or -1.
+template <int NT>
+__device__ int pc_ensure(SearchSmem& S, const ForestView& F, int t, int node, int m, const int* mem,
+                         const double* dirs) {
+  __shared__ int s_off;
+  const size_t x = F.nd(t, node);
+  if (F.node_pcm[x] == m && F.node_pc[x] >= 0) return F.node_pc[x];
+  if (m > kPdciSort) return -1;
+  if (threadIdx.x == 0) {
+    int off = F.node_pc[x];
+    if (off < 0 || F.node_pccap[x] < m) {
+      const int want = max(m + (m >> 1), 128);
+      TreeMeta* mt = F.meta + t;
+      off = mt->pc_top + want <= F.pc_cap ? mt->pc_top : -1;
+      if (off >= 0) { mt->pc_top += want; F.node_pc[x] = off; F.node_pccap[x] = want; }
+    }
+    s_off = off;
+  }
+  __syncthreads();
+  const int off = s_off;
+  if (off < 0) return -1;
+  const int D1 = F.dim + 1;
+  double* proj = F.pc_proj + ((size_t)t * F.pc_cap + off) * ICB_NPROJ;
+  int* ord = F.pc_ord + ((size_t)t * F.pc_cap + off) * ICB_NPROJ;
+  int* pos = F.pc_pos + ((size_t)t * F.pc_cap + off) * ICB_NPROJ;
+  for (int xx = threadIdx.x; xx < m * ICB_NPROJ; xx += NT) {
+    const int i = xx / ICB_NPROJ, j = xx % ICB_NPROJ;
+    const float* row = F.row(t, mem[i]);
+    double acc = 0.0;
+    for (int u = 0; u < F.dim; ++u) acc = __fma_rn(dirs[j * D1 + u], (double)row[u], acc);
+    acc = __fma_rn(dirs[j * D1 + F.dim], (double)F.tail[F.tk(t, mem[i])], acc);
+    proj[(size_t)i * ICB_NPROJ + j] = acc;
+  }
+  __syncthreads();
+  int n2 = 1;
+  while (n2 < m) n2 <<= 1;
+  unsigned long long* k64 = S.sortbuf;                            // [n2]
+  unsigned* k32 = reinterpret_cast<unsigned*>(k64 + n2);          // [n2]
+  int* pl = reinterpret_cast<int*>(k32 + n2);                     // [n2]
+  for (int j = 0; j < ICB_NPROJ; ++j) {
+    for (int i = threadIdx.x; i < n2; i += NT) {
+      const bool on = i < m;
+      k64[i] = on ? proj_key(proj[(size_t)i * ICB_NPROJ + j]) : ~0ull;
+      k32[i] = on ? (unsigned)mem[i] : 0xffffffffu;
+      pl[i] = on ? i : -1;
+    }
+    __syncthreads();
+    bitonic3<NT>(k64, k32, pl, n2);
+    for (int r = threadIdx.x; r < m; r += NT) {
+      ord[(size_t)r * ICB_NPROJ + j] = pl[r];
+      pos[(size_t)pl[r] * ICB_NPROJ + j] = r;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) F.node_pcm[x] = m;
+  __syncthreads();
+  return off;
+}
+
 template <int NT>
 __device__ int pdci_visit(SearchSmem& S, const ForestView& F, const SearchScratch& SS, int t, int node,
                           int g, long long cap, double* dirs_tmp) {
@@ -788,7 +852,56 @@ __device__ int pdci_visit(SearchSmem& S, const ForestView& F, const SearchScratc
     for (int u = 0; u < D1; ++u) acc = __fma_rn(dirs[threadIdx.x * D1 + u], S.q64[u], acc);
     S.dirs_tmp[threadIdx.x] = acc;   // query projections
   }
-  // member projections
+  __syncthreads();
+  const int cnt = (int)min((long long)m, cap);
+  const int pco = pc_ensure<NT>(S, F, t, node, m, mem, dirs);
+  if (pco >= 0) {
+    const double* proj = F.pc_proj + ((size_t)t * F.pc_cap + pco) * ICB_NPROJ;
+    const int* ord = F.pc_ord + ((size_t)t * F.pc_cap + pco) * ICB_NPROJ;
+    const int* pos = F.pc_pos + ((size_t)t * F.pc_cap + pco) * ICB_NPROJ;
+    __shared__ int s_start[ICB_NPROJ];
+    if (threadIdx.x < ICB_NPROJ) {   // ladder start: projections strictly below the query's
+      const int j = threadIdx.x;
+      const double qp = S.dirs_tmp[j];
+      int lo = 0, hi = m;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (proj[(size_t)ord[(size_t)mid * ICB_NPROJ + j] * ICB_NPROJ + j] < qp) lo = mid + 1;
+        else hi = mid;
+      }
+      s_start[j] = lo;
+    }
+    __syncthreads();
+    int n2 = 1;
+    while (n2 < m) n2 <<= 1;
+    unsigned long long* k64 = S.sortbuf;
+    unsigned* k32 = reinterpret_cast<unsigned*>(k64 + n2);
+    int* pl = reinterpret_cast<int*>(k32 + n2);
+    for (int i = threadIdx.x; i < n2; i += NT) {
+      unsigned long long bh = ~0ull, bl = 0xffffffffull;
+      if (i < m) {
+        bh = 0; bl = 0;
+        for (int j = 0; j < ICB_NPROJ; ++j) {
+          const int p = pos[(size_t)i * ICB_NPROJ + j], st = s_start[j];
+          const double gap = fabs(__dsub_rn(proj[(size_t)i * ICB_NPROJ + j], S.dirs_tmp[j]));
+          const unsigned long long h = (unsigned long long)__double_as_longlong(gap);
+          const unsigned long long sec = p < st ? (unsigned long long)((1 << 23) - 1 - p)
+                                                : (unsigned long long)((1 << 23) + p);
+          const unsigned long long l = ((unsigned long long)j << 24) | sec;
+          if (h > bh || (h == bh && l > bl)) { bh = h; bl = l; }
+        }
+      }
+      k64[i] = bh;
+      k32[i] = (unsigned)bl;
+      pl[i] = i < m ? mem[i] : -1;
+    }
+    __syncthreads();
+    bitonic3<NT>(k64, k32, pl, n2);
+    for (int r = threadIdx.x; r < cnt; r += NT) SS.vis[r] = pl[r];
+    __syncthreads();
+    return cnt;
+  }
+  // uncached: member projections, then ranks by counting
   for (int x = threadIdx.x; x < m * ICB_NPROJ; x += NT) {
     int i = x / ICB_NPROJ, j = x % ICB_NPROJ;
     const float* row = F.row(t, mem[i]);
@@ -798,59 +911,6 @@ __device__ int pdci_visit(SearchSmem& S, const ForestView& F, const SearchScratc
     SS.proj[(size_t)i * ICB_NPROJ + j] = acc;
   }
   __syncthreads();
-  const int cnt = (int)min((long long)m, cap);
-  if (m > kPdciSortMin && m <= kPdciSort) {
-    int n2 = 1;
-    while (n2 < m) n2 <<= 1;
-    unsigned long long* k64 = S.sortbuf;                            // [n2]
-    unsigned* k32 = reinterpret_cast<unsigned*>(k64 + n2);          // [n2]
-    int* pl = reinterpret_cast<int*>(k32 + n2);                     // [n2]
-    for (int i = threadIdx.x; i < m; i += NT) { SS.ekey[2 * (size_t)i] = 0; SS.ekey[2 * (size_t)i + 1] = 0; }
-    for (int j = 0; j < ICB_NPROJ; ++j) {
-      // ladder j: members by (projection, id)
-      for (int i = threadIdx.x; i < n2; i += NT) {
-        const bool on = i < m;
-        k64[i] = on ? orderable_f64(SS.proj[(size_t)i * ICB_NPROJ + j]) : ~0ull;
-        k32[i] = on ? (unsigned)mem[i] : 0xffffffffu;
-        pl[i] = on ? i : -1;
-      }
-      __syncthreads();
-      bitonic3<NT>(k64, k32, pl, n2);
-      // start = #projections strictly below the query's (binary search)
-      const double qp = S.dirs_tmp[j];
-      const unsigned long long qk = orderable_f64(qp);
-      int lo = 0, hi = m;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (k64[mid] < qk) lo = mid + 1;
-        else hi = mid;
-      }
-      const int start = lo;
-      for (int pos = threadIdx.x; pos < m; pos += NT) {
-        const int i = pl[pos];
-        const double gap = fabs(__dsub_rn(SS.proj[(size_t)i * ICB_NPROJ + j], qp));
-        const unsigned long long h = (unsigned long long)__double_as_longlong(gap);
-        const unsigned long long sec = pos < start ? (unsigned long long)((1 << 23) - 1 - pos)
-                                                   : (unsigned long long)((1 << 23) + pos);
-        const unsigned long long l = ((unsigned long long)j << 24) | sec;
-        const unsigned long long bh = SS.ekey[2 * (size_t)i], bl = SS.ekey[2 * (size_t)i + 1];
-        if (h > bh || (h == bh && l > bl)) { SS.ekey[2 * (size_t)i] = h; SS.ekey[2 * (size_t)i + 1] = l; }
-      }
-      __syncthreads();
-    }
-    // the cnt smallest emission keys, ascending
-    for (int i = threadIdx.x; i < n2; i += NT) {
-      const bool on = i < m;
-      k64[i] = on ? SS.ekey[2 * (size_t)i] : ~0ull;
-      k32[i] = on ? (unsigned)SS.ekey[2 * (size_t)i + 1] : 0xffffffffu;
-      pl[i] = on ? mem[i] : -1;
-    }
-    __syncthreads();
-    bitonic3<NT>(k64, k32, pl, n2);
-    for (int r = threadIdx.x; r < cnt; r += NT) SS.vis[r] = pl[r];
-    __syncthreads();
-    return cnt;
-  }
   // emission keys
   for (int i = threadIdx.x; i < m; i += NT) {
     unsigned long long best_hi = 0, best_lo = 0;

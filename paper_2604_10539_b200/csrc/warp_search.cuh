@@ -13,9 +13,12 @@
 // is the fixed-order fp32 distance (per lane fma chain, xor butterfly
 // 16,8,4,2,1 -- the first three levels transposed across 8 rows, which keeps
 // each row's pairing tree); ranking keys (d2 bits, id).  A node that the
-// reference would visit with P-DCI (size > 64 = max(EXHAUSTIVE_NODE_LIMIT,
-// visit_cap)) makes the search return false: the caller falls back to the
-// block search, which implements P-DCI.
+// reference visits with P-DCI (size > 64 = max(EXHAUSTIVE_NODE_LIMIT,
+// visit_cap)) contributes its 64-member visit list, computed here from the
+// tree's P-DCI cache (member projections and ladder ranks, search.cuh
+// pc_ensure) when the node's entries and directions are cached and it has at
+// most kWarpPdciMax members; otherwise the search returns false and the
+// caller falls back to the block search (which also fills the cache).
 #pragma once
 #include "icb.cuh"
 
@@ -23,6 +26,7 @@ namespace icb {
 
 constexpr int kWarpBeam = 8;
 constexpr int kWarpMaxCand = kWarpBeam * 64;   // 8 nodes x 64 members
+constexpr int kWarpPdciMax = 256;              // P-DCI nodes the warp visits itself (8 members per lane)
 
 struct WarpSearchBuf {   // per warp, shared memory
   int ids[kWarpMaxCand];
@@ -38,6 +42,80 @@ __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v)
     v = w < v ? w : v;
   }
   return v;
+}
+
+// P-DCI visit list of node x (sz > 64 members at `moff`, cache entries at
+// `pco`, directions `dirs`) for the lifted query (q, qt): the 64 members of
+// smallest emission key (search.cuh pdci_visit, same keys) into out[0..64).
+__device__ inline void warp_pdci_visit(const ForestView& F, int t, const int* mem, int sz, int pco,
+                                       const double* dirs, const float* q, float qt, int* out) {
+  const int lane = threadIdx.x & 31;
+  const int D1 = F.dim + 1;
+  const double* proj = F.pc_proj + ((size_t)t * F.pc_cap + pco) * ICB_NPROJ;
+  const int* ord = F.pc_ord + ((size_t)t * F.pc_cap + pco) * ICB_NPROJ;
+  const int* pos = F.pc_pos + ((size_t)t * F.pc_cap + pco) * ICB_NPROJ;
+  // query projection and ladder start of direction `lane` (lanes 0..7), the
+  // same sequential fp64 chain as the block visit
+  double qp = 0.0;
+  int st = 0;
+  if (lane < ICB_NPROJ) {
+    double acc = 0.0;
+    for (int u = 0; u < D1; ++u) acc = __fma_rn(dirs[lane * D1 + u], u < F.dim ? (double)q[u] : (double)qt, acc);
+    qp = acc;
+    int lo = 0, hi = sz;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (proj[(size_t)ord[(size_t)mid * ICB_NPROJ + lane] * ICB_NPROJ + lane] < qp) lo = mid + 1;
+      else hi = mid;
+    }
+    st = lo;
+  }
+  double qpj[ICB_NPROJ];
+  int stj[ICB_NPROJ];
+#pragma unroll
+  for (int j = 0; j < ICB_NPROJ; ++j) { qpj[j] = __shfl_sync(0xffffffffu, qp, j); stj[j] = __shfl_sync(0xffffffffu, st, j); }
+  constexpr int R = kWarpPdciMax / 32;
+  unsigned long long kh[R];
+  unsigned kl[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = lane + 32 * r;
+    unsigned long long bh = ~0ull, bl = 0xffffffffull;
+    if (i < sz) {
+      bh = 0; bl = 0;
+#pragma unroll
+      for (int j = 0; j < ICB_NPROJ; ++j) {
+        const int p = pos[(size_t)i * ICB_NPROJ + j];
+        const double gap = fabs(__dsub_rn(proj[(size_t)i * ICB_NPROJ + j], qpj[j]));
+        const unsigned long long h = (unsigned long long)__double_as_longlong(gap);
+        const unsigned long long sec = p < stj[j] ? (unsigned long long)((1 << 23) - 1 - p)
+                                                  : (unsigned long long)((1 << 23) + p);
+        const unsigned long long l = ((unsigned long long)j << 24) | sec;
+        if (h > bh || (h == bh && l > bl)) { bh = h; bl = l; }
+      }
+    }
+    kh[r] = bh;
+    kl[r] = (unsigned)bl;
+  }
+  // 64 rounds of warp argmin over the (unique) emission keys
+  for (int c = 0; c < 64; ++c) {
+    unsigned long long mh = ~0ull;
+    unsigned ml = 0xffffffffu;
+    int mr = -1;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (kh[r] < mh || (kh[r] == mh && kl[r] < ml)) { mh = kh[r]; ml = kl[r]; mr = r; }
+    const unsigned long long wh = warp_min_u64(mh);
+    const unsigned wl = __reduce_min_sync(0xffffffffu, mh == wh ? ml : 0xffffffffu);
+    const bool mine = mh == wh && ml == wl && mr >= 0;
+    if (mine) {
+      out[c] = mem[lane + 32 * mr];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (r == mr) { kh[r] = ~0ull; kl[r] = 0xffffffffu; }
+    }
+  }
+  __syncwarp();
 }
 
 // q: lifted query (smem, ICB_DPAD floats), qt its tail.  On success returns
@@ -58,26 +136,39 @@ __device__ inline bool warp_parent_search(const ForestView& F, int t, const floa
   for (int lv = L; lv >= floor; --lv) {
     // the level's nodes: lane i < nn holds node i
     const int nn = lv == L ? 1 : ns;
-    int sz = 0, off = 0;
+    int sz = 0, off = 0, nd = -1;
     if (lane < nn) {
-      const int nd = lv == L ? mt.top_node : F.own(t, sv, lv);
+      nd = lv == L ? mt.top_node : F.own(t, sv, lv);
       sz = F.node_size[F.nd(t, nd)];
       off = F.node_off[F.nd(t, nd)];
     }
-    if (__any_sync(0xffffffffu, sz > 64)) return false;   // P-DCI node: block search
-    int ex = sz;
+    // P-DCI nodes: 64-member visit lists from the cache, else the block search
+    const bool big = sz > 64;
+    if (__any_sync(0xffffffffu, big)) {
+      const bool ready = !big || (sz <= kWarpPdciMax && F.node_pcm[F.nd(t, nd)] == sz &&
+                                  F.node_pc[F.nd(t, nd)] >= 0 && F.node_dirs[F.nd(t, nd)] >= 0);
+      if (!__all_sync(0xffffffffu, ready)) return false;
+    }
+    const int cnt = big ? 64 : sz;
+    int ex = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, ex, o);
       if (lane >= o) ex += y;
     }
     const int M = __shfl_sync(0xffffffffu, ex, 31);
-    ex -= sz;
-    // candidate ids, node by node (coalesced member copies)
+    ex -= cnt;
+    // candidate ids, node by node (coalesced member copies / P-DCI visit lists)
     for (int i = 0; i < nn; ++i) {
       const int e = __shfl_sync(0xffffffffu, ex, i), o = __shfl_sync(0xffffffffu, off, i);
       const int s = __shfl_sync(0xffffffffu, sz, i);
-      for (int j = lane; j < s; j += 32) W.ids[e + j] = mem[o + j];
+      if (s > 64) {
+        const size_t x = F.nd(t, __shfl_sync(0xffffffffu, nd, i));
+        const double* dirs = F.dirs + ((size_t)t * F.dirs_cap + F.node_dirs[x]) * ICB_NPROJ * (F.dim + 1);
+        warp_pdci_visit(F, t, mem + o, s, F.node_pc[x], dirs, q, qt, W.ids + e);
+      } else {
+        for (int j = lane; j < s; j += 32) W.ids[e + j] = mem[o + j];
+      }
     }
     __syncwarp();
     ev += (unsigned long long)M;
