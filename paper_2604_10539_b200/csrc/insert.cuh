@@ -68,6 +68,44 @@ __device__ inline int new_node(const ForestView& F, int t, int level, int parent
   return id;
 }
 
+// Keep a node's P-DCI cache (search.cuh pc_ensure) valid across an append of
+// member `tok` at position sz (ONE thread): its 8 projections (the same fp64
+// chains), then on every ladder its rank by (projection, id) and the shifted
+// ranks of the members after it.  Without fresh entries, room and directions
+// the cache is left stale (rebuilt by the next block visit).
+__device__ inline void pc_append(const ForestView& F, int t, size_t x, const int* mem, int sz, int tok) {
+  const int off = F.node_pc[x];
+  if (off < 0 || F.node_pcm[x] != sz || F.node_pccap[x] <= sz || F.node_dirs[x] < 0) return;
+  const int D1 = F.dim + 1;
+  const double* dirs = F.dirs + ((size_t)t * F.dirs_cap + F.node_dirs[x]) * ICB_NPROJ * D1;
+  double* proj = F.pc_proj + ((size_t)t * F.pc_cap + off) * ICB_NPROJ;
+  int* ord = F.pc_ord + ((size_t)t * F.pc_cap + off) * ICB_NPROJ;
+  int* pos = F.pc_pos + ((size_t)t * F.pc_cap + off) * ICB_NPROJ;
+  const float* row = F.row(t, tok);
+  const float tl = F.tail[F.tk(t, tok)];
+  for (int j = 0; j < ICB_NPROJ; ++j) {
+    double acc = 0.0;
+    for (int u = 0; u < F.dim; ++u) acc = __fma_rn(dirs[j * D1 + u], (double)row[u], acc);
+    acc = __fma_rn(dirs[j * D1 + F.dim], (double)tl, acc);
+    proj[(size_t)sz * ICB_NPROJ + j] = acc;
+    int lo = 0, hi = sz;   // rank: members below (acc, tok)
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1, mi = ord[(size_t)mid * ICB_NPROJ + j];
+      const double p = proj[(size_t)mi * ICB_NPROJ + j];
+      if (p < acc || (p == acc && mem[mi] < tok)) lo = mid + 1;
+      else hi = mid;
+    }
+    for (int r = sz; r > lo; --r) {
+      const int mi = ord[(size_t)(r - 1) * ICB_NPROJ + j];
+      ord[(size_t)r * ICB_NPROJ + j] = mi;
+      pos[(size_t)mi * ICB_NPROJ + j] = r;
+    }
+    ord[(size_t)lo * ICB_NPROJ + j] = sz;
+    pos[(size_t)sz * ICB_NPROJ + j] = lo;
+  }
+  F.node_pcm[x] = sz + 1;
+}
+
 __device__ inline void add_member(const ForestView& F, int t, int node, int tok) {
   TreeMeta* m = F.meta + t;
   size_t x = F.nd(t, node);
@@ -84,9 +122,9 @@ __device__ inline void add_member(const ForestView& F, int t, int node, int tok)
     F.node_capm[x] = ncap;
   }
   mem[off + sz] = tok;
+  pc_append(F, t, x, mem + off, sz, tok);
   F.node_size[x] = sz + 1;
   note_node_size(m, F.node_level[x], sz + 1);
-  // the node's P-DCI ladders are a function of its member set: nothing to update
 }
 
 __device__ __forceinline__ void set_own(const ForestView& F, int t, int tok, int lv, int node) {
@@ -496,6 +534,7 @@ __device__ inline void insert_points(SearchSmem& S, GroupSmem* GSA, const RingVi
         }
         if (ok) {
           mem[off + sz] = tok;
+          pc_append(F, t, x, mem + off, sz, tok);
           F.node_size[x] = sz + 1;
           note_node_size(m, s_rlv[w], sz + 1);
           ++sz;

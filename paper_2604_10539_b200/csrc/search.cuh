@@ -757,6 +757,7 @@ __device__ void bitonic3(unsigned long long* k64, unsigned* k32, int* pl, int n)
 }
 
 __device__ __forceinline__ unsigned long long orderable_f64(double x) {
+  if (x == 0.0) x = 0.0;   // -0 == +0 (ties then break by id, as the numeric comparison does)
   const unsigned long long b = (unsigned long long)__double_as_longlong(x);
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
