@@ -160,3 +160,13 @@ extern "C" int icb_insert_profile(unsigned long long* out, int reset) {
   }
   return ICB_OK;
 }
+
+extern "C" int icb_pdci_stats(unsigned long long* out, int reset) {
+  ICB_CUDA(cudaDeviceSynchronize());
+  ICB_CUDA(cudaMemcpyFromSymbol(out, icb::g_pdci_miss, sizeof(unsigned long long) * 4));
+  if (reset) {
+    unsigned long long z[4] = {};
+    ICB_CUDA(cudaMemcpyToSymbol(icb::g_pdci_miss, z, sizeof(z)));
+  }
+  return ICB_OK;
+}

@@ -27,6 +27,8 @@ namespace icb {
 constexpr int kWarpBeam = 8;
 constexpr int kWarpMaxCand = kWarpBeam * 64;   // 8 nodes x 64 members
 constexpr int kWarpPdciMax = 256;              // P-DCI nodes the warp visits itself (8 members per lane)
+// warp-search P-DCI misses by reason: too large, no directions, no cache entries, stale entries
+static __device__ unsigned long long g_pdci_miss[4];
 
 struct WarpSearchBuf {   // per warp, shared memory
   int ids[kWarpMaxCand];
@@ -147,6 +149,11 @@ __device__ inline bool warp_parent_search(const ForestView& F, int t, const floa
     if (__any_sync(0xffffffffu, big)) {
       const bool ready = !big || (sz <= kWarpPdciMax && F.node_pcm[F.nd(t, nd)] == sz &&
                                   F.node_pc[F.nd(t, nd)] >= 0 && F.node_dirs[F.nd(t, nd)] >= 0);
+      if (!ready) {   // why the warp cannot visit this P-DCI node (icb_pdci_stats)
+        const size_t x = F.nd(t, nd);
+        const int why = sz > kWarpPdciMax ? 0 : F.node_dirs[x] < 0 ? 1 : F.node_pc[x] < 0 ? 2 : 3;
+        atomicAdd(&g_pdci_miss[why], 1ull);
+      }
       if (!__all_sync(0xffffffffu, ready)) return false;
     }
     const int cnt = big ? 64 : sz;

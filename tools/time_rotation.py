@@ -80,6 +80,17 @@ if os.environ.get("ICB_PROF"):
     print("mean fallbacks per tree-rotation %.2f; slowest-10%% trees %.2f" % (fb.mean() / len(ms),
                                                                           fb[order[:24]].mean() / len(ms)))
 
+lib2 = __import__("paper_2604_10539_b200._native", fromlist=["lib"]).lib()
+import ctypes  # noqa: E402
+import numpy as np  # noqa: E402
+pm = np.zeros(4, dtype=np.uint64)
+lib2.icb_pdci_stats.argtypes = [ctypes.c_void_p, ctypes.c_int]
+lib2.icb_pdci_stats(pm.ctypes.data_as(ctypes.c_void_p), 0)
+print("warp P-DCI misses (too large, no directions, no cache, stale):", pm.tolist())
+for t in (0, 1):
+    i = f.info(t)
+    print("tree", t, "n_dirs", i["n_dirs"])
+
 # node sizes per level (largest nodes drive the P-DCI fallbacks)
 import numpy as np  # noqa: E402
 for tr in (0, eng.T // 2):
