@@ -1168,7 +1168,11 @@ int icb_build_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t n_poi
   build_page_totals_kernel<<<(n + 127) / 128, 128, 0, st>>>(F, A, max_nodes, leaf_first, leaf_pages);
   build_summary_kernel<<<n, 256, 0, st>>>(F, A);
   ICB_CUDA(cudaGetLastError());
-  return S.finish();
+  int rc = S.finish();
+  if (rc) return rc;
+  // P-DCI directions + ladder caches of the nodes decode will visit with P-DCI
+  // (the default decode budget's visit cap: 4 x 256)
+  return icb_pdci_warm_impl(f, trees, n, 1024, st);
 }
 
 extern "C" int icb_build_profile(unsigned long long* out, int reset) {

@@ -122,7 +122,7 @@ int icb_forest_create(const icb_forest_config* cfg, icb_forest** out) {
   AL(F.prev_sel, T * (c.page_cap / 32 + 1), 0);
   F.upper_cap = c.tok_cap / 4 + 64;   // ~r = 10% of points expected; overflow only disables the start shortcut
   AL(F.upper, T * F.upper_cap, 0);
-  F.pc_cap = std::min(4096, c.tok_cap + 64);
+  F.pc_cap = std::min(6144, c.tok_cap + 64);
   AL(F.node_pc, T * c.node_cap, 0xff);
   AL(F.node_pcm, T * c.node_cap, 0xff);
   AL(F.node_pccap, T * c.node_cap, 0);

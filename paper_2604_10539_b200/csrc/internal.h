@@ -129,3 +129,4 @@ bool icb_dense_flash_ok(int G, int dim, int dim_v, int kv_dtype);
 int icb_dense_flash_impl(int32_t n, int32_t G, const float* q, const void* k, const void* v, int64_t ld,
                          int32_t n_tokens, const int32_t* token_dev, float* out, int32_t splits, float* part,
                          unsigned* counter, cudaStream_t st);
+int icb_pdci_warm_impl(icb_forest* f, const int32_t* trees, int32_t n, int64_t qcap, cudaStream_t st);

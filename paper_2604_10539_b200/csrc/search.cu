@@ -440,6 +440,59 @@ __global__ void __launch_bounds__(NT) node_query_kernel(ForestView F, int t, int
 }
 }  // namespace icb
 
+namespace icb {
+// Warm the P-DCI caches of freshly built trees (one CTA per tree): directions
+// and ladder entries of every node the decode path visits with P-DCI --
+// levels >= 2 above 64 members (insert parent searches, visit cap 64) and
+// leaves above the query visit cap -- so no later search pays for them.
+template <int NT>
+__global__ void __launch_bounds__(NT) pdci_warm_kernel(ForestView F, const int32_t* trees, long long qcap,
+                                                       double* tmp_dirs) {
+  __shared__ SearchSmem S;
+  __shared__ int s_list[512], s_n;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  const RingView RG = ring_view(dsm, 1);
+  if (threadIdx.x == 0) S.sortbuf = reinterpret_cast<unsigned long long*>(RG.ring);
+  const int t = trees[blockIdx.x];
+  const int nn = F.meta[t].n_nodes;
+  double* tmp = tmp_dirs + (size_t)blockIdx.x * ICB_NPROJ * (F.dim + 1);
+  for (int base = 0; base < nn; base += 512 * 4) {
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    for (int node = base + threadIdx.x; node < min(nn, base + 512 * 4); node += NT) {
+      const size_t x = F.nd(t, node);
+      const int sz = F.node_size[x], lv = F.node_level[x];
+      if (sz > ICB_EXHAUSTIVE && sz <= kPdciSort && (lv >= 2 || sz > qcap)) {
+        const int at = atomicAdd(&s_n, 1);
+        if (at < 512) s_list[at] = node;
+      }
+    }
+    __syncthreads();
+    const int cnt = min(s_n, 512);
+    for (int i = 0; i < cnt; ++i) {
+      const int node = s_list[i];
+      const size_t x = F.nd(t, node);
+      const double* dirs = pdci_dirs<NT>(F, t, node, tmp);
+      if (F.node_dirs[x] < 0) break;   // direction cache full
+      pc_ensure<NT>(S, F, t, node, F.node_size[x], F.mem(t) + F.node_off[x], dirs);
+    }
+    __syncthreads();
+  }
+}
+}  // namespace icb
+
+int icb_pdci_warm_impl(icb_forest* f, const int32_t* trees, int32_t n, int64_t qcap, cudaStream_t st) {
+  if (n <= 0) return ICB_OK;
+  Scratch S(st);
+  double* tmp = S.alloc<double>((size_t)n * ICB_NPROJ * (f->view.dim + 1));
+  if (!S.ok()) return S.fail();
+  const size_t dsm = search_dsm_bytes(1);
+  ICB_CUDA(cudaFuncSetAttribute(pdci_warm_kernel<kSearchThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)dsm));
+  pdci_warm_kernel<kSearchThreads><<<n, kSearchThreads, dsm, st>>>(f->view, trees, qcap, tmp);
+  return S.finish();
+}
+
 int icb_node_query_impl(icb_forest* f, int32_t tree, int32_t node, const float* q_lifted, int32_t k,
                         int64_t visit_cap, int32_t* out_ids, int32_t* out_count, cudaStream_t st) {
   char* scratch;
