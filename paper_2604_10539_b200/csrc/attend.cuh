@@ -358,6 +358,43 @@ __device__ long long gather_pages(const ForestView& F, int t, const int32_t* sel
   return bytes;
 }
 
+// Residency accounting of one tree's step (TierStore.backload /
+// evict_unselected, pagestore.py:169-215): pages of `sel` not selected last
+// step are loaded; the previous-selection bitmap becomes `sel`.
+template <int NT>
+__device__ void tree_residency(const ForestView& F, int t, const int32_t* sel, int nsel, int64_t* stats,
+                               int scalar_bytes) {
+  if (!stats) return;
+  __shared__ int s_fill_sel, s_loaded, s_fill_loaded;
+  if (threadIdx.x == 0) { s_fill_sel = 0; s_loaded = 0; s_fill_loaded = 0; }
+  __syncthreads();
+  uint32_t* bits = F.prev_sel + (size_t)t * F.pwords();
+  int fs = 0, ld = 0, fl = 0;
+  for (int i = threadIdx.x; i < nsel; i += NT) {
+    const int p = sel[i];
+    const int f = F.page_fill[F.pg(t, p)];
+    fs += f;
+    if (!((bits[p >> 5] >> (p & 31)) & 1u)) { ld += 1; fl += f; }
+  }
+  atomicAdd(&s_fill_sel, fs);
+  atomicAdd(&s_loaded, ld);
+  atomicAdd(&s_fill_loaded, fl);
+  __syncthreads();
+  for (int w = threadIdx.x; w < F.pwords(); w += NT) bits[w] = 0u;
+  __syncthreads();
+  for (int i = threadIdx.x; i < nsel; i += NT) {
+    const int p = sel[i];
+    atomicOr(bits + (p >> 5), 1u << (p & 31));
+  }
+  if (threadIdx.x == 0) {
+    stats[0] += nsel;
+    stats[1] += s_fill_sel;
+    stats[2] += s_loaded;
+    stats[3] += (int64_t)s_fill_loaded * (F.dim + F.dim_v) * scalar_bytes;
+    stats[4] += s_loaded > 0 ? 1 : 0;
+  }
+}
+
 template <typename KT, int G, int NT, bool NC = true>
 __device__ void attend_tree_paged(const ForestView& F, int t, int GA, const float* q /*[GA][dim]*/,
                                   const int32_t* sel, int nsel, float* out /*[GA][dim_v]*/, int64_t* stats,
@@ -450,36 +487,6 @@ __device__ void attend_tree_paged(const ForestView& F, int t, int GA, const floa
     if (ln * 4 + 2 < F.dim_v) og[ln * 4 + 2] = acc.z * inv;
     if (ln * 4 + 3 < F.dim_v) og[ln * 4 + 3] = acc.w * inv;
   }
-  // residency accounting (pagestore.py:169-215)
-  if (stats) {
-    __shared__ int s_fill_sel, s_loaded, s_fill_loaded;
-    if (threadIdx.x == 0) { s_fill_sel = 0; s_loaded = 0; s_fill_loaded = 0; }
-    __syncthreads();
-    uint32_t* bits = F.prev_sel + (size_t)t * F.pwords();
-    int fs = 0, ld = 0, fl = 0;
-    for (int i = threadIdx.x; i < nsel; i += NT) {
-      const int p = sel[i];
-      const int f = F.page_fill[F.pg(t, p)];
-      fs += f;
-      if (!((bits[p >> 5] >> (p & 31)) & 1u)) { ld += 1; fl += f; }
-    }
-    atomicAdd(&s_fill_sel, fs);
-    atomicAdd(&s_loaded, ld);
-    atomicAdd(&s_fill_loaded, fl);
-    __syncthreads();
-    for (int w = threadIdx.x; w < F.pwords(); w += NT) bits[w] = 0u;
-    __syncthreads();
-    for (int i = threadIdx.x; i < nsel; i += NT) {
-      const int p = sel[i];
-      atomicOr(bits + (p >> 5), 1u << (p & 31));
-    }
-    if (threadIdx.x == 0) {
-      stats[0] += nsel;
-      stats[1] += s_fill_sel;
-      stats[2] += s_loaded;
-      stats[3] += (int64_t)s_fill_loaded * (F.dim + F.dim_v) * scalar_bytes;
-      stats[4] += s_loaded > 0 ? 1 : 0;
-    }
-  }
+  tree_residency<NT>(F, t, sel, nsel, stats, scalar_bytes);
 }
 }  // namespace icb

@@ -4,6 +4,7 @@
 #include "search.cuh"
 #include "insert.cuh"
 #include "attend.cuh"
+#include "attend_mma.cuh"
 #include "internal.h"
 
 namespace icb {
@@ -26,6 +27,7 @@ struct QueryArgs {
   int64_t* attn_stats;   // [n][5] or null
   int scalar_bytes;
   float scale_log2;
+  int attn_simt;              // 1: CUDA-core attention chunks (ICB_ATTN_SIMT=1, A/B), else tensor cores when possible
   // fused decode-step prologue (icb_step_attend, the STEP kernel variant):
   // rotate the oldest window page into the tree (if rotate), then append the
   // decode token to the window, then search + attend
@@ -205,11 +207,19 @@ __global__ void __launch_bounds__(NT, 512 / NT) query_kernel(ForestView F, Query
       atomicAdd(&s_moved, (unsigned long long)moved);
       __syncthreads();
       if (threadIdx.x == 0) F.pool_bytes[t] += (long long)s_moved;
-      if (F.kv_bf16)
+      if (attend_mma_ok(F, G) && !A.attn_simt) {
+        attend_tree_mma<NT, false>(F, t, G, qb, sel, nsel, ob, A.scale_log2, sm,
+                                   reinterpret_cast<unsigned char*>(&S.q[0][0]));
+        tree_residency<NT>(F, t, sel, nsel, stb, A.scalar_bytes);
+      } else if (F.kv_bf16)
         attend_tree_paged<__nv_bfloat16, GP, NT, false>(F, t, G, qb, sel, nsel, ob, stb, A.scalar_bytes,
                                                         A.scale_log2, sm);
       else
         attend_tree_paged<float, GP, NT, false>(F, t, G, qb, sel, nsel, ob, stb, A.scalar_bytes, A.scale_log2, sm);
+    } else if (attend_mma_ok(F, G) && !A.attn_simt) {
+      attend_tree_mma<NT, !STEP>(F, t, G, qb, sel, nsel, ob, A.scale_log2, sm,
+                                 reinterpret_cast<unsigned char*>(&S.q[0][0]));
+      tree_residency<NT>(F, t, sel, nsel, stb, A.scalar_bytes);
     } else if (F.kv_bf16) {
       attend_tree_paged<__nv_bfloat16, GP, NT, !STEP>(F, t, G, qb, sel, nsel, ob, stb, A.scalar_bytes, A.scale_log2, sm);
     } else {
@@ -301,6 +311,7 @@ int icb_query_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, co
   A.pages_cap = pages_cap; A.out_npages = out_npages;
   A.attn_out = attn_out; A.attn_stats = attn_stats; A.scalar_bytes = scalar_bytes;
   A.scale_log2 = (float)(1.4426950408889634 / sqrt((double)f->cfg.dim));
+  A.attn_simt = getenv("ICB_ATTN_SIMT") != nullptr;
   if (step) {
     A.rotate = step->rotate;
     if (step->rotate && (rc = ensure_insert_scratch(f, n, &A.rot_scratch, &A.rot_SL))) return rc;
