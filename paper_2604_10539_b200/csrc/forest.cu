@@ -3,6 +3,8 @@
 #include "internal.h"
 #include <cstring>
 #include <mutex>
+#include <sys/mman.h>
+#include <thread>
 
 static thread_local std::string g_last_error;
 static thread_local int g_last_code = 0;
@@ -33,6 +35,59 @@ __global__ void seed_kernel(ForestView F, int t, Pcg64 g, int n_words, uint32_t 
 }  // namespace icb
 
 using namespace icb;
+
+// Pinned, device-mapped host store of `bytes` (KV offload).  Pinning tens of
+// GB is dominated by faulting and locking the pages one range at a time, so
+// the range is mmap'ed once and registered in 1 GB chunks from parallel host
+// threads.  The chunks' device addresses must continue one another (true
+// when registered memory is used at its host address, UVA); otherwise, or if
+// anything fails, one cudaHostAlloc does it.  *dev gets the device address.
+static int pin_host_store(icb_forest* f, size_t bytes, void** dev) {
+  int can_use_host_ptr = 0, d = 0;
+  cudaGetDevice(&d);
+  cudaDeviceGetAttribute(&can_use_host_ptr, cudaDevAttrCanUseHostPointerForRegisteredMem, d);
+  const size_t chunk = 1ull << 30;
+  if (can_use_host_ptr && bytes >= 2 * chunk) {
+    void* h = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (h != MAP_FAILED) {
+      const size_t n = (bytes + chunk - 1) / chunk;
+      std::vector<cudaError_t> err(n, cudaSuccess);
+      const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+      std::vector<std::thread> pool;
+      for (unsigned w = 0; w < nt; ++w)
+        pool.emplace_back([&, w]() {
+          cudaSetDevice(d);
+          for (size_t i = w; i < n; i += nt) {
+            const size_t off = i * chunk, len = std::min(chunk, bytes - off);
+            err[i] = cudaHostRegister((char*)h + off, len, cudaHostRegisterMapped | cudaHostRegisterPortable);
+          }
+        });
+      for (auto& th : pool) th.join();
+      bool ok = true;
+      for (size_t i = 0; i < n && ok; ++i) {
+        void* dp = nullptr;
+        ok = err[i] == cudaSuccess && cudaHostGetDevicePointer(&dp, (char*)h + i * chunk, 0) == cudaSuccess &&
+             dp == (char*)h + i * chunk;
+      }
+      if (ok) {
+        f->host_regs.push_back({h, bytes});
+        *dev = h;
+        return ICB_OK;
+      }
+      for (size_t i = 0; i < n; ++i)
+        if (err[i] == cudaSuccess) cudaHostUnregister((char*)h + i * chunk);
+      cudaGetLastError();
+      munmap(h, bytes);
+    }
+  }
+  void* h = nullptr;
+  cudaError_t e = cudaHostAlloc(&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+  if (e != cudaSuccess) { icb_set_error(ICB_E_CUDA, cudaGetErrorString(e)); return ICB_E_CUDA; }
+  f->host_allocs.push_back(h);
+  e = cudaHostGetDevicePointer(dev, h, 0);
+  if (e != cudaSuccess) { icb_set_error(ICB_E_CUDA, cudaGetErrorString(e)); return ICB_E_CUDA; }
+  return ICB_OK;
+}
 
 void zero_node_sizes(icb_forest* f, const int32_t* trees, int n, cudaStream_t st) {
   dim3 grid((f->cfg.node_cap + 255) / 256, n);
@@ -144,15 +199,10 @@ int icb_forest_create(const icb_forest_config* cfg, icb_forest** out) {
     // the host store: pinned, mapped into the device address space
     const size_t nk = T * c.page_cap * c.page_size * F.dkp * kvb, nv = T * c.page_cap * c.page_size * F.dvp * kvb;
     for (int i = 0; i < 2 && rc == ICB_OK; ++i) {
-      void* h = nullptr;
-      cudaError_t e = cudaHostAlloc(&h, i ? nv : nk, cudaHostAllocMapped | cudaHostAllocPortable);
-      if (e != cudaSuccess) { icb_set_error(ICB_E_CUDA, cudaGetErrorString(e)); rc = ICB_E_CUDA; break; }
-      f->host_allocs.push_back(h);
-      // no memset: freshly pinned pages are zero, and every row is written at
+      // no memset: freshly mapped pages are zero, and every row is written at
       // full padded width (build scatter, write_slot) before anything reads it
       void* d = nullptr;
-      e = cudaHostGetDevicePointer(&d, h, 0);
-      if (e != cudaSuccess) { icb_set_error(ICB_E_CUDA, cudaGetErrorString(e)); rc = ICB_E_CUDA; break; }
+      rc = pin_host_store(f, i ? nv : nk, &d);
       (i ? F.page_v : F.page_k) = d;
     }
     char* qk = nullptr;
@@ -179,6 +229,11 @@ int icb_forest_destroy(icb_forest* f) {
   cudaDeviceSynchronize();
   for (void* p : f->allocs) cudaFree(p);
   for (void* p : f->host_allocs) cudaFreeHost(p);
+  for (auto& r : f->host_regs) {
+    const size_t chunk = 1ull << 30;
+    for (size_t off = 0; off < r.second; off += chunk) cudaHostUnregister((char*)r.first + off);
+    munmap(r.first, r.second);
+  }
   if (f->qscratch) cudaFree(f->qscratch);
   if (f->iscratch) cudaFree(f->iscratch);
   if (f->ascratch) cudaFree(f->ascratch);

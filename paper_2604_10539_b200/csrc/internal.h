@@ -4,6 +4,7 @@
 #include <stdint.h>
 #include <string>
 #include <vector>
+#include <utility>
 #include <algorithm>
 #include "icb.cuh"
 
@@ -33,6 +34,7 @@ struct icb_forest {
   ForestView view;
   std::vector<void*> allocs;
   std::vector<void*> host_allocs;   // pinned, mapped host store (kv_host)
+  std::vector<std::pair<void*, size_t>> host_regs;   // the same, mmap'ed + registered in chunks
   // persistent scratch for queries / inserts (grown on demand)
   void* qscratch = nullptr;
   size_t qscratch_bytes = 0;
