@@ -10,6 +10,8 @@
 namespace icb {
 
 __device__ unsigned long long g_search_prof[kPhases];
+__device__ unsigned long long g_cta_cycles[4096];
+__device__ int g_cta_sm[4096];
 
 struct QueryArgs {
   const int32_t* trees;
@@ -227,6 +229,13 @@ __global__ void __launch_bounds__(NT, 512 / NT) query_kernel(ForestView F, Query
     }
     if (A.P.prof && threadIdx.x == 0) atomicAdd(A.P.prof + 8, (unsigned long long)(clock64() - ta));
   }
+  if (A.P.prof && threadIdx.x == 0 && b < 4096) {
+    // per-CTA span and SM (profiling: the skew between trees)
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_cta_cycles[b] += (unsigned long long)(clock64() - tk0);
+    g_cta_sm[b] = (int)smid;
+  }
 }
 
 }  // namespace icb
@@ -237,6 +246,17 @@ using namespace icb;
 // in the public header): out[0..kPhases) = loop, union, scan + row list,
 // lift + start, stream, P-DCI + counters, selection, final top-k + pages,
 // fused attention; out[kPhases..kPhases + 8) = selection statistics.
+extern "C" int icb_search_cta_profile(unsigned long long* cycles, int* sm, int n, int reset) {
+  ICB_CUDA(cudaDeviceSynchronize());
+  ICB_CUDA(cudaMemcpyFromSymbol(cycles, g_cta_cycles, sizeof(unsigned long long) * n));
+  ICB_CUDA(cudaMemcpyFromSymbol(sm, g_cta_sm, sizeof(int) * n));
+  if (reset) {
+    static unsigned long long z[4096] = {};
+    ICB_CUDA(cudaMemcpyToSymbol(g_cta_cycles, z, sizeof(z)));
+  }
+  return ICB_OK;
+}
+
 extern "C" int icb_search_profile(unsigned long long* out, int reset) {
   ICB_CUDA(cudaDeviceSynchronize());
   ICB_CUDA(cudaMemcpyFromSymbol(out, g_search_prof, sizeof(unsigned long long) * kPhases));

@@ -613,12 +613,16 @@ __device__ int group_topb(GroupSmem& GS, unsigned char* rg, int gtid, int bar, c
   const int shift = nbits > NBB ? nbits - NBB : 0;
   for (int i = gtid; i < NB; i += NTG) hist[i] = 0;
   gsync(bar, NTG);
-  for (int i0 = gtid; i0 < Mpad; i0 += U * NTG) {
-    unsigned hb[U];
+  // histogram pass: only the keys' high (d2) words, 2U loads in flight
+  const unsigned* khi = reinterpret_cast<const unsigned*>(keys) + 1;
+  constexpr int U2 = 2 * U;
+  const int Mpad2 = (M + U2 * NTG - 1) / (U2 * NTG) * (U2 * NTG);
+  for (int i0 = gtid; i0 < Mpad2; i0 += U2 * NTG) {
+    unsigned hb[U2];
 #pragma unroll
-    for (int u = 0; u < U; ++u) hb[u] = i0 + u * NTG < M ? (unsigned)(keys[i0 + u * NTG] >> 32) : 0u;
+    for (int u = 0; u < U2; ++u) hb[u] = i0 + u * NTG < M ? khi[2 * (size_t)(i0 + u * NTG)] : 0u;
 #pragma unroll
-    for (int u = 0; u < U; ++u)
+    for (int u = 0; u < U2; ++u)
       if (i0 + u * NTG < M) {
         ICB_CHECK(hb[u] >= lo && hb[u] <= hi, "hb %u outside [%u, %u]", hb[u], lo, hi);
         atomicAdd(&hist[(hb[u] - lo) >> shift], 1);

@@ -36,3 +36,16 @@ tot = buf.sum()
 per_cta_us = buf / (8 * eng.T) / 1.9e3
 for n, v, u in zip(names, buf, per_cta_us):
     print(f"{n:10s} {v / tot * 100:5.1f}%  {u:8.1f} us per CTA-query")
+
+# per-CTA spans (the kernel ends with the slowest tree): solo vs shared SMs
+cyc = np.zeros(eng.T, dtype=np.uint64)
+smi = np.zeros(eng.T, dtype=np.int32)
+lib.icb_search_cta_profile.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+lib.icb_search_cta_profile(cyc.ctypes.data_as(ctypes.c_void_p), smi.ctypes.data_as(ctypes.c_void_p), eng.T, 1)
+us = cyc / 12 / 1.9e3   # all 12 steps of the run
+cnt = np.bincount(smi, minlength=148)
+shared = cnt[smi] > 1
+print("per-CTA us: mean %.1f p50 %.1f p90 %.1f max %.1f | solo SMs %d CTAs mean %.1f max %.1f | shared mean %.1f max %.1f" % (
+    us.mean(), np.median(us), np.percentile(us, 90), us.max(), (~shared).sum(), us[~shared].mean(), us[~shared].max(),
+    us[shared].mean(), us[shared].max()))
+print("blocks on solo SMs:", sorted(np.flatnonzero(~shared).tolist())[:60])
