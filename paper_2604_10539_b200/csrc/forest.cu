@@ -235,7 +235,6 @@ int icb_forest_destroy(icb_forest* f) {
     munmap(r.first, r.second);
   }
   if (f->qscratch) cudaFree(f->qscratch);
-  if (f->ord_buf) cudaFree(f->ord_buf);
   if (f->iscratch) cudaFree(f->iscratch);
   if (f->ascratch) cudaFree(f->ascratch);
   delete f;

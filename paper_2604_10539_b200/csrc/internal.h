@@ -42,9 +42,6 @@ struct icb_forest {
   void* iscratch = nullptr;   // insert-path scratch (separate: mark arrays must stay zero)
   size_t iscratch_bytes = 0;
   void* ascratch = nullptr;   // attention split-K partials
-  void* ord_buf = nullptr;    // fused-decode placement: cost / smmap / order (search.cu placement)
-  int ord_cap = 0, ord_n = 0;
-  const int32_t* ord_trees = nullptr;
   size_t ascratch_bytes = 0;
 };
 

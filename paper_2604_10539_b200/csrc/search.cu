@@ -30,11 +30,6 @@ struct QueryArgs {
   int scalar_bytes;
   float scale_log2;
   int attn_simt;              // 1: CUDA-core attention chunks (ICB_ATTN_SIMT=1, A/B), else tensor cores when possible
-  // cost-aware placement (fused decode step, > 148 trees): CTA blockIdx.x
-  // works on row order[blockIdx.x]; each CTA records its row's span and its SM
-  const int* order;
-  int* cost;                  // [n] by row: last span (clock cycles / 16)
-  int* smmap;                 // [n] by blockIdx.x: SM the CTA ran on
   // fused decode-step prologue (icb_step_attend, the STEP kernel variant):
   // rotate the oldest window page into the tree (if rotate), then append the
   // decode token to the window, then search + attend
@@ -71,9 +66,8 @@ __global__ void __launch_bounds__(NT, 512 / NT) query_kernel(ForestView F, Query
   __shared__ SearchSmem S;
   extern __shared__ __align__(128) unsigned char dsm[];
   GroupSmem* GSA = reinterpret_cast<GroupSmem*>(dsm);
-  const int b = A.order ? A.order[blockIdx.x] : blockIdx.x;
+  const int b = blockIdx.x;
   const int t = A.trees[b];
-  const long long t_entry = clock64();
   if constexpr (STEP) {
     // this tree's rotation and window append, in Engine.decode_step order,
     // before its search: the step's slowest rotation no longer gates every
@@ -235,12 +229,6 @@ __global__ void __launch_bounds__(NT, 512 / NT) query_kernel(ForestView F, Query
     }
     if (A.P.prof && threadIdx.x == 0) atomicAdd(A.P.prof + 8, (unsigned long long)(clock64() - ta));
   }
-  if (A.cost && threadIdx.x == 0) {
-    unsigned smid;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    A.cost[b] = (int)min((clock64() - t_entry) >> 4, (long long)0x7fffffff);
-    A.smmap[blockIdx.x] = (int)smid;
-  }
   if (A.P.prof && threadIdx.x == 0 && b < 4096) {
     // per-CTA span and SM (profiling: the skew between trees)
     unsigned smid;
@@ -307,93 +295,6 @@ int ensure_query_scratch(icb_forest* f, int n, int G, cudaStream_t st, char** ou
 
 int ensure_insert_scratch(icb_forest* f, int n, char** out, SlotLayout* lay);   // insert.cu
 
-namespace icb {
-// Placement of the next fused decode launch (> 148 trees, so 2 CTAs share
-// some SMs): per-tree spans are stable step to step (correlation ~0.9), and
-// the block -> SM map of a launch is fixed.  The heaviest trees go to the
-// blocks that ran alone on an SM; the rest pair heaviest with lightest on the
-// shared SMs.  Identity when the last launch's map is unknown or unusual.
-constexpr int kOrderMax = 2048;
-__global__ void __launch_bounds__(1024) order_kernel(const int* cost, const int* smmap, int* order, int n) {
-  __shared__ unsigned long long key[kOrderMax];
-  __shared__ int cnt[256], first[256], second[256];
-  __shared__ int solo[kOrderMax], pa[kOrderMax / 2], pb[kOrderMax / 2];
-  __shared__ int nsolo, npair, bad;
-  const int tid = threadIdx.x;
-  for (int i = tid; i < 256; i += blockDim.x) { cnt[i] = 0; first[i] = -1; second[i] = -1; }
-  if (tid == 0) { nsolo = 0; npair = 0; bad = 0; }
-  __syncthreads();
-  for (int blk = tid; blk < n; blk += blockDim.x) {
-    const int sm = smmap[blk];
-    if (sm < 0 || sm >= 256) { bad = 1; continue; }
-    const int c = atomicAdd(&cnt[sm], 1);
-    if (c == 0) first[sm] = blk;
-    else if (c == 1) second[sm] = blk;
-    else bad = 1;
-  }
-  __syncthreads();
-  if (tid == 0 && !bad) {
-    for (int sm = 0; sm < 256; ++sm) {
-      if (cnt[sm] == 1) solo[nsolo++] = first[sm];
-      else if (cnt[sm] == 2) { pa[npair] = min(first[sm], second[sm]); pb[npair] = max(first[sm], second[sm]); ++npair; }
-    }
-    if (nsolo + 2 * npair != n) bad = 1;
-  }
-  __syncthreads();
-  if (bad) {
-    for (int i = tid; i < n; i += blockDim.x) order[i] = i;
-    return;
-  }
-  int n2 = 1;
-  while (n2 < n) n2 <<= 1;
-  for (int i = tid; i < n2; i += blockDim.x)   // descending span, ties by row
-    key[i] = i < n ? ((unsigned long long)(0x7fffffffu - (unsigned)cost[i]) << 32) | (unsigned)i : ~0ull;
-  __syncthreads();
-  for (int size = 2; size <= n2; size <<= 1)
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = tid; i < (n2 >> 1); i += blockDim.x) {
-        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
-        const unsigned long long a = key[lo], c = key[hi];
-        if ((a > c) == ((lo & size) == 0)) { key[lo] = c; key[hi] = a; }
-      }
-      __syncthreads();
-    }
-  const int ns = nsolo, np = npair;
-  for (int i = tid; i < ns; i += blockDim.x) order[solo[i]] = (int)(unsigned)key[i];
-  for (int i = tid; i < np; i += blockDim.x) {
-    order[pa[i]] = (int)(unsigned)key[ns + i];
-    order[pb[i]] = (int)(unsigned)key[n - 1 - i];
-  }
-}
-}  // namespace icb
-
-// Placement state of the fused decode launch over `trees` (reset when the
-// tree list changes).
-static int placement(icb_forest* f, const int32_t* trees, int n, cudaStream_t st, int** order, int** cost,
-                     int** smmap) {
-  if (n <= 148 || n > kOrderMax || getenv("ICB_NO_ORDER")) return ICB_OK;
-  if (f->ord_cap < n) {
-    if (f->ord_buf) ICB_CUDA(cudaFree(f->ord_buf));
-    f->ord_buf = nullptr;
-    ICB_CUDA(cudaMalloc(&f->ord_buf, sizeof(int) * 3 * (size_t)n));
-    f->ord_cap = n;
-    f->ord_trees = nullptr;
-  }
-  int* ob = (int*)f->ord_buf;
-  if (f->ord_trees != trees || f->ord_n != n) {
-    ICB_CUDA(cudaMemsetAsync(ob, 0, sizeof(int) * n, st));                       // cost
-    ICB_CUDA(cudaMemsetAsync(ob + n, 0xff, sizeof(int) * n, st));                // smmap unknown
-    f->ord_trees = trees;
-    f->ord_n = n;
-  }
-  *cost = ob;
-  *smmap = ob + n;
-  *order = ob + 2 * n;
-  order_kernel<<<1, 1024, 0, st>>>(*cost, *smmap, *order, n);
-  ICB_CUDA(cudaGetLastError());
-  return ICB_OK;
-}
-
 int icb_query_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, const float* queries,
                    int32_t lifted_input, int32_t k, int64_t beam, int64_t visit_cap, int32_t target_level,
                    int32_t* out_ids, int32_t k_out, int32_t* out_counts, int32_t* out_pages,
@@ -431,11 +332,6 @@ int icb_query_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t G, co
   A.attn_out = attn_out; A.attn_stats = attn_stats; A.scalar_bytes = scalar_bytes;
   A.scale_log2 = (float)(1.4426950408889634 / sqrt((double)f->cfg.dim));
   A.attn_simt = getenv("ICB_ATTN_SIMT") != nullptr;
-  if (attn_out && !step) {
-    int *ord = nullptr, *cst = nullptr, *smm = nullptr;
-    if (int rc2 = placement(f, trees, n, st, &ord, &cst, &smm)) return rc2;
-    A.order = ord; A.cost = cst; A.smmap = smm;
-  }
   if (step) {
     A.rotate = step->rotate;
     if (step->rotate && (rc = ensure_insert_scratch(f, n, &A.rot_scratch, &A.rot_SL))) return rc;
