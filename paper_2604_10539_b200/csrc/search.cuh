@@ -251,11 +251,10 @@ __device__ void block_sort(SearchSmem& S, int n) {
 // barrier 1 + group.
 constexpr int kBins = 1024;
 constexpr int kBuf = 512;
-#ifndef ICB_STREAM_TMA
-#define ICB_STREAM_TMA 0   // 1: TMA bulk copies + mbarriers; 0: cp.async (measured faster)
-#endif
+// The row stream uses cp.async rings (a TMA bulk-copy ring measured slower for
+// 512-B rows and was removed).
 constexpr int kSub = 16;                             // ring slots per warp (2 batches of 8 rows)
-constexpr int kRing = (kSearchThreads / 32) * kSub;  // 256 slots x 528 B = 135 KB
+constexpr int kRing = (kSearchThreads / 32) * kSub;  // 128 slots x 512 B = 64 KB (+ 2 mbarriers each)
 
 struct GroupSmem {
   int hist[kBins];
