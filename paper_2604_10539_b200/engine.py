@@ -190,14 +190,58 @@ class Engine:
         if n_prefill < 1:
             raise ConfigError("prefill needs at least one token")
         cfg = self.cfg
-        dev = self.device
         # device tensors keep their dtype (an fp32 / bf16 stream is converted per
         # chunk of layers, never materialised whole in fp32); numpy / host -> fp32
-        keys = _on_device(keys[:n_prefill], dev)
-        values = _on_device(values[:n_prefill], dev)
+        keys = _on_device(keys[:n_prefill], self.device)
+        values = _on_device(values[:n_prefill], self.device)
         if tuple(keys.shape[1:]) != (cfg.layers, cfg.kv_heads, cfg.d) or \
                 tuple(values.shape[1:]) != (cfg.layers, cfg.kv_heads, cfg.d_prime):
             raise ConfigError("workload dims do not match the engine config")
+        geo = self._prefill_begin(n_prefill)
+        for layer in range(cfg.layers):
+            self._store_layer(layer, keys[:, layer], values[:, layer])
+        if not self.fallback:
+            try:
+                self._new_forest(geo, tight=True)
+                self._build_layers(geo, cfg.skip_layers, cfg.layers, keys[:, cfg.skip_layers:],
+                                   values[:, cfg.skip_layers:])
+                self.forest.check()
+            except ConfigError as e:
+                if "page capacity" not in str(e):
+                    raise
+                # the trees outgrew the tight page estimate: rebuild at the worst case
+                self.forest.close()
+                self._new_forest(geo, tight=False)
+                self._build_layers(geo, cfg.skip_layers, cfg.layers, keys[:, cfg.skip_layers:],
+                                   values[:, cfg.skip_layers:])
+                self.forest.check()
+        return self._prefill_end()
+
+    def prefill_layers(self, n_prefill: int) -> "LayerPrefill":
+        """Layer-streaming prefill: hand each layer's prompt K/V to the engine
+        as the model produces it; that layer's trees build on the engine's own
+        CUDA stream while the caller computes the next layer (the pipelined
+        prefill of PAPER.md:245-249 / engine.py:587-604, here real overlap on
+        the device).  Same trees as prefill(keys, values, n).
+
+            with torch.no_grad():
+                pf = eng.prefill_layers(n)
+                for layer in range(L):
+                    k, v = ...            # [n, kv_heads, d] / [n, kv_heads, d'] on the device
+                    pf.layer(layer, k, v)
+                pf.finish()
+        """
+        if self.prefilled:
+            raise ConfigError("engine already prefilled")
+        if n_prefill < 1:
+            raise ConfigError("prefill needs at least one token")
+        return LayerPrefill(self, n_prefill)
+
+    def _prefill_begin(self, n_prefill):
+        """Shapes, dense / evaluation mirrors and the page layout of a prefill
+        of n_prefill tokens (engine.py:240-276); returns the sink / window
+        geometry."""
+        cfg, dev = self.cfg, self.device
         self.n_prefill = n_prefill
         self.max_tokens = cfg.max_tokens or (n_prefill + 1024)
         s = cfg.page_size
@@ -215,80 +259,69 @@ class Engine:
             self._mk = torch.zeros((cfg.layers, cfg.kv_heads, self.max_tokens, cfg.d), dtype=torch.float32, device=dev)
             self._mv = torch.zeros((cfg.layers, cfg.kv_heads, self.max_tokens, cfg.d_prime), dtype=torch.float32,
                                    device=dev)
-            self._mk[:, :, :n_prefill] = keys.permute(1, 2, 0, 3).float()
-            self._mv[:, :, :n_prefill] = values.permute(1, 2, 0, 3).float()
             self._indexed_mask = torch.zeros(self.max_tokens, dtype=torch.bool, device=dev)
         self._dense_res = torch.empty((max(nd, 1), cfg.query_heads_per_group, cfg.d_prime), dtype=torch.float32,
                                       device=dev)   # dense attention output (nd planes)
         self.dense_k = torch.zeros((max(nd, 1), self.max_tokens, dpad), dtype=kvt, device=dev)
         self.dense_v = torch.zeros((max(nd, 1), self.max_tokens, dvpad), dtype=kvt, device=dev)
-        if nd:
-            k = keys[:, : self.n_dense].permute(1, 2, 0, 3).reshape(nd, n_prefill, cfg.d)
-            v = values[:, : self.n_dense].permute(1, 2, 0, 3).reshape(nd, n_prefill, cfg.d_prime)
-            self.dense_k[:, :n_prefill, : cfg.d] = k.to(kvt)
-            self.dense_v[:, :n_prefill, : cfg.d_prime] = v.to(kvt)
         if self.fallback:
-            self.prefilled = True
-            return self
+            return None
         sink_end = cfg.sink_pages * s
         win_start = (pages - cfg.window_pages) * s
         self.sink_tokens = list(range(sink_end))
         self.indexed_tokens = list(range(sink_end, win_start))
         if cfg.evaluate:
             self._indexed_mask[sink_end:win_start] = True
-        Li = cfg.layers - cfg.skip_layers
-        H = cfg.kv_heads
-        T = Li * H
-        self.T = T
+        self.T = (cfg.layers - cfg.skip_layers) * cfg.kv_heads
         # KV offload: the pool holds a step's sink, window and largest selection
         pool = (cfg.query_heads_per_group * min(cfg.token_budget, self.max_tokens) + cfg.sink_pages
                 + cfg.window_pages + 2)
-        self.trees_dev = torch.arange(T, dtype=torch.int32, device=dev)
+        self.trees_dev = torch.arange(self.T, dtype=torch.int32, device=dev)
         self._win_fills = [min(s, max(0, (n_prefill - win_start) - i * s)) for i in range(cfg.window_pages)]
         self._win_start = [win_start + i * s for i in range(cfg.window_pages)]
-        try:
-            self._build_forest(keys, values, n_prefill, sink_end, win_start, pool, tight=True)
-        except ConfigError as e:
-            if "page capacity" not in str(e):
-                raise
-            # the trees outgrew the tight page estimate: rebuild at the worst case
-            self.forest.close()
-            self._build_forest(keys, values, n_prefill, sink_end, win_start, pool, tight=False)
-        f = self.forest
-        k, beam, cap = _budget_tuple(cfg.budget())
-        self.k_eff = int(min(k, self.max_tokens))
-        self.beam, self.visit_cap = int(min(beam, 2**62)), int(min(cap, 2**62))
-        G = cfg.query_heads_per_group
-        self.pages_cap = int(min(f.caps.page_cap, G * self.k_eff))
-        if cfg.reuse_stride >= 2 and cfg.layer_serial:
-            raise ConfigError("reuse_stride is supported with layers batched per step (layer_serial=False)")
-        self._alloc_step_buffers()
-        self.prefilled = True
-        return self
+        return dict(n=n_prefill, sink_end=sink_end, win_start=win_start, pool=pool)
 
-    def _build_forest(self, keys, values, n_prefill, sink_end, win_start, pool, tight):
+    def _store_layer(self, layer, k, v):
+        """One layer's prompt K/V [n, H, d] into the dense mirror (dense
+        layers) and the evaluation mirrors."""
+        cfg = self.cfg
+        n = self.n_prefill
+        if cfg.evaluate:
+            self._mk[layer, :, :n] = k.permute(1, 0, 2).float()
+            self._mv[layer, :, :n] = v.permute(1, 0, 2).float()
+        if layer < self.n_dense:
+            H = cfg.kv_heads
+            self.dense_k[layer * H:(layer + 1) * H, :n, : cfg.d] = k.permute(1, 0, 2).to(self.dense_k.dtype)
+            self.dense_v[layer * H:(layer + 1) * H, :n, : cfg.d_prime] = v.permute(1, 0, 2).to(self.dense_v.dtype)
+
+    def _new_forest(self, geo, tight):
         cfg, dev, T, H, s = self.cfg, self.device, self.T, self.cfg.kv_heads, self.cfg.page_size
-        caps = ForestCaps.for_stream(win_start - sink_end, self.max_tokens - n_prefill, cfg.promotion_ratio, s,
-                                     cfg.sink_pages + cfg.window_pages, tight=tight)
+        caps = ForestCaps.for_stream(geo["win_start"] - geo["sink_end"], self.max_tokens - geo["n"],
+                                     cfg.promotion_ratio, s, cfg.sink_pages + cfg.window_pages, tight=tight)
         caps.tok_cap = self.max_tokens
         self.forest = f = DeviceForest(T, cfg.d, cfg.d_prime, tok_cap=self.max_tokens,
                                        promotion_ratio=cfg.promotion_ratio, page_size=s, kv_dtype=cfg.kv_dtype,
-                                       device=dev, kv_host=cfg.kv_offload, pool_pages=pool if cfg.kv_offload else 0,
-                                       caps=caps)
+                                       device=dev, kv_host=cfg.kv_offload,
+                                       pool_pages=geo["pool"] if cfg.kv_offload else 0, caps=caps)
         trees = list(range(T))
         f.seed(trees, [(cfg.seed, cfg.skip_layers + t // H, t % H) for t in trees])
-        tok = torch.arange(n_prefill, dtype=torch.int32, device=dev)
-        Li = T // H
-        # whole layers per chunk, ~2 GB of fp32 prefill keys + values at a time
-        per_layer = H * n_prefill * (cfg.d + cfg.d_prime) * 4
-        lchunk = max(1, min(Li, (2 << 30) // max(1, per_layer)))
-        for l0 in range(0, Li, lchunk):
-            l1 = min(Li, l0 + lchunk)
-            c0, c1 = l0 * H, l1 * H
+        self._tok_ar = torch.arange(geo["n"], dtype=torch.int32, device=dev)
+
+    def _build_layers(self, geo, la, lb, keys, values):
+        """Trees of indexed layers [la, lb) from their prompt K/V ([n, lb - la,
+        H, d]): sink and window pages, then dci_indexing (engine.py:254-281), in
+        chunks of whole layers (~2 GB of fp32 keys + values at a time)."""
+        cfg, H, f = self.cfg, self.cfg.kv_heads, self.forest
+        n, sink_end, win_start = geo["n"], geo["sink_end"], geo["win_start"]
+        tok = self._tok_ar
+        per_layer = H * n * (cfg.d + cfg.d_prime) * 4
+        lchunk = max(1, min(lb - la, (2 << 30) // max(1, per_layer)))
+        for l0 in range(la, lb, lchunk):
+            l1 = min(lb, l0 + lchunk)
+            c0, c1 = (l0 - cfg.skip_layers) * H, (l1 - cfg.skip_layers) * H
             trs = self.trees_dev[c0:c1]
-            sl = slice(cfg.skip_layers + l0, cfg.skip_layers + l1)
-            ki = keys[:, sl].permute(1, 2, 0, 3).reshape(c1 - c0, n_prefill, cfg.d)
-            vi = values[:, sl].permute(1, 2, 0, 3).reshape(c1 - c0, n_prefill, cfg.d_prime)
+            ki = keys[:, l0 - la:l1 - la].permute(1, 2, 0, 3).reshape(c1 - c0, n, cfg.d)
+            vi = values[:, l0 - la:l1 - la].permute(1, 2, 0, 3).reshape(c1 - c0, n, cfg.d_prime)
             # pages: sink ids 0.., window next, then indexed (engine.py:263-281)
             f.alloc_resident(trs, N.ROLE_SINK, cfg.sink_pages, tok[:sink_end].expand(c1 - c0, -1),
                              ki[:, :sink_end], vi[:, :sink_end])
@@ -297,7 +330,21 @@ class Engine:
             f.build(trs, tok[sink_end:win_start].expand(c1 - c0, -1), ki[:, sink_end:win_start],
                     vi[:, sink_end:win_start])
             del ki, vi
-        f.check()
+
+    def _prefill_end(self):
+        cfg = self.cfg
+        if not self.fallback:
+            f = self.forest
+            k, beam, cap = _budget_tuple(cfg.budget())
+            self.k_eff = int(min(k, self.max_tokens))
+            self.beam, self.visit_cap = int(min(beam, 2**62)), int(min(cap, 2**62))
+            G = cfg.query_heads_per_group
+            self.pages_cap = int(min(f.caps.page_cap, G * self.k_eff))
+            if cfg.reuse_stride >= 2 and cfg.layer_serial:
+                raise ConfigError("reuse_stride is supported with layers batched per step (layer_serial=False)")
+            self._alloc_step_buffers()
+        self.prefilled = True
+        return self
 
     def _check_workload(self, workload) -> None:
         """engine.py:216-224."""
@@ -977,3 +1024,63 @@ class _HeadView:
     @property
     def window(self):
         return self._pages(self._eng.forest.export(self._t)["win"])
+
+
+class LayerPrefill:
+    """Engine.prefill_layers(n): the prompt's K/V one layer at a time.  Each
+    layer's work (dense mirror or sink / window pages + dci_indexing of its
+    kv heads) runs on the engine's build stream after the caller's stream
+    reaches the hand-off, so it overlaps whatever the caller launches next.
+    The layer tensors are kept until finish() (a tree set that outgrows the
+    tight page capacities is rebuilt from them)."""
+
+    def __init__(self, eng: Engine, n_prefill: int):
+        self.eng = eng
+        self.geo = eng._prefill_begin(n_prefill)
+        self.stream = torch.cuda.Stream(device=eng.device)
+        self.kept: dict[int, tuple] = {}
+        if self.geo is not None:
+            with torch.cuda.stream(self.stream):
+                eng._new_forest(self.geo, tight=True)
+            self.stream.synchronize()
+
+    def layer(self, layer: int, keys, values) -> None:
+        """keys [n, kv_heads, d], values [n, kv_heads, d'] (device tensors; the
+        first n_prefill rows are read)."""
+        eng, cfg = self.eng, self.eng.cfg
+        if not 0 <= layer < cfg.layers or layer in self.kept:
+            raise InputError(f"layer {layer} outside [0, {cfg.layers}) or given twice")
+        n = eng.n_prefill
+        k = _on_device(keys[:n], eng.device)
+        v = _on_device(values[:n], eng.device)
+        if tuple(k.shape[1:]) != (cfg.kv_heads, cfg.d) or tuple(v.shape[1:]) != (cfg.kv_heads, cfg.d_prime):
+            raise ConfigError("layer K/V dims do not match the engine config")
+        ready = torch.cuda.Event()
+        ready.record(torch.cuda.current_stream(eng.device))
+        self.stream.wait_event(ready)
+        self.kept[layer] = (k, v)
+        with torch.cuda.stream(self.stream):
+            eng._store_layer(layer, k, v)
+            if self.geo is not None and layer >= cfg.skip_layers:
+                eng._build_layers(self.geo, layer, layer + 1, k[:, None], v[:, None])
+
+    def finish(self) -> Engine:
+        eng, cfg = self.eng, self.eng.cfg
+        if len(self.kept) != cfg.layers:
+            raise InputError(f"prefill got {len(self.kept)} of {cfg.layers} layers")
+        torch.cuda.current_stream(eng.device).wait_stream(self.stream)
+        self.stream.synchronize()
+        if self.geo is not None:
+            try:
+                eng.forest.check()
+            except ConfigError as e:
+                if "page capacity" not in str(e):
+                    raise
+                eng.forest.close()
+                eng._new_forest(self.geo, tight=False)
+                for layer in range(cfg.skip_layers, cfg.layers):
+                    k, v = self.kept[layer]
+                    eng._build_layers(self.geo, layer, layer + 1, k[:, None], v[:, None])
+                eng.forest.check()
+        self.kept.clear()
+        return eng._prefill_end()

@@ -159,6 +159,38 @@ def make_engine_goldens(only=None):
         print("engine", name, rows[0], rows[-1])
 
 
+def make_llama_golden():
+    """The reference engine on q/k/v from a (random-init) Llama forward:
+    tests/golden/llama_small.icet, written by tools/llama_trace.py."""
+    from icecache.workload import load_trace
+    wl = load_trace(os.path.join(OUT, "llama_small.icet"))
+    sp = wl.spec
+    cfg = ic.EngineConfig(layers=sp.layers, kv_heads=sp.kv_heads, query_heads_per_group=sp.query_heads_per_group,
+                          d=sp.d, d_prime=sp.d_prime, token_budget=32, skip_layers=1, evaluate=True, seed=5)
+    n_prefill, steps = 600, 100
+    eng = ic.Engine(cfg).prefill(wl, n_prefill)
+    tok_log = []
+    orig = eng._select_tokens
+
+    def spy(q, layer, kv_head, budget=None):
+        res = orig(q, layer, kv_head, budget)
+        tok_log[-1].append([layer, kv_head, list(map(int, res))])
+        return res
+    eng._select_tokens = spy
+    rows, outs = [], []
+    for t in range(steps):
+        tok_log.append([])
+        o, m = eng.decode_step(wl.decode_step(n_prefill, t))
+        rows.append(m.__dict__)
+        outs.append(np.stack([[o[l][qh].value_out for qh in range(cfg.n_query_heads)] for l in range(cfg.layers)]))
+    meta = dict(name="llama", trace="llama_small.icet", cfg=dict(token_budget=32, skip_layers=1, evaluate=True,
+                                                                 seed=5),
+                n_prefill=n_prefill, steps=steps, rows=rows, tokens=tok_log)
+    np.savez_compressed(os.path.join(OUT, "engine_llama.npz"), outputs=np.stack(outs).astype(np.float64),
+                        meta=json.dumps(meta))
+    print("engine llama", rows[0], rows[-1])
+
+
 def make_trace_golden():
     """An ICET trace written by the reference's save_trace (workload.py:175-192)
     and the arrays its load_trace (:195-224) returns."""
@@ -176,10 +208,13 @@ def make_trace_golden():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["tree", "engine", "trace"]
+    which = sys.argv[1:] or ["tree", "engine", "trace", "llama"]
+    if "llama" in which:
+        make_llama_golden()
+        which = [w for w in which if w != "llama"] if len(which) > 1 else []
     if "tree" in which:
         make_tree_goldens()
     if "trace" in which:
         make_trace_golden()
     if "engine" in which:
-        make_engine_goldens([w for w in which if w not in ("tree", "engine", "trace")] or None)
+        make_engine_goldens([w for w in which if w not in ("tree", "engine", "trace", "llama")] or None)

@@ -256,3 +256,74 @@ def test_kv_offload_matches_resident(cuda_ok, kv, reuse):
     fixed = off.cfg.sink_pages + off.cfg.window_pages
     assert (ps[:, 1] == n_sel + fixed).all()
     assert ps[:, 0].sum() > 0
+
+
+def test_layer_streaming_prefill_matches_batched(cuda_ok):
+    """Engine.prefill_layers (each layer's trees built on the engine's stream as
+    its K/V arrive) builds the same trees as prefill(keys, values, n): equal
+    exports, bit-identical decode outputs and selections."""
+    import torch
+    from paper_2604_10539_b200.engine import Engine, EngineConfig
+    sk = dict(n_tokens=2048 + 40, d=64, d_prime=32, clusters=16, layers=5, kv_heads=2, query_heads_per_group=2,
+              seed=21)
+    keys, values, queries, _ = generate(Spec(kind="clustered", **sk))
+    shape = dict(layers=5, kv_heads=2, query_heads_per_group=2, d=64, d_prime=32, seed=21)
+    cfg = dict(token_budget=32, skip_layers=2, kv_dtype="bf16", max_tokens=2048 + 40)
+    a = Engine(EngineConfig(**shape, **cfg)).prefill(keys, values, 2048)
+    b = Engine(EngineConfig(**shape, **cfg))
+    k = torch.as_tensor(keys, dtype=torch.float32, device="cuda")
+    v = torch.as_tensor(values, dtype=torch.float32, device="cuda")
+    pf = b.prefill_layers(2048)
+    for layer in range(5):
+        pf.layer(layer, k[:, layer] * 1.0, v[:, layer] * 1.0)   # fresh tensors, as a model would hand over
+    pf.finish()
+    for tr in range(a.T):
+        ea, eb = a.forest.export(tr), b.forest.export(tr)
+        assert ea["nodes"] == eb["nodes"] and ea["pages"] == eb["pages"], tr
+    for t in range(40):
+        tok = 2048 + t
+        oa, _ = a.decode_step(tok, queries[tok], keys[tok], values[tok])
+        ob, _ = b.decode_step(tok, queries[tok], keys[tok], values[tok])
+        assert torch.equal(oa, ob), t
+
+
+def test_engine_on_llama_qkv_matches_reference(cuda_ok):
+    """q/k/v from a Llama forward (tools/llama_trace.py: transformers'
+    LlamaForCausalLM, random init, post-RoPE q/k/v captured by an attention
+    hook, stored in the reference's ICET trace format): the device engine
+    against the oracle (ranked lists and pages bit-exact) and the reference's
+    own run on the same trace (step metrics, evaluation metrics, outputs)."""
+    import os
+    from paper_2604_10539_b200.engine import Engine, EngineConfig
+    from paper_2604_10539_b200.trace import load_trace
+    z, meta = load_golden("engine_llama.npz")
+    tr = load_trace(os.path.join(os.path.dirname(__file__), "golden", meta["trace"]))
+    keys, values, queries = (tr.keys.astype(np.float64), tr.values.astype(np.float64), tr.queries.astype(np.float64))
+    shape = dict(layers=tr.layers, kv_heads=tr.kv_heads, query_heads_per_group=tr.query_heads_per_group, d=tr.d,
+                 d_prime=tr.d_prime)
+    ck = meta["cfg"]
+    n0 = meta["n_prefill"]
+    oeng = OracleEngine(OConfig(**shape, token_budget=ck["token_budget"], skip_layers=ck["skip_layers"],
+                                seed=ck["seed"])).prefill(keys, values, n0)
+    eng = Engine(EngineConfig(**shape, **ck, kv_dtype="fp32", max_tokens=tr.n_tokens)).prefill(keys, values, n0)
+    G, H = tr.query_heads_per_group, tr.kv_heads
+    for t in range(meta["steps"]):
+        tok = n0 + t
+        oout, om, trace = oeng.decode_step(tok, queries[tok], keys[tok], values[tok])
+        out, m = eng.decode_step(tok, queries[tok], keys[tok], values[tok])
+        row = meta["rows"][t]
+        for k in KEYS:
+            assert getattr(m, k) == om[k] == row[k], (t, k)
+        assert abs(m.recall_at_k - row["recall_at_k"]) <= 1e-9, t
+        assert abs(m.page_hit_rate - row["page_hit_rate"]) <= 1e-9, t
+        assert abs(m.covered_attention_mass - row["covered_attention_mass"]) < 1e-6, t
+        ids, counts, pages, npages = eng.selected()
+        for layer in range(ck["skip_layers"], tr.layers):
+            for h in range(H):
+                trx = (layer - ck["skip_layers"]) * H + h
+                for g in range(G):
+                    assert list(ids[trx, g, :counts[trx, g]]) == trace["tokens"][(layer, h * G + g)], (t, layer, h, g)
+                assert list(pages[trx, :npages[trx]]) == trace["pages"][(layer, h)], (t, layer, h)
+        ref = z["outputs"][t]
+        o = out.cpu().numpy()
+        assert (np.linalg.norm(o - ref, axis=-1) / np.linalg.norm(ref, axis=-1)).max() < 1e-3, t

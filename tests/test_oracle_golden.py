@@ -140,3 +140,28 @@ def test_engine_matches_reference(name):
         ref_out = z["outputs"][t]
         err = np.linalg.norm(out - ref_out, axis=-1) / np.linalg.norm(ref_out, axis=-1)
         assert err.max() < 1e-10
+
+
+def test_oracle_engine_on_llama_trace_matches_reference():
+    """The oracle on the Llama-forward trace (tools/llama_trace.py) against the
+    reference's own run: step metrics and per-head token sets."""
+    import os
+    from paper_2604_10539_b200.trace import load_trace
+    z, meta = load_golden("engine_llama.npz")
+    tr = load_trace(os.path.join(os.path.dirname(__file__), "golden", meta["trace"]))
+    keys, values, queries = (tr.keys.astype(np.float64), tr.values.astype(np.float64), tr.queries.astype(np.float64))
+    ck = meta["cfg"]
+    cfg = OConfig(layers=tr.layers, kv_heads=tr.kv_heads, query_heads_per_group=tr.query_heads_per_group, d=tr.d,
+                  d_prime=tr.d_prime, token_budget=ck["token_budget"], skip_layers=ck["skip_layers"], seed=ck["seed"])
+    n0 = meta["n_prefill"]
+    eng = OracleEngine(cfg).prefill(keys, values, n0)
+    G = cfg.query_heads_per_group
+    for t in range(meta["steps"]):
+        tok = n0 + t
+        _, m, trace = eng.decode_step(tok, queries[tok], keys[tok], values[tok])
+        for key in ("pages_selected", "pages_loaded", "tokens_loaded", "bytes_moved", "transactions", "dci_queries"):
+            assert m[key] == meta["rows"][t][key], (t, key)
+        calls = meta["tokens"][t]
+        for i, (layer, h, want) in enumerate(calls):
+            g = i % G
+            assert set(trace["tokens"][(layer, h * G + g)]) == set(want), (t, layer, h, g)
