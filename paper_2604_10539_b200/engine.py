@@ -1037,7 +1037,9 @@ class LayerPrefill:
     def __init__(self, eng: Engine, n_prefill: int):
         self.eng = eng
         self.geo = eng._prefill_begin(n_prefill)
-        self.stream = torch.cuda.Stream(device=eng.device)
+        # high priority: the build's small launches take SMs as the model's
+        # kernels release them instead of queueing behind whole GEMM waves
+        self.stream = torch.cuda.Stream(device=eng.device, priority=-1)
         self.kept: dict[int, tuple] = {}
         if self.geo is not None:
             with torch.cuda.stream(self.stream):
