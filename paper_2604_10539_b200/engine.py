@@ -217,7 +217,7 @@ class Engine:
                 self.forest.check()
         return self._prefill_end()
 
-    def prefill_layers(self, n_prefill: int) -> "LayerPrefill":
+    def prefill_layers(self, n_prefill: int, group: int = 4) -> "LayerPrefill":
         """Layer-streaming prefill: hand each layer's prompt K/V to the engine
         as the model produces it; that layer's trees build on the engine's own
         CUDA stream while the caller computes the next layer (the pipelined
@@ -235,7 +235,7 @@ class Engine:
             raise ConfigError("engine already prefilled")
         if n_prefill < 1:
             raise ConfigError("prefill needs at least one token")
-        return LayerPrefill(self, n_prefill)
+        return LayerPrefill(self, n_prefill, group)
 
     def _prefill_begin(self, n_prefill):
         """Shapes, dense / evaluation mirrors and the page layout of a prefill
@@ -1034,8 +1034,10 @@ class LayerPrefill:
     The layer tensors are kept until finish() (a tree set that outgrows the
     tight page capacities is rebuilt from them)."""
 
-    def __init__(self, eng: Engine, n_prefill: int):
+    def __init__(self, eng: Engine, n_prefill: int, group: int = 4):
         self.eng = eng
+        self.group = max(1, int(group))   # indexed layers per build launch (batched trees build faster)
+        self.pending: list[int] = []
         self.geo = eng._prefill_begin(n_prefill)
         # high priority: the build's small launches take SMs as the model's
         # kernels release them instead of queueing behind whole GEMM waves
@@ -1063,13 +1065,34 @@ class LayerPrefill:
         self.kept[layer] = (k, v)
         with torch.cuda.stream(self.stream):
             eng._store_layer(layer, k, v)
-            if self.geo is not None and layer >= cfg.skip_layers:
-                eng._build_layers(self.geo, layer, layer + 1, k[:, None], v[:, None])
+        if self.geo is not None and layer >= cfg.skip_layers:
+            self.pending.append(layer)
+            if len(self.pending) >= self.group:
+                self._flush()
+
+    def _flush(self) -> None:
+        """Build the pending layers' trees in one launch sequence (runs of
+        consecutive layers)."""
+        eng = self.eng
+        runs: list[list[int]] = []
+        for layer in sorted(self.pending):
+            if runs and layer == runs[-1][-1] + 1:
+                runs[-1].append(layer)
+            else:
+                runs.append([layer])
+        self.pending = []
+        with torch.cuda.stream(self.stream):
+            for run in runs:
+                ks = torch.stack([self.kept[l][0] for l in run], 1)
+                vs = torch.stack([self.kept[l][1] for l in run], 1)
+                eng._build_layers(self.geo, run[0], run[-1] + 1, ks, vs)
 
     def finish(self) -> Engine:
         eng, cfg = self.eng, self.eng.cfg
         if len(self.kept) != cfg.layers:
             raise InputError(f"prefill got {len(self.kept)} of {cfg.layers} layers")
+        if self.pending:
+            self._flush()
         torch.cuda.current_stream(eng.device).wait_stream(self.stream)
         self.stream.synchronize()
         if self.geo is not None:

@@ -26,6 +26,7 @@ from paper_2604_10539_b200.engine import Engine, EngineConfig  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 D = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+GROUP = int(sys.argv[3]) if len(sys.argv) > 3 else 4
 from transformers import AttentionInterface, LlamaConfig, LlamaModel  # noqa: E402
 from transformers.integrations.sdpa_attention import sdpa_attention_forward  # noqa: E402
 
@@ -84,7 +85,7 @@ with torch.no_grad():
     eng2 = Engine(EngineConfig(**ecfg))
 
     def pipelined():
-        state["pf"] = eng2.prefill_layers(n)
+        state["pf"] = eng2.prefill_layers(n, group=GROUP)
         model(input_ids=ids[:, :n], use_cache=False)
         return state["pf"].finish()
     _, pipe_s = timed(pipelined)
@@ -104,6 +105,7 @@ with torch.no_grad():
     tpot = e0.elapsed_time(e1) / (D - 4)
 print(json.dumps({
     "model": "Llama-3.1-8B-shaped LlamaModel, random init, bf16 (transformers)", "prompt": n,
+    "layers_per_build": GROUP,
     "forward_s": round(fwd_s, 3), "serial_prefill_s": round(fwd_s + build_s, 3),
     "serial_build_s": round(build_s, 3), "pipelined_prefill_s": round(pipe_s, 3),
     "build_hidden_frac": round(1 - (pipe_s - fwd_s) / max(build_s, 1e-9), 3),
