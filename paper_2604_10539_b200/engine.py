@@ -1051,7 +1051,6 @@ class LayerPrefill:
             with torch.cuda.stream(self.stream):
                 eng._new_forest(self.geo, tight=True)
             self.stream.synchronize()
-        self.dev_index = eng.device.index if eng.device.index is not None else torch.cuda.current_device()
         self.q: "queue.Queue" = queue.Queue()
         self.error: BaseException | None = None
         self.worker = threading.Thread(target=self._work, daemon=True)
@@ -1075,10 +1074,7 @@ class LayerPrefill:
 
     def _work(self) -> None:
         eng, cfg = self.eng, self.eng.cfg
-        try:
-            torch.cuda.set_device(self.dev_index)
-        except BaseException as e:   # reported by finish()
-            self.error = e
+        torch.cuda.set_device(eng.device)
         while True:
             item = self.q.get()
             if item is None:
