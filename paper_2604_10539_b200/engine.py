@@ -1029,16 +1029,12 @@ class _HeadView:
 class LayerPrefill:
     """Engine.prefill_layers(n): the prompt's K/V one layer at a time.  Each
     layer's work (dense mirror or sink / window pages + dci_indexing of its
-    kv heads, `group` indexed layers per build) runs on the engine's build
-    stream, issued by a worker thread, after the caller's stream reaches the
-    hand-off -- so neither the device work nor the build's host-side
-    synchronisation holds up what the caller launches next.  The layer tensors
-    are kept until finish() (a tree set that outgrows the tight page
-    capacities is rebuilt from them)."""
+    kv heads) runs on the engine's build stream after the caller's stream
+    reaches the hand-off, so it overlaps whatever the caller launches next.
+    The layer tensors are kept until finish() (a tree set that outgrows the
+    tight page capacities is rebuilt from them)."""
 
     def __init__(self, eng: Engine, n_prefill: int, group: int = 4):
-        import queue
-        import threading
         self.eng = eng
         self.group = max(1, int(group))   # indexed layers per build launch (batched trees build faster)
         self.pending: list[int] = []
@@ -1051,10 +1047,6 @@ class LayerPrefill:
             with torch.cuda.stream(self.stream):
                 eng._new_forest(self.geo, tight=True)
             self.stream.synchronize()
-        self.q: "queue.Queue" = queue.Queue()
-        self.error: BaseException | None = None
-        self.worker = threading.Thread(target=self._work, daemon=True)
-        self.worker.start()
 
     def layer(self, layer: int, keys, values) -> None:
         """keys [n, kv_heads, d], values [n, kv_heads, d'] (device tensors; the
@@ -1069,29 +1061,14 @@ class LayerPrefill:
             raise ConfigError("layer K/V dims do not match the engine config")
         ready = torch.cuda.Event()
         ready.record(torch.cuda.current_stream(eng.device))
+        self.stream.wait_event(ready)
         self.kept[layer] = (k, v)
-        self.q.put((layer, k, v, ready))
-
-    def _work(self) -> None:
-        eng, cfg = self.eng, self.eng.cfg
-        torch.cuda.set_device(eng.device)
-        while True:
-            item = self.q.get()
-            if item is None:
-                return
-            if self.error is not None:
-                continue
-            try:
-                layer, k, v, ready = item
-                self.stream.wait_event(ready)
-                with torch.cuda.stream(self.stream):
-                    eng._store_layer(layer, k, v)
-                if self.geo is not None and layer >= cfg.skip_layers:
-                    self.pending.append(layer)
-                    if len(self.pending) >= self.group:
-                        self._flush()
-            except BaseException as e:   # reported by finish()
-                self.error = e
+        with torch.cuda.stream(self.stream):
+            eng._store_layer(layer, k, v)
+        if self.geo is not None and layer >= cfg.skip_layers:
+            self.pending.append(layer)
+            if len(self.pending) >= self.group:
+                self._flush()
 
     def _flush(self) -> None:
         """Build the pending layers' trees in one launch sequence (runs of
@@ -1112,10 +1089,6 @@ class LayerPrefill:
 
     def finish(self) -> Engine:
         eng, cfg = self.eng, self.eng.cfg
-        self.q.put(None)
-        self.worker.join()
-        if self.error is not None:
-            raise self.error
         if len(self.kept) != cfg.layers:
             raise InputError(f"prefill got {len(self.kept)} of {cfg.layers} layers")
         if self.pending:
