@@ -784,6 +784,17 @@ __global__ void build_entries_kernel(ForestView F, BuildArgs A, const int* top, 
   }
 }
 
+// Total entries on the device (no host round trip): padding entries of the
+// bound-sized arrays hold ~0 keys and sort last.
+__global__ void build_ent_total_kernel(ForestView F, BuildArgs A, const int* ent_base, const int* top, int n_max,
+                                       int* n_ent) {
+  const size_t last = (size_t)A.n * A.n_points - 1;
+  const int tot = ent_base[last] + top[last];
+  *n_ent = min(tot, n_max);
+  if (tot > n_max)
+    for (int b = 0; b < A.n; ++b) set_err(F.meta + A.trees[b], ICB_ERR_CAP_SCRATCH);
+}
+
 __global__ void build_flags_kernel(const unsigned long long* keys, int n, int* flags) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
@@ -791,11 +802,11 @@ __global__ void build_flags_kernel(const unsigned long long* keys, int n, int* f
 }
 
 // gid = inclusive scan of flags; tree_ent0[b] = first entry of tree b
-__global__ void build_nodes_kernel(ForestView F, BuildArgs A, const unsigned long long* keys, int n_ent,
+__global__ void build_nodes_kernel(ForestView F, BuildArgs A, const unsigned long long* keys, const int* n_ent_dev,
                                    const int* gid, const int* tree_ent0, const int* top,
                                    const int* own_base_pos) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n_ent) return;
+  if (j >= *n_ent_dev) return;
   unsigned long long k = keys[j];
   int b = (int)(k >> 52);
   int lv = 63 - (int)((k >> 46) & 63);
@@ -1114,18 +1125,23 @@ int icb_build_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t n_poi
     if (!S.ok()) return S.fail();
     cub::DeviceScan::ExclusiveSum(d_tmp, tmp, top, ent_base, n * P, st);
   }
-  // total entries (needs host value for sizing)
-  int last_base = 0, last_top = 0;
-  ICB_CUDA(cudaMemcpyAsync(&last_base, ent_base + (size_t)n * P - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
-  ICB_CUDA(cudaMemcpyAsync(&last_top, top + (size_t)n * P - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
-  ICB_CUDA(cudaStreamSynchronize(st));
-  const int n_ent = last_base + last_top;
+  // Entries: arrays sized by a bound, the true count stays on the device (no
+  // host synchronisation: a build can overlap the caller's work).  Levels
+  // beyond the first are geometric(r): their sum concentrates far below twice
+  // its mean; a count above the bound sets ICB_ERR_CAP_SCRATCH.
+  const double rr = f->cfg.promotion_ratio;
+  const size_t np_ = (size_t)n * P;
+  const int n_ent = (int)std::min<double>(2.0e9, (double)np_ + std::ceil(2.0 * (double)np_ * rr / (1.0 - rr)) + 4096);
+  int* n_ent_dev = S.alloc<int>(1);
+  if (!S.ok()) return S.fail();
+  build_ent_total_kernel<<<1, 1, 0, st>>>(F, A, ent_base, top, n_ent, n_ent_dev);
   unsigned long long* keys_in = S.alloc<unsigned long long>(n_ent);
   unsigned long long* keys_out = S.alloc<unsigned long long>(n_ent);
   int* flags = S.alloc<int>(n_ent);
   int* gid = S.alloc<int>(n_ent);
   int* tree_ent0 = S.alloc<int>(n);
   if (!S.ok()) return S.fail();
+  ICB_CUDA(cudaMemsetAsync(keys_in, 0xff, sizeof(unsigned long long) * (size_t)n_ent, st));   // padding sorts last
   build_entries_kernel<<<g256, 256, 0, st>>>(F, A, top, parent_pos, own_base_pos, firstpos, ent_base, keys_in);
   {
     size_t tmp = 0;
@@ -1147,7 +1163,7 @@ int icb_build_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t n_poi
                              cudaMemcpyDeviceToDevice, st));
   // zero node sizes of the involved trees
   zero_node_sizes(f, trees, n, st);
-  build_nodes_kernel<<<(n_ent + 255) / 256, 256, 0, st>>>(F, A, keys_out, n_ent, gid, tree_ent0, top,
+  build_nodes_kernel<<<(n_ent + 255) / 256, 256, 0, st>>>(F, A, keys_out, n_ent_dev, gid, tree_ent0, top,
                                                           own_base_pos);
   build_tree_totals_kernel<<<(n + 127) / 128, 128, 0, st>>>(F, A, gid, tree_ent0, ent_cnt);
   // parents, leaf page counts
