@@ -1003,6 +1003,8 @@ __global__ void __launch_bounds__(256) build_summary_kernel(ForestView F, BuildA
 
 }  // namespace icb
 
+#include "nn_tc.cuh"
+
 // ---------------------------------------------------------------- host driver
 using namespace icb;
 
@@ -1059,24 +1061,76 @@ int icb_build_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t n_poi
   build_cand64_kernel<<<dim3((stride + 7) / 8, n), 256, 0, st>>>(F, A, nsq, cands, cand_off, cand64,
                                                                  cand_sq, stride);
   static const bool exact_only = getenv("ICB_BUILD_EXACT_NN") != nullptr;   // A/B and test knob
-  // The filter pays while most windows fit NF_CAP.  Candidate sets grow with
-  // the tree, and on clustered 128-d keys the windows overflow at 128k points
-  // (73%).  Measured C2-shaped builds: 32k points filter 0.24 s vs exact
-  // 0.75 s, 64k 0.81 vs 1.94 s, 128k 8.7 vs 7.1 s.
-  if (exact_only || F.dim + 1 > NF_K || P > 98304) {
-    const int D1 = F.dim + 1, PS = D1 | 1;
-    size_t sm = sizeof(double) * (NN_BM * PS + NN_BN * (NN_KC + 1));
-    ICB_CUDA(cudaFuncSetAttribute(nn_parent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    nn_parent_kernel<<<dim3((P + NN_BM - 1) / NN_BM, n), 256, sm, st>>>(
+  static const bool f16_filter = getenv("ICB_BUILD_F16_FILTER") != nullptr;  // round-1 filter, A/B
+  const int D1 = F.dim + 1, PS = D1 | 1;
+  const size_t psm = sizeof(double) * (NN_BM * PS + NN_BN * (NN_KC + 1));
+  // exact argmin of the listed candidates; points whose window overflowed
+  // NF_CAP: the brute-force tiled kernel, restricted to blocks that contain one
+  auto verify = [&](auto* list, const double* p64, int* nf_cnt) -> int {
+    using IdxT = typename std::remove_pointer<decltype(list)>::type;
+    unsigned long long* prof = nullptr;
+    if (getenv("ICB_PROF")) ICB_CUDA(cudaGetSymbolAddress((void**)&prof, g_build_prof));
+    const int nv_sm = (int)sizeof(double) * (4 * (ICB_DPAD + 1) + 4 * 2 * 32 * 33);
+    ICB_CUDA(cudaFuncSetAttribute(nn_verify_kernel<IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize, nv_sm));
+    nn_verify_kernel<IdxT><<<dim3((P + 3) / 4, n), 128, nv_sm, st>>>(
+        F, A, pts, pts_off, cands, cand_off, p64, cand64, cand_sq, stride, list, nf_cnt, parent_pos, prof);
+    ICB_CUDA(cudaFuncSetAttribute(nn_parent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
+    nn_parent_kernel<<<dim3((P + NN_BM - 1) / NN_BM, n), 256, psm, st>>>(
+        F, A, nsq, pts, pts_off, cands, cand_off, cand64, cand_sq, stride, parent_pos, nf_cnt, NF_CAP);
+    return ICB_OK;
+  };
+  if (exact_only || D1 > TC_KB || (f16_filter && (D1 > NF_K || P > 98304))) {
+    ICB_CUDA(cudaFuncSetAttribute(nn_parent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
+    nn_parent_kernel<<<dim3((P + NN_BM - 1) / NN_BM, n), 256, psm, st>>>(
         F, A, nsq, pts, pts_off, cands, cand_off, cand64, cand_sq, stride, parent_pos);
+  } else if (!f16_filter) {
+    // exact-integer tensor-core filter (tcgen05 kind::i8, nn_tc.cuh), any size
+    const size_t a_tiles = (size_t)(P + TC_M - 1) / TC_M;
+    const size_t b_tiles = (size_t)(stride + TC_N - 1) / TC_N + 64;   // + one partial tile per level
+    double* p64 = S.alloc<double>((size_t)n * P * (ICB_DPAD + 1));
+    signed char* aimg = S.alloc<signed char>((size_t)n * a_tiles * TC_ATILE);
+    signed char* bimg = S.alloc<signed char>((size_t)n * b_tiles * TC_BTILE);
+    double* pmeta = S.alloc<double>((size_t)n * P * 3);
+    float2* cmeta = S.alloc<float2>((size_t)n * b_tiles * TC_N);
+    unsigned long long* cmax = S.alloc<unsigned long long>((size_t)n * 2);
+    int* ct_off = S.alloc<int>((size_t)n * 64);
+    int* nf_cnt = S.alloc<int>((size_t)n * P);
+    if (!S.ok()) return S.fail();
+    ICB_CUDA(cudaMemsetAsync(aimg, 0, (size_t)n * a_tiles * TC_ATILE, st));
+    ICB_CUDA(cudaMemsetAsync(bimg, 0, (size_t)n * b_tiles * TC_BTILE, st));
+    ICB_CUDA(cudaMemsetAsync(cmeta, 0xff, sizeof(float2) * n * b_tiles * TC_N, st));   // NaN: padding never listed
+    ICB_CUDA(cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * n * 2, st));
+    tc_tile_offsets_kernel<<<n, 32, 0, st>>>(F, A, cand_off, ct_off);
+    tc_prep_points_kernel<<<dim3((P + 7) / 8, n), 256, 0, st>>>(F, A, nsq, pts, pts_off, p64, aimg, a_tiles,
+                                                               pmeta);
+    tc_prep_cands_kernel<<<dim3((stride + 7) / 8, n), 256, 0, st>>>(F, A, cand_off, ct_off, cand64, cand_sq,
+                                                                    stride, bimg, b_tiles, cmeta, cmax);
+    auto run = [&](auto* list) -> int {
+      using IdxT = typename std::remove_pointer<decltype(list)>::type;
+      const int sm = TC_ATILE + TC_STAGES * TC_BTILE + 1024;
+      ICB_CUDA(cudaFuncSetAttribute(nn_tc_filter_kernel<IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      nn_tc_filter_kernel<IdxT><<<dim3((unsigned)a_tiles, n), TC_THREADS, sm, st>>>(
+          F, A, pts_off, cand_off, ct_off, aimg, a_tiles, bimg, b_tiles, pmeta, cmeta, cmax, list, nf_cnt);
+      return verify(list, p64, nf_cnt);
+    };
+    int rc;
+    if (P <= 65536) {
+      unsigned short* l16 = S.alloc<unsigned short>((size_t)n * P * NF_CAP);
+      if (!S.ok()) return S.fail();
+      rc = run(l16);
+    } else {
+      int* l32 = S.alloc<int>((size_t)n * P * NF_CAP);
+      if (!S.ok()) return S.fail();
+      rc = run(l32);
+    }
+    if (rc != ICB_OK) return rc;
   } else {
+    // round-1 f16 filter (mma.sync), kept for A/B: ICB_BUILD_F16_FILTER=1
     double* p64 = S.alloc<double>((size_t)n * P * (ICB_DPAD + 1));
     __half* p16 = S.alloc<__half>((size_t)n * P * NF_K);
     __half* c16 = S.alloc<__half>((size_t)n * stride * NF_K);
     int* nf_cnt = S.alloc<int>((size_t)n * P);
     if (!S.ok()) return S.fail();
-    unsigned long long* prof = nullptr;
-    if (getenv("ICB_PROF")) ICB_CUDA(cudaGetSymbolAddress((void**)&prof, g_build_prof));
     nn_half_kernel<<<dim3((P + 7) / 8, n), 256, 0, st>>>(F, A, nsq, pts, pts_off, cand64, cand_off, stride, p64,
                                                          p16, c16);
     // candidate indices of a level are < P: 16-bit lists when they fit
@@ -1086,18 +1140,7 @@ int icb_build_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t n_poi
       ICB_CUDA(cudaFuncSetAttribute(nn_filter_kernel<IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       nn_filter_kernel<IdxT><<<dim3((P + NF_BM - 1) / NF_BM, n), 256, sm, st>>>(
           F, A, pts_off, cand_off, p16, c16, cand_sq, stride, list, nf_cnt);
-      const int nv_sm = (int)sizeof(double) * (4 * (ICB_DPAD + 1) + 4 * 2 * 32 * 33);
-      ICB_CUDA(cudaFuncSetAttribute(nn_verify_kernel<IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize, nv_sm));
-      nn_verify_kernel<IdxT><<<dim3((P + 3) / 4, n), 128, nv_sm, st>>>(
-          F, A, pts, pts_off, cands, cand_off, p64, cand64, cand_sq, stride, list, nf_cnt, parent_pos, prof);
-      // points whose window held more than NF_CAP candidates: the brute-force
-      // tiled kernel, restricted to blocks that contain one
-      const int D1 = F.dim + 1, PS = D1 | 1;
-      const size_t psm = sizeof(double) * (NN_BM * PS + NN_BN * (NN_KC + 1));
-      ICB_CUDA(cudaFuncSetAttribute(nn_parent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
-      nn_parent_kernel<<<dim3((P + NN_BM - 1) / NN_BM, n), 256, psm, st>>>(
-          F, A, nsq, pts, pts_off, cands, cand_off, cand64, cand_sq, stride, parent_pos, nf_cnt, NF_CAP);
-      return ICB_OK;
+      return verify(list, p64, nf_cnt);
     };
     int rc;
     if (P <= 65536) {
