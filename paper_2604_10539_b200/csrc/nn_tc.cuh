@@ -195,12 +195,38 @@ __device__ __forceinline__ void tc_commit(unsigned long long* bar) {
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_ld16(unsigned taddr, int (&v)[16]) {
+__device__ __forceinline__ void tc_ld16(unsigned taddr, unsigned (&v)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
         "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
+}
+__device__ __forceinline__ void tc_st16(unsigned taddr, unsigned v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+      "r"(v)
+      : "memory");
+}
+__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ unsigned long long pk2(unsigned lo, unsigned hi) {
+  return ((unsigned long long)hi << 32) | lo;
+}
+__device__ __forceinline__ unsigned long long fsub2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned long long fmul2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
 }
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
@@ -222,6 +248,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   __shared__ unsigned s_tmem;
   __shared__ TcSeg seg[TC_MAX_SEG];
   __shared__ int s_nseg;
+  __shared__ __align__(16) float s_cm[4][2 * 64];   // epilogue warps: (-2 u_c, |c|^2) of two tiles
   const int b = blockIdx.y;
   const int t = A.trees[b];
   const int L = F.meta[t].levels;
@@ -280,22 +307,22 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
         for (int k = 0; k < seg[sg].ntile; ++k, ++i) {
           const int s = i % TC_STAGES, a = i & 1;
           mbar_wait(&full_bar[s], (i / TC_STAGES) & 1);
-          if (i >= 2) mbar_wait(&tempty[a], ((i >> 1) - 1) & 1);
+          mbar_wait(&tempty[a], (i >> 1) & 1);   // phase 0: the epilogue's initialisation
           tc_fence_after();
           const unsigned b_hi = smem_u32(sB + s * TC_BTILE), b_lo = b_hi + TC_BDIG;
           const unsigned d = tmem + a * TC_ACC_COLS;
 #pragma unroll
           for (int ks = 0; ks < TC_KSTEPS; ++ks)
-            tc_mma(d, tc_desc(a_hi + ks * 256), tc_desc(b_hi + ks * 256), ks);
+            tc_mma(d, tc_desc(a_hi + ks * 256), tc_desc(b_hi + ks * 256), 1);
 #pragma unroll
           for (int ks = 0; ks < TC_KSTEPS; ++ks)
-            tc_mma(d + TC_N, tc_desc(a_hi + ks * 256), tc_desc(b_lo + ks * 256), ks);
+            tc_mma(d + TC_N, tc_desc(a_hi + ks * 256), tc_desc(b_lo + ks * 256), 1);
 #pragma unroll
           for (int ks = 0; ks < TC_KSTEPS; ++ks)
             tc_mma(d + TC_N, tc_desc(a_lo + ks * 256), tc_desc(b_hi + ks * 256), 1);
 #pragma unroll
           for (int ks = 0; ks < TC_KSTEPS; ++ks)
-            tc_mma(d + 2 * TC_N, tc_desc(a_lo + ks * 256), tc_desc(b_lo + ks * 256), ks);
+            tc_mma(d + 2 * TC_N, tc_desc(a_lo + ks * 256), tc_desc(b_lo + ks * 256), 1);
           tc_commit(&empty_bar[s]);
           tc_commit(&tfull[a]);
         }
@@ -316,7 +343,36 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       W = (float)(2.0 * E * (1.0 + 0x1p-20) + 0x1p-21);   // + fl(m + W) rounding (|m| <= 4)
     }
     const unsigned tl = tmem + ((unsigned)(q4 * 32) << 16);
+    // accumulators start at the bits of M = 1.5 * 2^23, so an int32 sum S
+    // (|S| < 2^22: dim + 1 <= 129 coordinates of digit products <= 32512)
+    // reads back as the float M + S, exactly: no int -> float conversions
+    const unsigned mb = 0x4B400000u;
+    auto init_stage = [&](int a) {
+#pragma unroll
+      for (int c = 0; c < TC_ACC_COLS; c += 16) tc_st16(tl + a * TC_ACC_COLS + c, mb);
+    };
+    init_stage(0);
+    init_stage(1);
+    tc_wait_st();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) { mbar_arrive(&tempty[0]); mbar_arrive(&tempty[1]); }
+    // per warp: the tile's 32 candidates as (-2 u_c, |c|^2) column pairs,
+    // staged from a coalesced register prefetch of the next tile
+    float* cbuf = reinterpret_cast<float*>(s_cm[warp - 2]);
     const float2* cm = cmeta + (size_t)b * b_tiles * TC_N;
+    int nsg = 0, nk = 0;   // next tile to prefetch
+    float2 pre = make_float2(0.f, 0.f);
+    auto prefetch = [&]() {
+      if (nsg < nseg) {
+        pre = cm[(size_t)(seg[nsg].tile0 + nk) * TC_N + lane];
+        if (++nk == seg[nsg].ntile) { ++nsg; nk = 0; }
+      }
+    };
+    prefetch();
+    const unsigned long long M2 = 0x4B4000004B400000ull, C256 = 0x4380000043800000ull,
+                             C64K = 0x4780000047800000ull;
+    const unsigned long long UP2 = pk2(__float_as_uint(up), __float_as_uint(up));
     IdxT* lst = list + ((size_t)b * A.n_points + e) * NF_CAP;
     int i = 0;
     for (int sg = 0; sg < nseg; ++sg) {
@@ -325,31 +381,51 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       int c = 0;
       for (int k = 0; k < seg[sg].ntile; ++k, ++i) {
         const int a = i & 1;
+        float* cb = cbuf + a * 64;
+        __syncwarp();
+        cb[(lane >> 1) * 4 + (lane & 1)] = -2.f * pre.x;        // NaN padding stays NaN
+        cb[(lane >> 1) * 4 + 2 + (lane & 1)] = pre.y;
+        __syncwarp();
+        prefetch();
         mbar_wait(&tfull[a], (i >> 1) & 1);
         tc_fence_after();
-        const float2* cmt = cm + (size_t)(seg[sg].tile0 + k) * TC_N;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          int s11[16], s12[16], s22[16];
+          unsigned s11[16], s12[16], s22[16];
           const unsigned col = tl + a * TC_ACC_COLS + h * 16;
           tc_ld16(col, s11);
           tc_ld16(col + TC_N, s12);
           tc_ld16(col + 2 * TC_N, s22);
           tc_wait_ld();
-          if (mine) {
+          float d2[16];
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              const float2 uc = cmt[h * 16 + q];
-              const float x = fmaf((float)s11[q], 65536.f, fmaf((float)s12[q], 256.f, (float)s22[q]));
-              const float d2 = fmaf(-2.f * (up * uc.x), x, uc.y);
-              if (d2 <= m + W) {
+          for (int q = 0; q < 16; q += 2) {
+            const unsigned long long a2 = fsub2(pk2(s11[q], s11[q + 1]), M2);
+            const unsigned long long b2 = fsub2(pk2(s12[q], s12[q + 1]), M2);
+            const unsigned long long c2 = fsub2(pk2(s22[q], s22[q + 1]), M2);
+            const unsigned long long x2 = fmul2(ffma2(a2, C64K, ffma2(b2, C256, c2)), UP2);
+            const float4 kc = *reinterpret_cast<const float4*>(cb + (h * 8 + (q >> 1)) * 4);
+            const unsigned long long r2 =
+                ffma2(pk2(__float_as_uint(kc.x), __float_as_uint(kc.y)), x2,
+                      pk2(__float_as_uint(kc.z), __float_as_uint(kc.w)));
+            d2[q] = __uint_as_float((unsigned)r2);
+            d2[q + 1] = __uint_as_float((unsigned)(r2 >> 32));
+          }
+          float mn = d2[0];
+#pragma unroll
+          for (int q = 1; q < 16; ++q) mn = fminf(mn, d2[q]);
+          m = fminf(m, mn);
+          if (mine && mn <= m + W) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (d2[q] <= m + W) {
                 if (c < NF_CAP) lst[c] = (IdxT)(k * TC_N + h * 16 + q);
                 ++c;
               }
-              m = fminf(m, d2);
-            }
           }
         }
+        init_stage(a);
+        tc_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[a]);

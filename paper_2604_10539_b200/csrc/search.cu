@@ -245,7 +245,8 @@ using namespace icb;
 // Phase cycle counters of the search (enabled by ICB_PROF=1; debug tool, not
 // in the public header): out[0..kPhases) = loop, union, scan + row list,
 // lift + start, stream, P-DCI + counters, selection, final top-k + pages,
-// fused attention; out[kPhases..kPhases + 8) = selection statistics.
+// fused attention; out[kPhases..kPhases + 8) = selection statistics;
+// out[kPhases + 8..kPhases + 24) = row-list statistics and sub-phase cycles (g_scan_stats).
 extern "C" int icb_search_cta_profile(unsigned long long* cycles, int* sm, int n, int reset) {
   ICB_CUDA(cudaDeviceSynchronize());
   ICB_CUDA(cudaMemcpyFromSymbol(cycles, g_cta_cycles, sizeof(unsigned long long) * n));
@@ -261,10 +262,12 @@ extern "C" int icb_search_profile(unsigned long long* out, int reset) {
   ICB_CUDA(cudaDeviceSynchronize());
   ICB_CUDA(cudaMemcpyFromSymbol(out, g_search_prof, sizeof(unsigned long long) * kPhases));
   ICB_CUDA(cudaMemcpyFromSymbol(out + kPhases, g_topb_stats, sizeof(unsigned long long) * 8));
+  ICB_CUDA(cudaMemcpyFromSymbol(out + kPhases + 8, g_scan_stats, sizeof(unsigned long long) * 16));
   if (reset) {
-    unsigned long long z[kPhases + 8] = {};
+    unsigned long long z[16] = {};
     ICB_CUDA(cudaMemcpyToSymbol(g_search_prof, z, sizeof(unsigned long long) * kPhases));
     ICB_CUDA(cudaMemcpyToSymbol(g_topb_stats, z, sizeof(unsigned long long) * 8));
+    ICB_CUDA(cudaMemcpyToSymbol(g_scan_stats, z, sizeof(unsigned long long) * 16));
   }
   return ICB_OK;
 }

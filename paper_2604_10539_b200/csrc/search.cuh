@@ -575,6 +575,16 @@ __device__ unsigned long long group_threshold(GroupSmem& GS, int gtid, int bar, 
 // selection statistics (per translation unit; the query kernel's are
 // reported by icb_search_profile): selections, radix fallbacks, boundary sizes
 static __device__ unsigned long long g_topb_stats[8];
+// ICB_PROF: level iterations, union nodes, rows, row-list passes, binary-search passes, start levels
+static __device__ unsigned long long g_scan_stats[16];
+#define ICB_SUB(k)                                                              \
+  do {                                                                          \
+    if (P.prof && threadIdx.x == 0) {                                           \
+      long long n_ = clock64();                                                 \
+      atomicAdd(&g_scan_stats[k], (unsigned long long)(n_ - tsub_));            \
+      tsub_ = n_;                                                               \
+    }                                                                           \
+  } while (0)
 
 template <int GP>
 struct TopB {
@@ -1127,8 +1137,10 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
   const bool oskip = S.oskip;
 
   long long tmark_ = clock64();
+  long long tsub_ = 0;
   for (int lv = start; lv >= floor; --lv) {
     ICB_MARK(0);
+    if (P.prof && threadIdx.x == 0) tsub_ = clock64();
     // (1) union of the nodes requested by the heads' survivors
     if (lv == start) {
       if (tid == 0) { SS.ulist[0] = F.meta[t].top_node; SS.umask[0] = (int)allmask; S.U = 1; }
@@ -1177,10 +1189,16 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
         for (int u = 0; u < UU; ++u) x[u] = gg[u] >= 0 ? F.own_base[F.tk(t, x[u])] : 0;
 #pragma unroll
         for (int u = 0; u < UU; ++u) x[u] = gg[u] >= 0 ? ownl[x[u] + lv - 1] : 0;
+        // all UU mark atomics in flight before any result is used
+        unsigned prev[UU];
 #pragma unroll
         for (int u = 0; u < UU; ++u) {
           ICB_CHECK(gg[u] < 0 || (x[u] >= 0 && x[u] < F.node_cap), "own(.., %d) = %d", lv, x[u]);
-          const bool fresh = gg[u] >= 0 && atomicOr(SS.nmask + x[u], 1u << gg[u]) == 0u;
+          prev[u] = gg[u] >= 0 ? atomicOr(SS.nmask + x[u], 1u << gg[u]) : 1u;
+        }
+#pragma unroll
+        for (int u = 0; u < UU; ++u) {
+          const bool fresh = prev[u] == 0u;
           // one smem atomic per warp for the new nodes' list slots
           const unsigned bal = __ballot_sync(0xffffffffu, fresh);
           int at = 0;
@@ -1189,6 +1207,7 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
           if (fresh) SS.ulist[at + __popc(bal & ((1u << lane) - 1))] = x[u];
         }
       }
+      ICB_SUB(8);
       if (oskip) {   // one shared atomic per head per warp (redux over the warp first)
 #pragma unroll
         for (int h = 0; h < GP; ++h) {
@@ -1198,8 +1217,10 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
         }
       }
       __syncthreads();
+      ICB_SUB(9);
       for (int i = tid; i < S.U; i += NT) SS.umask[i] = (int)SS.nmask[SS.ulist[i]];
       __syncthreads();
+      ICB_SUB(10);
     }
     const int U = S.U;
     ICB_MARK(1);
@@ -1292,6 +1313,7 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
       block_scan_multi<NT, GP + 1>(v, ex, tot, S.wsum2);
       const int r0p = S.scan_carry[GP];          // rows before this pass
       const bool direct = tot[GP] <= kRowNodeCap;
+      if (P.prof && tid == 0) { atomicAdd(&g_scan_stats[3], 1ull); if (!direct) atomicAdd(&g_scan_stats[4], 1ull); }
       int run[GP + 1];
 #pragma unroll
       for (int g = 0; g <= GP; ++g) run[g] = S.scan_carry[g] + ex[g];
@@ -1314,6 +1336,7 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
         run[GP] += s;
       }
       __syncthreads();
+      ICB_SUB(11);
       // the pass's rows in parallel: row r belongs to the last node whose
       // prefix is <= r (binary search over the staged prefixes; nodes without
       // rows share their successor's prefix and are never chosen)
@@ -1365,8 +1388,15 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
     __syncthreads();
     for (int g = 0; g < G; ++g)
       if (S.M[g] > SS.ccap) { if (tid == 0) set_err(F.meta + t, ICB_ERR_CAP_SCRATCH); return; }
+    ICB_SUB(12);
     ICB_MARK(2);
     const int R = S.misc[6];
+    if (P.prof && tid == 0) {
+      atomicAdd(&g_scan_stats[0], 1ull);
+      atomicAdd(&g_scan_stats[1], (unsigned long long)U);
+      atomicAdd(&g_scan_stats[2], (unsigned long long)R);
+      if (lv == start) atomicAdd(&g_scan_stats[5], 1ull);
+    }
     // (3b) stream the rows through shared memory.  Every warp owns a private
     //      kSub-slot ring (two batches of 8 rows): it issues the async copies
     //      (cp.async, one 512-byte row per instruction) of its batch after

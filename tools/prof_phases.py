@@ -20,7 +20,7 @@ st = clustered_stream(ctx, 40, 32, 8, 4, 128, 128, device="cuda")
 eng = Engine(EngineConfig(**C2, kv_dtype="bf16", max_tokens=ctx + 64)).prefill(st.keys, st.values, ctx)
 lib = N.lib()
 lib.icb_search_profile.argtypes = [ctypes.c_void_p, ctypes.c_int]
-buf = np.zeros(17, dtype=np.uint64)
+buf = np.zeros(33, dtype=np.uint64)
 for i in range(4):
     eng.decode_step(ctx + i, st.queries[i], st.keys[ctx + i], st.values[ctx + i], metrics=False)
 lib.icb_search_profile(buf.ctypes.data_as(ctypes.c_void_p), 1)
@@ -31,6 +31,13 @@ names = ["loop", "union", "scan+rowlist", "lift+start", "stream", "pdci+ctr", "s
 print('top-B selections', buf[9], 'radix fallbacks', buf[10], 'avg boundary bin', buf[11] / max(1, buf[9]))
 ns = max(1, buf[9])
 print('top-B us per selection: hist %.2f scan %.2f emit %.2f sort+tail %.2f' % tuple(buf[12 + i] / ns / 1.9e3 for i in range(4)))
+sc = buf[17:33]
+lv_it = max(1, sc[0])
+print('row lists: level iterations %d (start levels %d) | union nodes %.0f rows %.0f passes %.2f binary-search passes %.2f per level' % (
+    sc[0], sc[5], sc[1] / lv_it, sc[2] / lv_it, sc[3] / lv_it, sc[4] / lv_it))
+nq = 8 * eng.T
+print('sub-phases us per CTA-query: union loop %.1f | sync %.1f | umask %.1f | scan nodes+stage %.1f | rows %.1f' % tuple(
+    sc[8 + i] / nq / 1.9e3 for i in range(5)))
 buf = buf[:9]
 tot = buf.sum()
 per_cta_us = buf / (8 * eng.T) / 1.9e3

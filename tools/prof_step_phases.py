@@ -23,7 +23,7 @@ eng = Engine(EngineConfig(**C2, kv_dtype="bf16", max_tokens=ctx + steps + 1)).pr
 lib = N.lib()
 lib.icb_search_profile.argtypes = [ctypes.c_void_p, ctypes.c_int]
 names = ["loop", "union", "scan+rowlist", "lift+start", "stream", "pdci+ctr", "select", "final+pages", "attention"]
-buf = np.zeros(17, dtype=np.uint64)
+buf = np.zeros(25, dtype=np.uint64)
 for i in range(steps):
     rot = eng.rotation_due()
     lib.icb_search_profile(buf.ctypes.data_as(ctypes.c_void_p), 1)
