@@ -1138,6 +1138,14 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
 
   long long tmark_ = clock64();
   long long tsub_ = 0;
+  // union marks: kMarkBits per node (one bit per head) in the row ring, which
+  // is idle between the selection and the row list; global marks when the
+  // forest's node capacity does not fit
+  constexpr unsigned kMarkBits = GP <= 4 ? 4u : 8u;
+  constexpr int kMarkPerWord = 32 / (int)kMarkBits;
+  constexpr unsigned kMarkMask = (1u << kMarkBits) - 1u;
+  unsigned* rmark = reinterpret_cast<unsigned*>(RG.ring);
+  const bool smark = (long long)F.node_cap <= (long long)kRing * ICB_ROWF * 4 / 4 * kMarkPerWord;
   for (int lv = start; lv >= floor; --lv) {
     ICB_MARK(0);
     if (P.prof && threadIdx.x == 0) tsub_ = clock64();
@@ -1148,6 +1156,8 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
     } else {
       if (tid == 0) S.U = 0;
       if (tid < GP) { GSA[tid].lo = 0xffffffffu; GSA[tid].hi = 0u; }
+      if (smark)
+        for (int i = tid; i < (F.node_cap + kMarkPerWord - 1) / kMarkPerWord; i += NT) rmark[i] = 0u;
       __syncthreads();
       // every (head, survivor) pair in parallel: independent own() lookups
       int pre[GP + 1];
@@ -1194,7 +1204,12 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
 #pragma unroll
         for (int u = 0; u < UU; ++u) {
           ICB_CHECK(gg[u] < 0 || (x[u] >= 0 && x[u] < F.node_cap), "own(.., %d) = %d", lv, x[u]);
-          prev[u] = gg[u] >= 0 ? atomicOr(SS.nmask + x[u], 1u << gg[u]) : 1u;
+          if (smark) {
+            const unsigned sh = (unsigned)(x[u] % kMarkPerWord) * kMarkBits;
+            prev[u] = gg[u] >= 0 ? (atomicOr(rmark + x[u] / kMarkPerWord, (1u << gg[u]) << sh) >> sh) & kMarkMask : 1u;
+          } else {
+            prev[u] = gg[u] >= 0 ? atomicOr(SS.nmask + x[u], 1u << gg[u]) : 1u;
+          }
         }
 #pragma unroll
         for (int u = 0; u < UU; ++u) {
@@ -1218,7 +1233,11 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
       }
       __syncthreads();
       ICB_SUB(9);
-      for (int i = tid; i < S.U; i += NT) SS.umask[i] = (int)SS.nmask[SS.ulist[i]];
+      for (int i = tid; i < S.U; i += NT) {
+        const int x = SS.ulist[i];
+        SS.umask[i] = smark ? (int)((rmark[x / kMarkPerWord] >> ((x % kMarkPerWord) * kMarkBits)) & kMarkMask)
+                            : (int)SS.nmask[x];
+      }
       __syncthreads();
       ICB_SUB(10);
     }
@@ -1658,7 +1677,7 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
       atomicAdd(&F.meta[t].rows_read, (unsigned long long)S.misc[5]);
       if (lv < start && !oskip) atomicAdd(&F.meta[t].owner_rereads, (unsigned long long)U);
     }
-    if (lv < start)
+    if (lv < start && !smark)
       for (int i = tid; i < U; i += NT) SS.nmask[SS.ulist[i]] = 0u;
     __syncthreads();
     ICB_MARK(5);
