@@ -833,6 +833,7 @@ __global__ void build_nodes_kernel(ForestView F, BuildArgs A, const unsigned lon
     F.node_owner[F.nd(t, node)] = tok;
     F.node_opos[F.nd(t, node)] = local;   // absolute here; made node-relative by build_summary_kernel
     F.own_list[(size_t)t * F.own_cap + own_base_pos[(size_t)b * A.n_points + pos] + lv - 1] = node;
+    if (lv == 1) F.own1[F.tk(t, tok)] = node;
   }
   // node size: count members
   atomicAdd(F.node_size + F.nd(t, node), 1);

@@ -160,6 +160,7 @@ int icb_forest_create(const icb_forest_config* cfg, icb_forest** out) {
   AL(F.own_base, T * c.tok_cap, 0);
   AL(F.tok2page, T * c.tok_cap, 0xff);
   AL(F.own_list, T * c.own_cap, 0);
+  AL(F.own1, T * c.tok_cap, 0);
   AL(F.node_level, T * c.node_cap, 0);
   AL(F.node_parent, T * c.node_cap, 0);
   AL(F.node_owner, T * c.node_cap, 0);

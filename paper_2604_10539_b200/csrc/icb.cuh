@@ -104,6 +104,7 @@ struct ForestView {
   int* own_base;      // [T][tok_cap]  own(p, lv) = own_list[own_base[p] + lv - 1]
   int* tok2page;      // [T][tok_cap]
   int* own_list;      // [T][own_cap]
+  int* own1;          // [T][tok_cap]  own(p, 1) for points of top >= 2 (the search's union fast path)
   int* node_level;    // [T][node_cap]
   int* node_parent;
   int* node_owner;

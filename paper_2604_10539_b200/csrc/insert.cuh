@@ -129,6 +129,7 @@ __device__ inline void add_member(const ForestView& F, int t, int node, int tok)
 
 __device__ __forceinline__ void set_own(const ForestView& F, int t, int tok, int lv, int node) {
   F.own_list[(size_t)t * F.own_cap + F.own_base[F.tk(t, tok)] + lv - 1] = node;
+  if (lv == 1) F.own1[F.tk(t, tok)] = node;
 }
 
 // KV offload: the HBM pool row mirroring page `page` row `slot` when the page

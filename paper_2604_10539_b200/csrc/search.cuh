@@ -1196,9 +1196,15 @@ __device__ void tree_search(SearchSmem& S, GroupSmem* GSA, const RingView& RG, c
           }
         }
 #pragma unroll
-        for (int u = 0; u < UU; ++u) x[u] = gg[u] >= 0 ? F.own_base[F.tk(t, x[u])] : 0;
+        if (lv == 1) {   // one lookup: own(p, 1) is kept per token
 #pragma unroll
-        for (int u = 0; u < UU; ++u) x[u] = gg[u] >= 0 ? ownl[x[u] + lv - 1] : 0;
+          for (int u = 0; u < UU; ++u) x[u] = gg[u] >= 0 ? F.own1[F.tk(t, x[u])] : 0;
+        } else {
+#pragma unroll
+          for (int u = 0; u < UU; ++u) x[u] = gg[u] >= 0 ? F.own_base[F.tk(t, x[u])] : 0;
+#pragma unroll
+          for (int u = 0; u < UU; ++u) x[u] = gg[u] >= 0 ? ownl[x[u] + lv - 1] : 0;
+        }
         // all UU mark atomics in flight before any result is used
         unsigned prev[UU];
 #pragma unroll
