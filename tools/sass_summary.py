@@ -9,7 +9,7 @@ import sys
 
 lib = sys.argv[1] if len(sys.argv) > 1 else "paper_2604_10539_b200/libicecache_b200.so"
 sass = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
-CLASSES = ["UTCHMMA", "UTCQMMA", "UTCMMA", "LDTM", "STTM", "HMMA", "UTMALDG", "UBLKCP", "LDGSTS", "SYNCS",
+CLASSES = ["UTCHMMA", "UTCIMMA", "UTCQMMA", "UTCMMA", "LDTM", "STTM", "HMMA", "UTMALDG", "UBLKCP", "LDGSTS", "SYNCS",
            "LDSM", "DFMA", "FFMA2", "FFMA", "SHFL", "REDUX"]
 cur = None
 counts = collections.OrderedDict()
