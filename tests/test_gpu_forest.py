@@ -86,14 +86,23 @@ def _filter_case(kind, n, d, rng):
         return rng.standard_normal(d)[None, :] + 1e-5 * rng.standard_normal((n, d))
     if kind == "tiny_norms":      # coordinates in f16's subnormal range
         return rng.standard_normal((n, d)) * 10.0 ** rng.uniform(-6, 0, (n, 1))
+    if kind == "spiky":           # one dominant coordinate: coarse int8 digits for all the others
+        x = 1e-3 * rng.standard_normal((n, d))
+        x[np.arange(n), rng.integers(0, d, n)] += rng.choice([-1.0, 1.0], n) * rng.uniform(0.5, 1.0, n)
+        return x
+    if kind == "near_ties_spiky":  # near-ties whose rows also quantise coarsely
+        base = np.zeros(d)
+        base[3] = 1.0
+        return base[None, :] + 1e-4 * rng.standard_normal((n, d))
     return rng.standard_normal((n, d)) + 3.0 * rng.standard_normal((8, d))[rng.integers(0, 8, n)]
 
 
 @pytest.mark.parametrize("kind,r", [("duplicates", 0.1), ("near_ties", 0.1), ("tiny_norms", 0.1),
-                                    ("clustered", 0.3)])
+                                    ("clustered", 0.3), ("spiky", 0.1), ("near_ties_spiky", 0.1)])
 def test_build_parent_filter_edge_cases(cuda_ok, kind, r):
-    """The tensor-core parent filter (build.cu nn_filter_kernel) must pick the
-    exact fp64 1-NN parent, first index on ties, on inputs built to defeat it."""
+    """The tensor-core parent filter (nn_tc.cuh nn_tc_filter_kernel) must pick
+    the exact fp64 1-NN parent, first index on ties, on inputs built to defeat
+    it (exact ties, near-ties, tiny and spiky coordinates)."""
     n, d = 3000, 128
     rng = np.random.default_rng(hash(kind) % 2**32)
     keys = _filter_case(kind, n, d, rng).astype(np.float32)
