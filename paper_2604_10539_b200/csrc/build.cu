@@ -1086,10 +1086,10 @@ int icb_build_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t n_poi
         F, A, nsq, pts, pts_off, cands, cand_off, cand64, cand_sq, stride, parent_pos);
   } else if (!f16_filter) {
     // exact-integer tensor-core filter (tcgen05 kind::i8, nn_tc.cuh), any size
-    const size_t a_tiles = (size_t)(P + TC_M - 1) / TC_M;
+    const size_t a_rows = (size_t)(P + TC_M - 1) / TC_M * TC_M;
     const size_t b_tiles = (size_t)(stride + TC_N - 1) / TC_N + 64;   // + one partial tile per level
     double* p64 = S.alloc<double>((size_t)n * P * (ICB_DPAD + 1));
-    signed char* aimg = S.alloc<signed char>((size_t)n * a_tiles * TC_ATILE);
+    signed char* aimg = S.alloc<signed char>((size_t)n * a_rows * TC_AROW);
     signed char* bimg = S.alloc<signed char>((size_t)n * b_tiles * TC_BTILE);
     double* pmeta = S.alloc<double>((size_t)n * P * 3);
     float2* cmeta = S.alloc<float2>((size_t)n * b_tiles * TC_N);
@@ -1097,21 +1097,22 @@ int icb_build_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t n_poi
     int* ct_off = S.alloc<int>((size_t)n * 64);
     int* nf_cnt = S.alloc<int>((size_t)n * P);
     if (!S.ok()) return S.fail();
-    ICB_CUDA(cudaMemsetAsync(aimg, 0, (size_t)n * a_tiles * TC_ATILE, st));
+    ICB_CUDA(cudaMemsetAsync(aimg, 0, (size_t)n * a_rows * TC_AROW, st));
     ICB_CUDA(cudaMemsetAsync(bimg, 0, (size_t)n * b_tiles * TC_BTILE, st));
     ICB_CUDA(cudaMemsetAsync(cmeta, 0xff, sizeof(float2) * n * b_tiles * TC_N, st));   // NaN: padding never listed
     ICB_CUDA(cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * n * 2, st));
+    ICB_CUDA(cudaMemsetAsync(nf_cnt, 0, sizeof(int) * n * P, st));   // window hits are counted atomically
     tc_tile_offsets_kernel<<<n, 32, 0, st>>>(F, A, cand_off, ct_off);
-    tc_prep_points_kernel<<<dim3((P + 7) / 8, n), 256, 0, st>>>(F, A, nsq, pts, pts_off, p64, aimg, a_tiles,
+    tc_prep_points_kernel<<<dim3((P + 7) / 8, n), 256, 0, st>>>(F, A, nsq, pts, pts_off, p64, aimg, a_rows,
                                                                pmeta);
     tc_prep_cands_kernel<<<dim3((stride + 7) / 8, n), 256, 0, st>>>(F, A, cand_off, ct_off, cand64, cand_sq,
                                                                     stride, bimg, b_tiles, cmeta, cmax);
     auto run = [&](auto* list) -> int {
       using IdxT = typename std::remove_pointer<decltype(list)>::type;
-      const int sm = TC_ATILE + TC_STAGES * TC_BTILE + 1024;
+      const int sm = TC_STAGES * TC_BTILE + 1024;
       ICB_CUDA(cudaFuncSetAttribute(nn_tc_filter_kernel<IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-      nn_tc_filter_kernel<IdxT><<<dim3((unsigned)a_tiles, n), TC_THREADS, sm, st>>>(
-          F, A, pts_off, cand_off, ct_off, aimg, a_tiles, bimg, b_tiles, pmeta, cmeta, cmax, list, nf_cnt);
+      nn_tc_filter_kernel<IdxT><<<dim3((unsigned)(a_rows / TC_M), n), TC_THREADS, sm, st>>>(
+          F, A, pts_off, cand_off, ct_off, aimg, a_rows, bimg, b_tiles, pmeta, cmeta, cmax, list, nf_cnt);
       return verify(list, p64, nf_cnt);
     };
     int rc;

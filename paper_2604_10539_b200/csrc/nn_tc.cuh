@@ -27,35 +27,41 @@
 // f16 filter (whose windows overflow at 128k points).
 //
 // Tiles.  A CTA owns 128 consecutive point entries (the M = 128 rows of the
-// MMA = the 128 TMEM lanes) and streams the candidate tiles of their level(s),
-// 32 candidates per tile (N = 32), K = 160 bytes per digit (5 MMA k-steps of
-// 32).  Operands are stored in global memory already in the canonical
-// no-swizzle K-major UMMA layout (8-row x 16-byte core matrices; LBO = 128 B
-// between the two core matrices of a k-step, SBO = 1280 B between 8-row
-// groups), so one 1-D bulk copy moves a tile.  Warp roles: warp 0 bulk copies
-// (4-stage ring), warp 1 issues the 20 MMAs of a tile (one thread) into one of
-// two accumulator stages (3 x 32 TMEM columns each), warps 2-5 drain TMEM
-// (tcgen05.ld, each warp its 32-lane quarter) and run the window test.
+// MMA = the 128 TMEM lanes); their digits sit in TMEM as the MMAs' A operand
+// (80 columns, loaded once), so shared memory only carries the candidates.
+// It streams the candidate tiles of the rows' level(s), 64 candidates per
+// tile (N = 64), K = 160 bytes per digit (5 MMA k-steps of 32).  Candidate
+// tiles are stored in global memory already in the canonical no-swizzle
+// K-major UMMA layout (8-row x 16-byte core matrices; LBO = 128 B between the
+// two core matrices of a k-step, SBO = 1280 B between 8-row groups), so one
+// 1-D bulk copy moves a tile.  Warp roles (one CTA per SM): warp 0 bulk
+// copies (6-stage ring), warp 1 issues the 20 MMAs of a tile (one thread)
+// into one of two accumulator stages (3 x 64 TMEM columns each), warps 2-9
+// drain TMEM (tcgen05.ld; two warps per 32-lane quarter, 32 columns each) and
+// run the window test.
 #pragma once
 
 namespace icb {
 
 constexpr int TC_M = 128;                    // point rows per CTA = TMEM lanes
-constexpr int TC_N = 32;                     // candidates per tile (MMA N)
+constexpr int TC_N = 64;                     // candidates per tile (MMA N)
 constexpr int TC_KB = 160;                   // int8 coordinates per digit row (dim + 1 <= 129, padded)
 constexpr int TC_KSTEPS = TC_KB / 32;        // MMA k-steps per digit pair
 constexpr int TC_SBO = (TC_KB / 16) * 128;   // bytes between 8-row core-matrix groups
-constexpr int TC_ADIG = TC_M * TC_KB;        // one digit plane of a point tile
+constexpr int TC_AROW = 2 * TC_KB;           // one point row: both digit planes, row-major (TMEM A operand)
 constexpr int TC_BDIG = TC_N * TC_KB;        // one digit plane of a candidate tile
-constexpr int TC_ATILE = 2 * TC_ADIG;        // 40 KB
-constexpr int TC_BTILE = 2 * TC_BDIG;        // 10 KB
-constexpr int TC_STAGES = 4;
-constexpr int TC_THREADS = 192;
+constexpr int TC_BTILE = 2 * TC_BDIG;        // 20 KB
+constexpr int TC_STAGES = 6;
+constexpr int TC_EPI_WARPS = 8;              // two per TMEM lane quarter, 32 columns each
+constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
 constexpr int TC_QMAX = 32639;               // |X| <= 127 * 256 + 127
+constexpr int TC_A_COLS = TC_KB / 4 * 2;     // A digits in TMEM: 4 int8 per 32-bit column, two planes
+constexpr int TC_ACC0 = 128;                 // first accumulator column
 constexpr int TC_ACC_COLS = 3 * TC_N;        // S11, S12, S22
-constexpr int TC_TMEM_COLS = 256;            // two accumulator stages (192 used); two CTAs per SM
+constexpr int TC_TMEM_COLS = 512;            // A (80) + two accumulator stages (384); one CTA per SM
 constexpr float TC_ERND = 3.814697265625e-06f;   // 2^-18
 constexpr int TC_MAX_SEG = 64;
+static_assert(TC_A_COLS <= TC_ACC0 && TC_ACC0 + 2 * TC_ACC_COLS <= TC_TMEM_COLS, "TMEM budget");
 
 // byte offset of (row r, coordinate k) inside one digit plane
 __device__ __forceinline__ int tc_off(int r, int k) {
@@ -66,7 +72,7 @@ __device__ __forceinline__ int tc_off(int r, int k) {
 // Returns (on every lane) u, e = max |x - u X| and the L1 norms of x~ and x.
 __device__ __forceinline__ void tc_quant_row(const double* x, int D1, int lane, signed char* hi_plane,
                                              signed char* lo_plane, int r, double& u, double& err, double& l1q,
-                                             double& l1x) {
+                                             double& l1x, bool umma_layout = true) {
   double v[TC_KB / 32];
   double s = 0.0;
 #pragma unroll
@@ -93,8 +99,9 @@ __device__ __forceinline__ void tc_quant_row(const double* x, int D1, int lane, 
     a2 += fabs(v[q]);
     const int lo = ((X + 128) & 255) - 128;
     const int hi = (X - lo) >> 8;
-    hi_plane[tc_off(r, i)] = (signed char)hi;
-    lo_plane[tc_off(r, i)] = (signed char)lo;
+    const int o = umma_layout ? tc_off(r, i) : i;
+    hi_plane[o] = (signed char)hi;
+    lo_plane[o] = (signed char)lo;
   }
   for (int o = 16; o; o >>= 1) {
     e = fmax(e, __shfl_xor_sync(0xffffffffu, e, o));
@@ -119,10 +126,10 @@ __global__ void tc_tile_offsets_kernel(ForestView F, BuildArgs A, const int* can
   }
 }
 
-// point rows: the fp64 lifted row (for the verify kernel) and its digits in the
-// CTA tile image; pmeta[e] = (u, e, L1 of x~)
+// point rows: the fp64 lifted row (for the verify kernel) and its digits,
+// row-major (the filter copies them into TMEM); pmeta[e] = (u, e, L1 of x~)
 __global__ void tc_prep_points_kernel(ForestView F, BuildArgs A, const double* nsq, const int* pts,
-                                      const int* pts_off, double* p64, signed char* aimg, size_t a_tiles,
+                                      const int* pts_off, double* p64, signed char* aimg, size_t a_rows,
                                       double* pmeta) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.y;
@@ -134,9 +141,9 @@ __global__ void tc_prep_points_kernel(ForestView F, BuildArgs A, const double* n
   double* row = p64 + ((size_t)b * A.n_points + r) * (ICB_DPAD + 1);
   lift64_row(F, A, b, pts[(size_t)b * A.n_points + r], F.meta[t].c, nsq, row, lane, 32);
   __syncwarp();
-  signed char* tile = aimg + ((size_t)b * a_tiles + r / TC_M) * TC_ATILE;
+  signed char* arow = aimg + ((size_t)b * a_rows + r) * TC_AROW;
   double u, e, l1q, l1x;
-  tc_quant_row(row, F.dim + 1, lane, tile, tile + TC_ADIG, r % TC_M, u, e, l1q, l1x);
+  tc_quant_row(row, F.dim + 1, lane, arow, arow + TC_KB, 0, u, e, l1q, l1x, false);
   if (lane == 0) {
     double* m = pmeta + ((size_t)b * A.n_points + r) * 3;
     m[0] = u; m[1] = e; m[2] = l1q;
@@ -183,11 +190,17 @@ __device__ __forceinline__ unsigned long long tc_desc(unsigned saddr) {
 constexpr unsigned TC_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(TC_N >> 3) << 17) |
                               ((unsigned)(TC_M >> 4) << 24);
 
-__device__ __forceinline__ void tc_mma(unsigned tmem_d, unsigned long long da, unsigned long long db, int acc) {
+// D[tmem] += A[tmem] . B[smem]^T (A: 128 lanes x 32 int8 in 8 columns)
+__device__ __forceinline__ void tc_mma_ts(unsigned tmem_d, unsigned tmem_a, unsigned long long db) {
   asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(TC_IDESC), "r"(acc));
+      "{\n.reg .pred p;\nsetp.eq.u32 p, 1, 1;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(TC_IDESC));
+}
+__device__ __forceinline__ void tc_st8(unsigned taddr, const uint4& a, const uint4& b) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(a.x),
+               "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
 }
 __device__ __forceinline__ void tc_commit(unsigned long long* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -235,20 +248,20 @@ struct TcSeg {
 };
 
 template <typename IdxT>
-__global__ void __launch_bounds__(TC_THREADS, 2)
+__global__ void __launch_bounds__(TC_THREADS, 1)
     nn_tc_filter_kernel(ForestView F, BuildArgs A, const int* pts_off, const int* cand_off, const int* ct_off,
-                        const signed char* aimg, size_t a_tiles, const signed char* bimg, size_t b_tiles,
+                        const signed char* aimg, size_t a_rows, const signed char* bimg, size_t b_tiles,
                         const double* pmeta, const float2* cmeta, const unsigned long long* cmax, IdxT* list,
                         int* cnt) {
   extern __shared__ __align__(1024) unsigned char tc_raw[];
-  unsigned char* sm = (unsigned char*)(((size_t)tc_raw + 1023) & ~(size_t)1023);
-  unsigned char* sA = sm;
-  unsigned char* sB = sm + TC_ATILE;
-  __shared__ __align__(8) unsigned long long full_bar[TC_STAGES], empty_bar[TC_STAGES], tfull[2], tempty[2], abar;
+  unsigned char* sB = (unsigned char*)(((size_t)tc_raw + 1023) & ~(size_t)1023);
+  __shared__ __align__(8) unsigned long long full_bar[TC_STAGES], empty_bar[TC_STAGES], tfull[2], tempty[2];
   __shared__ unsigned s_tmem;
   __shared__ TcSeg seg[TC_MAX_SEG];
   __shared__ int s_nseg;
-  __shared__ __align__(16) float s_cm[4][2 * 64];   // epilogue warps: (-2 u_c, |c|^2) of two tiles
+  __shared__ __align__(16) float s_cm[TC_EPI_WARPS][2 * 64];   // per epilogue warp: (-2 u_c, |c|^2) of two tiles
+  __shared__ int s_cnt[TC_M];          // window hits per row (both halves)
+  __shared__ float s_min[2][TC_M];     // running minimum per row and half
   const int b = blockIdx.y;
   const int t = A.trees[b];
   const int L = F.meta[t].levels;
@@ -269,9 +282,13 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     }
     s_nseg = ns;
     for (int s = 0; s < TC_STAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
-    mbar_init(&abar, 1);
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], TC_EPI_WARPS); }
     mbar_fence_init();
+  }
+  if (threadIdx.x < TC_M) {
+    s_cnt[threadIdx.x] = 0;
+    s_min[0][threadIdx.x] = INFINITY;
+    s_min[1][threadIdx.x] = INFINITY;
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
@@ -287,8 +304,6 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(&abar, TC_ATILE);
-      bulk_g2s(sA, aimg + ((size_t)b * a_tiles + blockIdx.x) * TC_ATILE, TC_ATILE, &abar);
       int i = 0;
       for (int sg = 0; sg < nseg; ++sg)
         for (int k = 0; k < seg[sg].ntile; ++k, ++i) {
@@ -300,36 +315,31 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      mbar_wait(&abar, 0);
-      const unsigned a_hi = smem_u32(sA), a_lo = a_hi + TC_ADIG;
       int i = 0;
       for (int sg = 0; sg < nseg; ++sg)
         for (int k = 0; k < seg[sg].ntile; ++k, ++i) {
           const int s = i % TC_STAGES, a = i & 1;
           mbar_wait(&full_bar[s], (i / TC_STAGES) & 1);
-          mbar_wait(&tempty[a], (i >> 1) & 1);   // phase 0: the epilogue's initialisation
+          mbar_wait(&tempty[a], (i >> 1) & 1);   // phase 0: the epilogue's initialisation (and A in TMEM)
           tc_fence_after();
           const unsigned b_hi = smem_u32(sB + s * TC_BTILE), b_lo = b_hi + TC_BDIG;
-          const unsigned d = tmem + a * TC_ACC_COLS;
+          const unsigned d = tmem + TC_ACC0 + a * TC_ACC_COLS;
+          const unsigned a_hi = tmem, a_lo = tmem + TC_A_COLS / 2;
 #pragma unroll
-          for (int ks = 0; ks < TC_KSTEPS; ++ks)
-            tc_mma(d, tc_desc(a_hi + ks * 256), tc_desc(b_hi + ks * 256), 1);
+          for (int ks = 0; ks < TC_KSTEPS; ++ks) tc_mma_ts(d, a_hi + ks * 8, tc_desc(b_hi + ks * 256));
 #pragma unroll
-          for (int ks = 0; ks < TC_KSTEPS; ++ks)
-            tc_mma(d + TC_N, tc_desc(a_hi + ks * 256), tc_desc(b_lo + ks * 256), 1);
+          for (int ks = 0; ks < TC_KSTEPS; ++ks) tc_mma_ts(d + TC_N, a_hi + ks * 8, tc_desc(b_lo + ks * 256));
 #pragma unroll
-          for (int ks = 0; ks < TC_KSTEPS; ++ks)
-            tc_mma(d + TC_N, tc_desc(a_lo + ks * 256), tc_desc(b_hi + ks * 256), 1);
+          for (int ks = 0; ks < TC_KSTEPS; ++ks) tc_mma_ts(d + TC_N, a_lo + ks * 8, tc_desc(b_hi + ks * 256));
 #pragma unroll
-          for (int ks = 0; ks < TC_KSTEPS; ++ks)
-            tc_mma(d + 2 * TC_N, tc_desc(a_lo + ks * 256), tc_desc(b_lo + ks * 256), 1);
+          for (int ks = 0; ks < TC_KSTEPS; ++ks) tc_mma_ts(d + 2 * TC_N, a_lo + ks * 8, tc_desc(b_lo + ks * 256));
           tc_commit(&empty_bar[s]);
           tc_commit(&tfull[a]);
         }
     }
   } else {
-    // epilogue: warp w drains TMEM lanes 32 (w % 4) .. +31
-    const int q4 = warp & 3;
+    // epilogue: warp w drains TMEM lanes 32 (w % 4) .. +31, columns half * 32 .. +31 of each accumulator
+    const int q4 = warp & 3, half = (warp - 2) >> 2, ew = warp - 2;
     const int row = q4 * 32 + lane;
     const int e = e0 + row;
     const bool valid = e < e1;
@@ -343,13 +353,26 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       W = (float)(2.0 * E * (1.0 + 0x1p-20) + 0x1p-21);   // + fl(m + W) rounding (|m| <= 4)
     }
     const unsigned tl = tmem + ((unsigned)(q4 * 32) << 16);
+    if (half == 0) {
+      // the point rows' digits into TMEM (the MMAs' A operand): row e -> lane,
+      // 4 int8 per column, hi plane then lo plane
+      const uint4* src = reinterpret_cast<const uint4*>(aimg + ((size_t)b * a_rows + e) * TC_AROW);
+#pragma unroll
+      for (int c = 0; c < TC_A_COLS / 8; ++c) {
+        uint4 x = make_uint4(0, 0, 0, 0), y = make_uint4(0, 0, 0, 0);
+        if (valid) { x = src[2 * c]; y = src[2 * c + 1]; }
+        tc_st8(tl + c * 8, x, y);
+      }
+    }
     // accumulators start at the bits of M = 1.5 * 2^23, so an int32 sum S
     // (|S| < 2^22: dim + 1 <= 129 coordinates of digit products <= 32512)
     // reads back as the float M + S, exactly: no int -> float conversions
     const unsigned mb = 0x4B400000u;
     auto init_stage = [&](int a) {
 #pragma unroll
-      for (int c = 0; c < TC_ACC_COLS; c += 16) tc_st16(tl + a * TC_ACC_COLS + c, mb);
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) tc_st16(tl + TC_ACC0 + a * TC_ACC_COLS + c * TC_N + half * 32 + h * 16, mb);
     };
     init_stage(0);
     init_stage(1);
@@ -357,10 +380,10 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     tc_fence_before();
     __syncwarp();
     if (lane == 0) { mbar_arrive(&tempty[0]); mbar_arrive(&tempty[1]); }
-    // per warp: the tile's 32 candidates as (-2 u_c, |c|^2) column pairs,
+    // per warp: its 32 candidates of the tile as (-2 u_c, |c|^2) column pairs,
     // staged from a coalesced register prefetch of the next tile
-    float* cbuf = reinterpret_cast<float*>(s_cm[warp - 2]);
-    const float2* cm = cmeta + (size_t)b * b_tiles * TC_N;
+    float* cbuf = s_cm[ew];
+    const float2* cm = cmeta + (size_t)b * b_tiles * TC_N + half * 32;
     int nsg = 0, nk = 0;   // next tile to prefetch
     float2 pre = make_float2(0.f, 0.f);
     auto prefetch = [&]() {
@@ -377,8 +400,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     int i = 0;
     for (int sg = 0; sg < nseg; ++sg) {
       const bool mine = valid && e >= seg[sg].e_begin && e < seg[sg].e_end;
-      float m = INFINITY;
-      int c = 0;
+      float m = INFINITY;   // this half's running minimum (>= the row's)
       for (int k = 0; k < seg[sg].ntile; ++k, ++i) {
         const int a = i & 1;
         float* cb = cbuf + a * 64;
@@ -392,7 +414,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           unsigned s11[16], s12[16], s22[16];
-          const unsigned col = tl + a * TC_ACC_COLS + h * 16;
+          const unsigned col = tl + TC_ACC0 + a * TC_ACC_COLS + half * 32 + h * 16;
           tc_ld16(col, s11);
           tc_ld16(col + TC_N, s12);
           tc_ld16(col + 2 * TC_N, s22);
@@ -418,9 +440,9 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
           if (mine && mn <= m + W) {
 #pragma unroll
             for (int q = 0; q < 16; ++q)
-              if (d2[q] <= m + W) {
-                if (c < NF_CAP) lst[c] = (IdxT)(k * TC_N + h * 16 + q);
-                ++c;
+              if (d2[q] <= m + W) {   // both halves of the row list into it: one shared counter
+                const int slot = atomicAdd(&s_cnt[row], 1);
+                if (slot < NF_CAP) lst[slot] = (IdxT)(k * TC_N + half * 32 + h * 16 + q);
               }
           }
         }
@@ -429,9 +451,17 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[a]);
+        // the row's two halves share their running minima (a tighter window)
+        // (any value read is a minimum over candidates already seen: >= the final one)
+        if (mine) {
+          s_min[half][row] = m;
+          m = fminf(m, s_min[half ^ 1][row]);
+        }
       }
-      if (mine) cnt[(size_t)b * A.n_points + e] = c;
     }
+    // every epilogue warp is done with its rows: publish the hit counts
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * TC_EPI_WARPS) : "memory");
+    if (half == 0 && valid) cnt[(size_t)b * A.n_points + e] = s_cnt[row];
   }
   tc_fence_before();
   __syncthreads();
