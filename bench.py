@@ -630,6 +630,10 @@ def main():
             print(json.dumps(run_reference(args)), flush=True)
         return
     if world > 1:
+        # NCCL's init lines (nranks, NVLS / P2P transport) go to the log, so a
+        # scaling run shows every rank joined the communicator
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch
         dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
         torch.cuda.set_device(dev)

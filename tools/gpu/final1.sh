@@ -6,8 +6,10 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')
 for cfg in "32768 bf16 c2" "131072 bf16 c3" "32768 fp32 c2fp32"; do
   set -- $cfg
   timeout 600 python tools/prof_query.py $1 $2 > $O/pq_$3.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:query_kernel -s 6 -c 1 -o $O/prof_query_$3 -f python tools/prof_query.py $1 $2 > $O/ncu_$3.log 2>&1 && \
-  python tools/ncu_traffic.py $O/prof_query_$3.ncu-rep ctx$1_$2_s1 "ncu --set full, query_kernel (tools/prof_query.py $1 $2), profiles/r02_query_kernel_$3_ncu_summary.json" >> $O/traffic.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:query_kernel -s 6 -c 1 -o /tmp/prof_query_$3 -f python tools/prof_query.py $1 $2 > $O/ncu_$3.log 2>&1 && \
+  python tools/ncu_summary.py /tmp/prof_query_$3.ncu-rep query_kernel $O/r02_query_kernel_$3_ncu_summary.json > /dev/null 2>&1; \
+  python tools/ncu_lines.py /tmp/prof_query_$3.ncu-rep 40 > $O/lines_$3.txt 2>&1; \
+  python tools/ncu_traffic.py /tmp/prof_query_$3.ncu-rep ctx$1_$2_s1 "ncu --set full, query_kernel (tools/prof_query.py $1 $2), profiles/r02_query_kernel_$3_ncu_summary.json" >> $O/traffic.log 2>&1
 done
 cp profiles/search_traffic.json $O/search_traffic.json
 timeout 900 python bench.py > $O/b_default.log 2>&1; echo "rc=$?" >> $O/b_default.log
