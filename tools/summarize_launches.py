@@ -5,6 +5,7 @@ import csv
 import sys
 
 src, dst = sys.argv[1], sys.argv[2]
+cmd = sys.argv[3] if len(sys.argv) > 3 else None
 rows = list(csv.reader(open(src)))
 hdr = None
 agg = collections.defaultdict(list)
@@ -12,8 +13,11 @@ for r in rows:
     if "Kernel Name" in r:
         hdr = r
         ki, vi, ui = r.index("Kernel Name"), r.index("Metric Value"), r.index("Metric Unit")
+        mi = r.index("Metric Name") if "Metric Name" in r else None
         continue
     if hdr and len(r) > vi:
+        if mi is not None and r[mi] != "gpu__time_duration.sum":
+            continue
         try:
             val = float(r[vi].replace(",", ""))
         except ValueError:
@@ -23,6 +27,8 @@ for r in rows:
 tot = sum(sum(v) for v in agg.values())
 with open(dst, "w") as fh:
     fh.write(f"# ncu launch list summary ({src})\n\n")
+    if cmd:
+        fh.write(f"Command: `{cmd}`\n\n")
     fh.write("Cold-cache, serialized per-launch device times (compare shares, not absolutes).\n\n")
     fh.write("| share | launches | mean us | kernel |\n|---:|---:|---:|---|\n")
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
