@@ -502,8 +502,10 @@ __global__ void __launch_bounds__(128) nn_verify_kernel(ForestView F, BuildArgs 
                                                         const double* p64, const double* cand64,
                                                         const double* cand_sq, int stride, const IdxT* list,
                                                         const int* cnt, int* parent_pos,
-                                                        unsigned long long* prof) {
+                                                        unsigned long long* prof, const float* list_d2 = nullptr,
+                                                        const float* thr = nullptr) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ int s_keep[4][NF_CAP];   // the listed candidates inside the final window (list_d2 given)
   const int b = blockIdx.y;
   const int t = A.trees[b];
   const int L = F.meta[t].levels;
@@ -527,9 +529,27 @@ __global__ void __launch_bounds__(128) nn_verify_kernel(ForestView F, BuildArgs 
   const int nc = cand_off[(size_t)b * 64 + lv + 1] - c0;
   const int c = cnt[(size_t)b * A.n_points + e];
   const bool all = c > NF_CAP;   // overflowed windows: nn_parent_kernel's shared tiles do those points
-  const int m = all ? 0 : c;
+  int m = all ? 0 : c;
   const double* c64base = cand64 + ((size_t)b * stride + c0) * (ICB_DPAD + 1);
   const IdxT* lst = list + ((size_t)b * A.n_points + e) * NF_CAP;
+  // The tensor-core filter lists against a running minimum; with its d2~ per
+  // entry and the row's final threshold, only the entries inside the final
+  // window need the exact chain (the argmin and its ties are among them).
+  const bool pruned = list_d2 != nullptr && !all;
+  if (pruned) {
+    const float th = thr[(size_t)b * A.n_points + e];
+    const float* ld = list_d2 + ((size_t)b * A.n_points + e) * NF_CAP;
+    int mm = 0;
+    for (int i0 = 0; i0 < m; i0 += 32) {
+      const int i = i0 + lane;
+      const bool keep = i < m && ld[i] <= th;
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) s_keep[warp][mm + __popc(bal & ((1u << lane) - 1))] = (int)lst[i];
+      mm += __popc(bal);
+    }
+    __syncwarp();
+    m = mm;
+  }
   if (prof && lane == 0) {
     atomicAdd(prof + 0, 1ull);
     atomicAdd(prof + 1, (unsigned long long)m);
@@ -543,7 +563,7 @@ __global__ void __launch_bounds__(128) nn_verify_kernel(ForestView F, BuildArgs 
   const int steps = ((m + 31) >> 5) * nch;
   auto cand = [&](int rd) -> int {
     const int i = rd * 32 + lane;
-    return i < m ? (all ? i : (int)lst[i]) : 0;
+    return i < m ? (all ? i : pruned ? s_keep[warp][i] : (int)lst[i]) : 0;
   };
   auto issue = [&](int st) {
     const int rd = st / nch, u0 = (st - rd * nch) * 32;
@@ -1067,14 +1087,16 @@ int icb_build_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t n_poi
   const size_t psm = sizeof(double) * (NN_BM * PS + NN_BN * (NN_KC + 1));
   // exact argmin of the listed candidates; points whose window overflowed
   // NF_CAP: the brute-force tiled kernel, restricted to blocks that contain one
-  auto verify = [&](auto* list, const double* p64, int* nf_cnt) -> int {
+  auto verify = [&](auto* list, const double* p64, int* nf_cnt, const float* list_d2 = nullptr,
+                    const float* thr = nullptr) -> int {
     using IdxT = typename std::remove_pointer<decltype(list)>::type;
     unsigned long long* prof = nullptr;
     if (getenv("ICB_PROF")) ICB_CUDA(cudaGetSymbolAddress((void**)&prof, g_build_prof));
     const int nv_sm = (int)sizeof(double) * (4 * (ICB_DPAD + 1) + 4 * 2 * 32 * 33);
     ICB_CUDA(cudaFuncSetAttribute(nn_verify_kernel<IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize, nv_sm));
     nn_verify_kernel<IdxT><<<dim3((P + 3) / 4, n), 128, nv_sm, st>>>(
-        F, A, pts, pts_off, cands, cand_off, p64, cand64, cand_sq, stride, list, nf_cnt, parent_pos, prof);
+        F, A, pts, pts_off, cands, cand_off, p64, cand64, cand_sq, stride, list, nf_cnt, parent_pos, prof, list_d2,
+        thr);
     ICB_CUDA(cudaFuncSetAttribute(nn_parent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
     nn_parent_kernel<<<dim3((P + NN_BM - 1) / NN_BM, n), 256, psm, st>>>(
         F, A, nsq, pts, pts_off, cands, cand_off, cand64, cand_sq, stride, parent_pos, nf_cnt, NF_CAP);
@@ -1096,6 +1118,8 @@ int icb_build_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t n_poi
     unsigned long long* cmax = S.alloc<unsigned long long>((size_t)n * 2);
     int* ct_off = S.alloc<int>((size_t)n * 64);
     int* nf_cnt = S.alloc<int>((size_t)n * P);
+    float* nf_d2 = S.alloc<float>((size_t)n * P * NF_CAP);   // d2~ of each listed candidate
+    float* nf_thr = S.alloc<float>((size_t)n * P);           // each row's final window threshold
     if (!S.ok()) return S.fail();
     ICB_CUDA(cudaMemsetAsync(aimg, 0, (size_t)n * a_rows * TC_AROW, st));
     ICB_CUDA(cudaMemsetAsync(bimg, 0, (size_t)n * b_tiles * TC_BTILE, st));
@@ -1112,8 +1136,9 @@ int icb_build_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t n_poi
       const int sm = TC_STAGES * TC_BTILE + 1024;
       ICB_CUDA(cudaFuncSetAttribute(nn_tc_filter_kernel<IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       nn_tc_filter_kernel<IdxT><<<dim3((unsigned)(a_rows / TC_M), n), TC_THREADS, sm, st>>>(
-          F, A, pts_off, cand_off, ct_off, aimg, a_rows, bimg, b_tiles, pmeta, cmeta, cmax, list, nf_cnt);
-      return verify(list, p64, nf_cnt);
+          F, A, pts_off, cand_off, ct_off, aimg, a_rows, bimg, b_tiles, pmeta, cmeta, cmax, list, nf_cnt, nf_d2,
+          nf_thr);
+      return verify(list, p64, nf_cnt, nf_d2, nf_thr);
     };
     int rc;
     if (P <= 65536) {

@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     nn_tc_filter_kernel(ForestView F, BuildArgs A, const int* pts_off, const int* cand_off, const int* ct_off,
                         const signed char* aimg, size_t a_rows, const signed char* bimg, size_t b_tiles,
                         const double* pmeta, const float2* cmeta, const unsigned long long* cmax, IdxT* list,
-                        int* cnt) {
+                        int* cnt, float* list_d2, float* thr) {
   extern __shared__ __align__(1024) unsigned char tc_raw[];
   unsigned char* sB = (unsigned char*)(((size_t)tc_raw + 1023) & ~(size_t)1023);
   __shared__ __align__(8) unsigned long long full_bar[TC_STAGES], empty_bar[TC_STAGES], tfull[2], tempty[2];
@@ -397,6 +397,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                              C64K = 0x4780000047800000ull;
     const unsigned long long UP2 = pk2(__float_as_uint(up), __float_as_uint(up));
     IdxT* lst = list + ((size_t)b * A.n_points + e) * NF_CAP;
+    float* ld2 = list_d2 + ((size_t)b * A.n_points + e) * NF_CAP;
     int i = 0;
     for (int sg = 0; sg < nseg; ++sg) {
       const bool mine = valid && e >= seg[sg].e_begin && e < seg[sg].e_end;
@@ -442,7 +443,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             for (int q = 0; q < 16; ++q)
               if (d2[q] <= m + W) {   // both halves of the row list into it: one shared counter
                 const int slot = atomicAdd(&s_cnt[row], 1);
-                if (slot < NF_CAP) lst[slot] = (IdxT)(k * TC_N + half * 32 + h * 16 + q);
+                if (slot < NF_CAP) {
+                  lst[slot] = (IdxT)(k * TC_N + half * 32 + h * 16 + q);
+                  ld2[slot] = d2[q];
+                }
               }
           }
         }
@@ -461,7 +465,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     // every epilogue warp is done with its rows: publish the hit counts
     asm volatile("bar.sync 1, %0;" ::"n"(32 * TC_EPI_WARPS) : "memory");
-    if (half == 0 && valid) cnt[(size_t)b * A.n_points + e] = s_cnt[row];
+    if (half == 0 && valid) {
+      cnt[(size_t)b * A.n_points + e] = s_cnt[row];
+      // the row's final window: the verify kernel skips listed entries above it
+      thr[(size_t)b * A.n_points + e] = fminf(s_min[0][row], s_min[1][row]) + W;
+    }
   }
   tc_fence_before();
   __syncthreads();
