@@ -493,11 +493,14 @@ struct NfSmem {
   int cnt[NF_BM];                  // window hits per row
 };
 
+constexpr int NV_W = 8;   // verify: warps (points) per CTA
+constexpr int NV_R = 8;   // verify: candidates per round (the windows hold ~2 after pruning)
+
 // One warp per point entry: the exact fp64 d2 of nn_parent_kernel over the
 // point's window hits (all of its level's candidates when the window held more
 // than NF_CAP), first index on ties.  The point row is broadcast from smem.
 template <typename IdxT>
-__global__ void __launch_bounds__(128) nn_verify_kernel(ForestView F, BuildArgs A, const int* pts,
+__global__ void __launch_bounds__(NV_W * 32) nn_verify_kernel(ForestView F, BuildArgs A, const int* pts,
                                                         const int* pts_off, const int* cands, const int* cand_off,
                                                         const double* p64, const double* cand64,
                                                         const double* cand_sq, int stride, const IdxT* list,
@@ -505,21 +508,21 @@ __global__ void __launch_bounds__(128) nn_verify_kernel(ForestView F, BuildArgs 
                                                         unsigned long long* prof, const float* list_d2 = nullptr,
                                                         const float* thr = nullptr) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __shared__ int s_keep[4][NF_CAP];   // the listed candidates inside the final window (list_d2 given)
+  __shared__ int s_keep[NV_W][NF_CAP];   // the listed candidates inside the final window (list_d2 given)
   const int b = blockIdx.y;
   const int t = A.trees[b];
   const int L = F.meta[t].levels;
   if (L < 2) return;
-  const int e = blockIdx.x * 4 + warp;
+  const int e = blockIdx.x * NV_W + warp;
   const int npts = pts_off[(size_t)b * 64 + L];
   if (e >= npts) return;
-  // per warp: the point row (broadcast) and two 32-candidate x 32-coordinate
+  // per warp: the point row (broadcast) and two NV_R-candidate x 32-coordinate
   // chunks of candidate rows (cp.async double buffer over the flattened
-  // (round of 32 candidates, coordinate chunk) sequence); every lane runs one
+  // (round of NV_R candidates, coordinate chunk) sequence); every lane runs one
   // candidate's sequential chain through the chunks, acc in its register
   extern __shared__ double nv_smem[];
   double* p = nv_smem + warp * (ICB_DPAD + 1);
-  double (*T)[32][33] = reinterpret_cast<double (*)[32][33]>(nv_smem + 4 * (ICB_DPAD + 1)) + warp * 2;
+  double (*T)[NV_R][33] = reinterpret_cast<double (*)[NV_R][33]>(nv_smem + NV_W * (ICB_DPAD + 1)) + warp * 2;
   const int D1 = F.dim + 1;
   const double* src = p64 + ((size_t)b * A.n_points + e) * (ICB_DPAD + 1);
   for (int u = lane; u < D1; u += 32) p[u] = src[u];
@@ -560,14 +563,14 @@ __global__ void __launch_bounds__(128) nn_verify_kernel(ForestView F, BuildArgs 
   // chunks of 32 coordinates; a final remainder of 1 joins the last chunk (33 wide)
   const int nch = D1 > 32 && D1 % 32 == 1 ? D1 >> 5 : (D1 + 31) >> 5;
   auto chunk_w = [&](int ch) { return ch == nch - 1 ? D1 - ch * 32 : 32; };
-  const int steps = ((m + 31) >> 5) * nch;
+  const int steps = (m + NV_R - 1) / NV_R * nch;
   auto cand = [&](int rd) -> int {
-    const int i = rd * 32 + lane;
-    return i < m ? (all ? i : pruned ? s_keep[warp][i] : (int)lst[i]) : 0;
+    const int i = rd * NV_R + lane;
+    return lane < NV_R && i < m ? (all ? i : pruned ? s_keep[warp][i] : (int)lst[i]) : 0;
   };
   auto issue = [&](int st) {
     const int rd = st / nch, u0 = (st - rd * nch) * 32;
-    const int nr = min(32, m - rd * 32), un = chunk_w(st - rd * nch);
+    const int nr = min(NV_R, m - rd * NV_R), un = chunk_w(st - rd * nch);
     const int jl = cand(rd);
     double (*B)[33] = T[st & 1];
     for (int r = 0; r < nr; ++r) {
@@ -592,7 +595,7 @@ __global__ void __launch_bounds__(128) nn_verify_kernel(ForestView F, BuildArgs 
     }
     __syncwarp();
     const int rd = st / nch, ch = st - rd * nch, u0 = ch * 32;
-    const int nr = min(32, m - rd * 32), un = chunk_w(ch);
+    const int nr = min(NV_R, m - rd * NV_R), un = chunk_w(ch);
     if (ch == 0) { acc = 0.0; jr = cand(rd); }
     const double (*B)[33] = T[st & 1];
     if (lane < nr) {
@@ -1092,9 +1095,9 @@ int icb_build_impl(icb_forest* f, const int32_t* trees, int32_t n, int32_t n_poi
     using IdxT = typename std::remove_pointer<decltype(list)>::type;
     unsigned long long* prof = nullptr;
     if (getenv("ICB_PROF")) ICB_CUDA(cudaGetSymbolAddress((void**)&prof, g_build_prof));
-    const int nv_sm = (int)sizeof(double) * (4 * (ICB_DPAD + 1) + 4 * 2 * 32 * 33);
+    const int nv_sm = (int)sizeof(double) * (NV_W * (ICB_DPAD + 1) + NV_W * 2 * NV_R * 33);
     ICB_CUDA(cudaFuncSetAttribute(nn_verify_kernel<IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize, nv_sm));
-    nn_verify_kernel<IdxT><<<dim3((P + 3) / 4, n), 128, nv_sm, st>>>(
+    nn_verify_kernel<IdxT><<<dim3((P + NV_W - 1) / NV_W, n), NV_W * 32, nv_sm, st>>>(
         F, A, pts, pts_off, cands, cand_off, p64, cand64, cand_sq, stride, list, nf_cnt, parent_pos, prof, list_d2,
         thr);
     ICB_CUDA(cudaFuncSetAttribute(nn_parent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
