@@ -475,7 +475,8 @@ __global__ void __launch_bounds__(NT) node_query_kernel(ForestView F, int t, int
 }  // namespace icb
 
 namespace icb {
-// Warm the P-DCI caches of freshly built trees (one CTA per tree): directions
+// Warm the P-DCI caches of freshly built trees (kWarmSplit CTAs per tree, each
+// taking every kWarmSplit-th chunk of 2048 nodes): directions
 // and ladder entries of every node the decode path visits with P-DCI --
 // levels >= 2 above 64 members (insert parent searches, visit cap 64) and
 // leaves above the query visit cap -- so no later search pays for them.
@@ -489,8 +490,8 @@ __global__ void __launch_bounds__(NT) pdci_warm_kernel(ForestView F, const int32
   if (threadIdx.x == 0) S.sortbuf = reinterpret_cast<unsigned long long*>(RG.ring);
   const int t = trees[blockIdx.x];
   const int nn = F.meta[t].n_nodes;
-  double* tmp = tmp_dirs + (size_t)blockIdx.x * ICB_NPROJ * (F.dim + 1);
-  for (int base = 0; base < nn; base += 512 * 4) {
+  double* tmp = tmp_dirs + ((size_t)blockIdx.x * gridDim.y + blockIdx.y) * ICB_NPROJ * (F.dim + 1);
+  for (int base = blockIdx.y * 512 * 4; base < nn; base += gridDim.y * 512 * 4) {
     if (threadIdx.x == 0) s_n = 0;
     __syncthreads();
     for (int node = base + threadIdx.x; node < min(nn, base + 512 * 4); node += NT) {
@@ -518,12 +519,13 @@ __global__ void __launch_bounds__(NT) pdci_warm_kernel(ForestView F, const int32
 int icb_pdci_warm_impl(icb_forest* f, const int32_t* trees, int32_t n, int64_t qcap, cudaStream_t st) {
   if (n <= 0) return ICB_OK;
   Scratch S(st);
-  double* tmp = S.alloc<double>((size_t)n * ICB_NPROJ * (f->view.dim + 1));
+  constexpr int kWarmSplit = 8;
+  double* tmp = S.alloc<double>((size_t)n * kWarmSplit * ICB_NPROJ * (f->view.dim + 1));
   if (!S.ok()) return S.fail();
   const size_t dsm = search_dsm_bytes(1);
   ICB_CUDA(cudaFuncSetAttribute(pdci_warm_kernel<kSearchThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)dsm));
-  pdci_warm_kernel<kSearchThreads><<<n, kSearchThreads, dsm, st>>>(f->view, trees, qcap, tmp);
+  pdci_warm_kernel<kSearchThreads><<<dim3(n, kWarmSplit), kSearchThreads, dsm, st>>>(f->view, trees, qcap, tmp);
   return S.finish();
 }
 

@@ -805,8 +805,16 @@ __device__ int pc_ensure(SearchSmem& S, const ForestView& F, int t, int node, in
     if (off < 0 || F.node_pccap[x] < m) {
       const int want = max(m + (m >> 1), 128);
       TreeMeta* mt = F.meta + t;
-      off = mt->pc_top + want <= F.pc_cap ? mt->pc_top : -1;
-      if (off >= 0) { mt->pc_top += want; F.node_pc[x] = off; F.node_pccap[x] = want; }
+      // bump allocation that never overshoots the arena (several CTAs may warm
+      // one tree's nodes concurrently, pdci_warm_kernel)
+      int cur = *(volatile int*)&mt->pc_top;
+      off = -1;
+      while (cur + want <= F.pc_cap) {
+        const int prev = atomicCAS(&mt->pc_top, cur, cur + want);
+        if (prev == cur) { off = cur; break; }
+        cur = prev;
+      }
+      if (off >= 0) { F.node_pc[x] = off; F.node_pccap[x] = want; }
     }
     s_off = off;
   }
